@@ -1,0 +1,548 @@
+#!/usr/bin/env python3
+"""CGBN forward+backward benchmark (BASELINE.json metric, configs[1]).
+
+Workload ("resnet50_bn_b32"): every BatchNorm layer of ResNet-50 (53 layers, C=64..2048,
+224x224 input) at batch 32 per GPU, fp32 NCHW. One step = the CGBN forward of all 53
+layers followed by their CGBN backward in reverse order — per layer: stats kernel ->
+statistics exchange over the BN group (= all N GPUs, NCCL all-gather; identity at N=1)
+-> normalise (+running-stat update) kernel; backward reduce kernel -> exchange -> dx
+kernel. Weak scaling: every GPU holds its own batch of 32.
+
+metric value = algorithmic bytes (32 B per fp32 activation element: fwd 12, bwd 20,
+SURVEY.md §8d) of the whole job / device time per step, max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cgbn|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CGBN fwd+bwd algorithmic GB/s (whole job; per-GPU and % HBM roofline in extra keys)"
+UNIT = "GB/s"
+BYTES_PER_ELEM = 32  # fwd 12 + bwd 20
+
+
+def resnet50_bn_shapes(batch=32):
+    """The 53 BN layers of torchvision ResNet-50 (v1.5: stride on conv2) at 224x224."""
+    shapes = [(batch, 64, 112, 112)]  # stem bn1
+    cfg = [(64, 256, 3, 56, 56), (128, 512, 4, 56, 28), (256, 1024, 6, 28, 14),
+           (512, 2048, 3, 14, 7)]
+    for width, out, blocks, in_hw, hw in cfg:
+        for b in range(blocks):
+            h1 = in_hw if b == 0 else hw
+            shapes.append((batch, width, h1, h1))   # bn1 (after 1x1 conv, input res)
+            shapes.append((batch, width, hw, hw))   # bn2 (after strided 3x3)
+            shapes.append((batch, out, hw, hw))     # bn3
+            if b == 0:
+                shapes.append((batch, out, hw, hw))  # downsample bn
+    return shapes
+
+
+def numel(s):
+    n = 1
+    for e in s:
+        n *= e
+    return n
+
+
+# ----------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"cgbn_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------------
+# reference arm / CPU baseline (the reference's own CPU implementation)
+
+def _reference_module():
+    """The UNMODIFIED reference (bigbatch) installed in baseline/_ref, else None."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "bigbatch")):
+        sys.path.insert(0, ref_dir)
+        try:
+            import bigbatch  # noqa: F401
+            return bigbatch
+        except Exception:  # noqa: BLE001
+            return None
+    return None
+
+
+def reference_step(bb, shape, ranks, seed):
+    """One CGBN fwd+bwd of one layer through the reference's stock path:
+    DeviceGroup(ranks).run with sync_bn_forward + sync_bn_backward (f64, its default).
+    Returns (seconds, algorithmic bytes)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    xs = [rng.standard_normal(shape).astype(np.float32).astype(np.float64) for _ in range(ranks)]
+    dys = [rng.standard_normal(shape).astype(np.float32).astype(np.float64) for _ in range(ranks)]
+    c = shape[1]
+    gamma = rng.uniform(0.5, 1.5, c)
+    beta = rng.standard_normal(c)
+    t_in = [bb.Tensor(x) for x in xs]
+    d_in = [bb.Tensor(d) for d in dys]
+
+    def worker(h):
+        st = bb.BNLayerState(gamma=gamma.copy(), beta=beta.copy())
+        _, cache = bb.sync_bn_forward(h, t_in[h.rank], st)
+        bb.sync_bn_backward(h, d_in[h.rank], cache, st)
+
+    g = bb.DeviceGroup(ranks)
+    t0 = time.perf_counter()
+    g.run(worker)
+    return time.perf_counter() - t0, BYTES_PER_ELEM * numel(shape) * ranks
+
+
+def port_step(shape, ranks, seed):
+    """Fallback when baseline/_ref is absent: the oracle port (oracle/cgbn_oracle.py)."""
+    import numpy as np
+    from oracle import cgbn_oracle as O
+    rng = np.random.default_rng(seed)
+    xs = [rng.standard_normal(shape).astype(np.float32).astype(np.float64) for _ in range(ranks)]
+    dys = [rng.standard_normal(shape).astype(np.float32).astype(np.float64) for _ in range(ranks)]
+    c = shape[1]
+    t0 = time.perf_counter()
+    O.cgbn_world(xs, rng.uniform(0.5, 1.5, c), rng.standard_normal(c), ranks, dys=dys)
+    return time.perf_counter() - t0, BYTES_PER_ELEM * numel(shape) * ranks
+
+
+def cpu_sample(shapes, ranks, budget_s, max_units=None, min_units=1):
+    """Run layer samples (batch 2 per rank, cycling through the workload's layers)
+    through the reference until budget_s elapsed. Returns dict."""
+    bb = _reference_module()
+    kind = "reference" if bb is not None else "port"
+    t_total, b_total, units = 0.0, 0, 0
+    i = 0
+    while True:
+        s = shapes[i % len(shapes)]
+        shape = (2,) + tuple(s[1:])
+        dt, nb = (reference_step(bb, shape, ranks, i) if bb is not None
+                  else port_step(shape, ranks, i))
+        t_total += dt
+        b_total += nb
+        units += 1
+        i += 1
+        if max_units is not None and units >= max_units:
+            break
+        if units >= min_units and t_total >= budget_s:
+            break
+    return {"kind": kind, "seconds": t_total, "bytes": b_total, "units": units,
+            "gbs": b_total / t_total / 1e9}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n = args.gpus
+    shapes = resnet50_bn_shapes(32)
+    bb = _reference_module()
+    kind = "reference" if bb is not None else "port"
+    # warmup
+    for i in range(args.warmup):
+        s = shapes[i % len(shapes)]
+        (reference_step(bb, (2,) + tuple(s[1:]), n, i) if bb is not None
+         else port_step((2,) + tuple(s[1:]), n, i))
+    t_total, b_total = 0.0, 0
+    for k in range(args.steps):
+        s = shapes[k % len(shapes)]
+        shape = (2,) + tuple(s[1:])
+        dt, nb = (reference_step(bb, shape, n, 1000 + k) if bb is not None
+                  else port_step(shape, n, 1000 + k))
+        t_total += dt
+        b_total += nb
+    value = b_total / t_total / 1e9
+    cores = 1
+    sample = (f"per step: one ResNet-50 BN layer (cycling through the 53 layers in order) at "
+              f"batch 2 per simulated device, {n} device(s) as the reference's DeviceGroup "
+              f"threads, f64 (reference default), sync_bn_forward+sync_bn_backward")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": "resnet50_bn_b32 (sampled: batch 2 per layer-step)",
+                   "parallelism": f"cgbn_group{n}", "bn_group_size": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample, "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------------
+# GPU arm
+
+class GraphKernelTimer:
+    """Records CUDA events around every native launch; external events when capturing
+    so that the event nodes live inside the CUDA graph."""
+
+    def __init__(self, external):
+        import torch
+        self.torch = torch
+        self.external = external
+        self.spans = []
+        self._cur = None
+
+    def _ev(self):
+        if self.external:
+            return self.torch.cuda.Event(enable_timing=True, external=True)
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def begin(self, name, nbytes):
+        e0 = self._ev()
+        e0.record()
+        self._cur = (name, nbytes, e0)
+
+    def end(self):
+        e1 = self._ev()
+        e1.record()
+        name, nb, e0 = self._cur
+        self.spans.append((name, nb, e0, e1))
+
+    def collect(self, acc):
+        for name, nb, e0, e1 in self.spans:
+            ms = e0.elapsed_time(e1)
+            a = acc.setdefault(name, [0.0, 0, 0])
+            a[0] += ms
+            a[1] += nb
+            a[2] += 1
+
+
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1711_07240_b200 as cg
+    from paper_1711_07240_b200 import batchnorm as bnmod
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        handle = cg.DistHandle(bn_group_size=world)
+    else:
+        handle = cg.SoloHandle(dev)
+    cg.set_strict(False)
+
+    shapes = resnet50_bn_shapes(32)
+    elems = [numel(s) for s in shapes]
+    step_bytes_rank = BYTES_PER_ELEM * sum(elems)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    xs, dys, states = [], [], []
+    for s in shapes:
+        xs.append(torch.randn(s, device=dev, generator=gen))
+        dys.append(torch.randn(s, device=dev, generator=gen))
+        c = s[1]
+        gamma = torch.rand(c, device=dev, generator=gen) + 0.5
+        beta = torch.randn(c, device=dev, generator=gen)
+        states.append(cg.BNLayerState(gamma=gamma, beta=beta))
+
+    def step():
+        caches = []
+        for x, st in zip(xs, states):
+            _, cache = cg.sync_bn_forward(handle, x, st)
+            caches.append(cache)
+        for i in range(len(xs) - 1, -1, -1):
+            cg.sync_bn_backward(handle, dys[i], caches[i], states[i])
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+
+    use_graph = not args.no_graph
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    def run_once():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
+    # ---- timed region
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        run_once()
+    t1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms_total = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+    value = step_bytes_rank * world / (ms_step * 1e-3) / 1e9
+    launches_per_step = 4 * len(shapes)
+
+    # ---- per-kernel times: same step captured with event nodes (external events), else
+    # an eagerly instrumented step; several replays, CUDA events on the launch stream.
+    kstats = {}
+    timing_mode = "graph-external-events"
+    try:
+        tg = torch.cuda.CUDAGraph()
+        timer = GraphKernelTimer(external=True)
+        bnmod.kernel_timer = timer
+        with torch.cuda.graph(tg):
+            step()
+        bnmod.kernel_timer = None
+        for _ in range(min(args.steps, 10)):
+            tg.replay()
+            torch.cuda.synchronize()
+            timer.collect(kstats)
+        del tg
+    except Exception as exc:  # noqa: BLE001
+        bnmod.kernel_timer = None
+        timing_mode = f"eager-events ({type(exc).__name__})"
+        kstats = {}
+        for _ in range(min(args.steps, 10)):
+            timer = GraphKernelTimer(external=False)
+            bnmod.kernel_timer = timer
+            step()
+            bnmod.kernel_timer = None
+            torch.cuda.synchronize()
+            timer.collect(kstats)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks \
+        else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    kern = {}
+    tot_ms = sum(v[0] for v in kstats.values()) or 1.0
+    for name, (ms, nb, cnt) in kstats.items():
+        kern[name] = {"ms_per_step": ms / max(1, cnt / len(shapes)), "launches": cnt,
+                      "alg_gbs": nb / (ms * 1e-3) / 1e9 if ms > 0 else None,
+                      "share": ms / tot_ms}
+    dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
+    roofline = None
+    if dom:
+        ach = kern[dom]["alg_gbs"]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                    "peak_source": peak_src, "timing": timing_mode}
+
+    # ---- statistics exchange latency (N>1): NCCL all-gather of the fwd partial
+    exch = None
+    if world > 1:
+        exch = {}
+        for c in (256, 2048):
+            v = torch.zeros(2 * c + 1, dtype=torch.float64, device=dev)
+            for _ in range(5):
+                handle.exchange(cg.SCOPE_BN_GROUP, "probe", v)
+            torch.cuda.synchronize()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            reps = 200
+            e0.record()
+            for _ in range(reps):
+                handle.exchange(cg.SCOPE_BN_GROUP, "probe", v)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / reps
+            tt = torch.tensor([us], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            exch[f"C{c}_us"] = float(tt.item())
+        exch["transport"] = "NCCL all_gather_into_tensor (eager, per call)"
+        exch["per_step_exchanges"] = 2 * len(shapes)
+        exch["est_share_of_step"] = (exch["C256_us"] * 2 * len(shapes) * 1e-3) / ms_step
+
+    # ---- e2e: public API with host (pinned) buffers, H2D/D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hx = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
+        hdy = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
+        hy = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
+        hdx = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
+        for i in range(len(shapes)):
+            hx[i].copy_(xs[i])
+            hdy[i].copy_(dys[i])
+        dx_in = [torch.empty(s, device=dev) for s in shapes]
+        ddy_in = [torch.empty(s, device=dev) for s in shapes]
+
+        def e2e_step():
+            caches = []
+            for i, st in enumerate(states):
+                dx_in[i].copy_(hx[i], non_blocking=True)
+                y, cache = cg.sync_bn_forward(handle, dx_in[i], st)
+                hy[i].copy_(y, non_blocking=True)
+                caches.append(cache)
+            for i in range(len(shapes) - 1, -1, -1):
+                ddy_in[i].copy_(hdy[i], non_blocking=True)
+                dxo, dg, db = cg.sync_bn_backward(handle, ddy_in[i], caches[i], states[i])
+                hdx[i].copy_(dxo, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        k_e = max(1, min(args.steps, args.e2e_steps))
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(k_e):
+            e2e_step()
+        a1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_e = a0.elapsed_time(a1) / k_e
+        if world > 1:
+            tt = torch.tensor([ms_e], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_e = float(tt.item())
+        e2e = {"value": step_bytes_rank * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * sum(elems), "d2h_bytes_per_step": 8 * sum(elems),
+               "ms_per_step": ms_e, "steps": k_e,
+               "path": "sync_bn_forward/sync_bn_backward per layer, pinned host x/dy in, "
+                       "y/dx out, eager (no graph)"}
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = cpu_sample(shapes, 1, args.cpu_budget_s)
+        cpu = {"value": res["gbs"], "unit": UNIT, "cores": 1, "kind": res["kind"],
+               "sample": (f"{res['units']} ResNet-50 BN layer shapes at batch 2 (cycling the "
+                          f"53 layers), f64, sync_bn_forward+backward via "
+                          f"DeviceGroup(1); {res['seconds']:.1f} s"),
+               "host_cpus": os.cpu_count()}
+
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (fp64 statistics)", "data": "synthetic (torch.randn, seeded per rank)",
+            "config": {"workload": "resnet50_bn_b32", "layers": len(shapes),
+                       "per_gpu_batch": 32, "elements_per_gpu": sum(elems),
+                       "alg_bytes_per_elem": BYTES_PER_ELEM,
+                       "parallelism": f"cgbn_group{world}", "bn_group_size": world,
+                       "layout": "NCHW", "relu": False,
+                       "l2_policy": ("inputs > L2: 53 layers' x+dy = "
+                                     f"{8 * sum(elems) / 1e9:.2f} GB per step >> 126 MB L2; "
+                                     "intra-layer re-reads of x may hit L2"),
+                       "cuda_graph": use_graph},
+            "per_gpu_gbs": value / world,
+            "per_gpu_hbm_frac": value / world / hbm_peak,
+            "kernels": kern,
+            "roofline": roofline,
+            "exchange": exch,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

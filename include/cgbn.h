@@ -1,0 +1,155 @@
+/*
+ * cgbn.h — C ABI of the B200-native Cross-GPU Batch Normalization (CGBN) hot path.
+ *
+ * This is the drop-in boundary for the reference's CGBN operator
+ * (`bigbatch.batchnorm`, /root/reference/pkg/src/bigbatch/batchnorm.py). The reference
+ * has no native code: its hot path is NumPy (channel_sum / channel_affine in tensor.py)
+ * glued by the `reduce_vec` seam that is bound to `allreduce_sum` over the BN sub-group
+ * (batchnorm.py:115-144, 169-185, 188-236). Every entry point below replaces one piece
+ * of that path; the per-function comment names the reference lines it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types. All device pointers are CUDA device
+ *    memory on the device current to the calling thread. `stream` is a cudaStream_t
+ *    passed as void* (NULL = legacy default stream). Every call is asynchronous
+ *    (stream-ordered) and performs no allocation and no host synchronisation.
+ *  - Activations are fp32, contiguous. `layout` is CGBN_LAYOUT_NCHW (x[N][C][HW]; a 2-D
+ *    (N, C) tensor is NCHW with HW == 1) or CGBN_LAYOUT_NHWC (x[N][HW][C]).
+ *  - Statistics travel between kernels and ranks as fp64 "partials":
+ *      forward  partial (2C+1 doubles): [mean_r (C) | M2_r (C) | count_r (1)]
+ *      backward partial (2C   doubles): [sum dy (C) | sum dy*(x-mean) (C)]
+ *    The forward partial is the reference's packed [sum, sum_sq, m] vector
+ *    (batchnorm.py:120) re-expressed as (mean, centred M2, count) so that the merge is
+ *    cancellation-free; the backward partial is the reference's [sum dy, sum dy*x_hat]
+ *    (batchnorm.py:198-202) with the 1/std factor applied after the reduction.
+ *  - A group of G ranks exchanges partials (NCCL all-gather, the host rendezvous of the
+ *    threaded DeviceGroup, or the one-shot P2P path) and each consumer kernel folds the
+ *    G partials in ascending rank order, exactly like the reference's star all-reduce
+ *    (collectives.py:293-295); every rank therefore computes bitwise-identical
+ *    statistics.
+ *  - Return value: 0 (CGBN_OK) or a CGBN_ERR_* code; cgbn_last_error() returns a
+ *    thread-local message for the last failing call. Data-dependent errors found on the
+ *    device (non-finite statistics, total count < 2) are OR-ed into the caller-provided
+ *    device status word (CGBN_STATUS_* bits) and checked by the host at sync points.
+ */
+#ifndef CGBN_H_
+#define CGBN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGBN_ABI_VERSION 1
+
+#define CGBN_LAYOUT_NCHW 0
+#define CGBN_LAYOUT_NHWC 1
+
+#define CGBN_MAX_GROUP 64
+
+#define CGBN_OK 0
+#define CGBN_ERR_INVALID 1 /* bad argument (shape, alignment, group size, ws too small) */
+#define CGBN_ERR_CUDA 2    /* CUDA launch / runtime error */
+
+#define CGBN_STATUS_NONFINITE 1u  /* NaN/Inf reached the statistics (tensor.py:59-60) */
+#define CGBN_STATUS_SMALL_COUNT 2u /* total count < 2 (batchnorm.py:133-137) */
+
+#define CGBN_DTYPE_F32 0
+#define CGBN_DTYPE_F64 1
+
+/* ABI version (CGBN_ABI_VERSION) and build info. */
+int cgbn_abi_version(void);
+const char* cgbn_build_info(void);
+
+/* Thread-local message describing the last non-zero return of any cgbn_* call. */
+const char* cgbn_last_error(void);
+
+/* Number of SMs of the current device (cached per device). */
+int cgbn_num_sms(void);
+
+/* Bytes of zero-initialised workspace the reduction kernels (cgbn_fwd_stats,
+ * cgbn_bwd_reduce) need for this shape. The workspace holds per-CTA partials and
+ * per-channel arrival tickets; the kernels leave the tickets at zero on exit, so one
+ * zeroed buffer can be reused by every later call on the same stream. */
+size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout);
+
+/* Forward, step 1: this rank's per-channel partial statistics.
+ * Replaces channel_sum(x, with_sum_sq) (tensor.py:143-153; the _channels_last_rows +
+ * sequential_sum_rows pair, tensor.py:121-140) as called from _train_forward
+ * (batchnorm.py:118) — one read of x, deterministic fixed-order cross-CTA fold.
+ * Writes `partial` (2C+1 doubles). */
+int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                   double* partial, void* ws, size_t ws_bytes, void* stream);
+
+/* Forward, step 2: fold the G gathered partials (ascending rank order), finalise
+ * mean/var/inv_std, update the running statistics in place, and write
+ * y = gamma * (x - mean) * inv_std + beta (optionally ReLU'd).
+ * Replaces _train_forward's post-reduction half (batchnorm.py:121-143): mu/var
+ * (:122-124, :128-132), the m < 2 check (:133-137), inv_std (:138), the two
+ * channel_affine calls (:139-140, tensor.py:156-170) and bn_update_running
+ * (batchnorm.py:239-252).
+ *  partials : host array of G device pointers, partials[r] = rank r's forward partial.
+ *  saved    : out, 3C+1 doubles [mean (C) | var (C) | inv_std (C) | total_count (1)];
+ *             the backward reads it (it replaces BNForwardCache.mu/var/total_count —
+ *             x_hat is recomputed from x instead of being stored, batchnorm.py:142).
+ *  running_mean/var may be NULL (no update). momentum in [0, 1]. */
+int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                       const double* const* partials, int G,
+                       const float* gamma, const float* beta, double eps, double momentum,
+                       float* running_mean, float* running_var, double* saved, int relu,
+                       float* y, unsigned* status, void* stream);
+
+/* Eval-mode forward: y = gamma * (x - running_mean) / sqrt(running_var + eps) + beta.
+ * Replaces bn_forward_local(mode="eval") (batchnorm.py:158-166); no collective and the
+ * running statistics are left untouched. */
+int cgbn_fwd_eval(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                  const float* gamma, const float* beta, const float* running_mean,
+                  const float* running_var, double eps, int relu, float* y, void* stream);
+
+/* Backward, step 1: this rank's partial [sum g, sum g*(x-mean)] with g = dy (times the
+ * ReLU mask recomputed from x when relu != 0). Replaces the two sequential_sum_rows
+ * calls of _backward_core (batchnorm.py:198-201). Writes `partial` (2C doubles). */
+int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW,
+                    int layout, const double* saved, const float* gamma, const float* beta,
+                    int relu, double* partial, void* ws, size_t ws_bytes, void* stream);
+
+/* Backward, step 2: fold the G gathered backward partials (ascending rank order) into
+ * the BN-group sums dbeta = sum g, dgamma = sum g*x_hat (identical on every rank, as in
+ * batchnorm.py:203) and write dx = gamma/sqrt(var+eps)*(g - dbeta/m - x_hat*dgamma/m)
+ * (batchnorm.py:204-209). As in the reference, `eps` is the backward state's eps while
+ * x_hat keeps the forward's normalisation. dgamma/dbeta (C floats each) may be NULL. */
+int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                const double* const* partials, int G, const double* saved,
+                const float* gamma, const float* beta, double eps, int relu, float* dx,
+                float* dgamma, float* dbeta, unsigned* status, void* stream);
+
+/* x_hat = (x - mean) * inv_std from a saved forward context (the reference caches
+ * x_hat in BNForwardCache, batchnorm.py:142; here it is recomputed on demand). */
+int cgbn_xhat(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+              const double* saved, float* xhat, void* stream);
+
+/* Ascending-rank fold of G device vectors of n elements (dtype CGBN_DTYPE_F32/F64):
+ * out = v[0] + v[1] + ... + v[G-1], evaluated left to right. This is the arithmetic of
+ * the reference's allreduce_sum at the root (collectives.py:293-295); the transport
+ * (gathering the G vectors) is done by the caller. */
+int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void* out,
+                  void* stream);
+
+/* Per-channel sums of an activation (sum and optional sum of squares, fp64 out).
+ * Device counterpart of the reference's channel_sum (tensor.py:143-153). sum_sq may be
+ * NULL. ws as for cgbn_fwd_stats. */
+int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                     double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream);
+
+/* Per-channel affine map out = scale[c] * x + shift[c] (fp64 coefficients).
+ * Device counterpart of the reference's channel_affine (tensor.py:156-170). */
+int cgbn_channel_affine(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                        const double* scale, const double* shift, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CGBN_H_ */

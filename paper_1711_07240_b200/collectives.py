@@ -1,0 +1,461 @@
+"""Device groups and the statistics exchange of the CGBN hot path.
+
+Mirrors the reference's ``bigbatch.collectives`` surface (DeviceGroup, DeviceHandle,
+allreduce_sum, scopes, CollectiveProtocolError / CollectiveTimeoutError;
+/root/reference/pkg/src/bigbatch/collectives.py:24-298), re-designed for GPUs:
+
+* The reference moves numpy vectors between threads through per-(rank, scope) queues
+  and folds them at the lowest rank in ascending rank order (collectives.py:260-298).
+* Here the per-rank vectors stay in device memory. A collective is split into a
+  *transport* that makes every rank's vector visible to every rank of the scope, and a
+  *fold* that each consumer kernel performs itself in ascending rank order (so all
+  ranks compute bitwise-identical results, like the reference's root fold followed by
+  the broadcast of the result).
+
+Two transports:
+
+``DeviceGroup`` (threaded, one process): one host thread per rank, each with its own
+  CUDA stream; ranks may share one GPU ("G shards on one GPU", the mode the parity tests
+  use) or sit on different GPUs. The transport is a host rendezvous that exchanges
+  device pointers plus CUDA events — no device-side waiting, so emulated ranks on one
+  GPU can never deadlock. It keeps the reference's diagnostics: per-scope sequence
+  numbers, kind/length mismatch -> CollectiveProtocolError naming ranks, timeouts ->
+  CollectiveTimeoutError naming the missing ranks, and abort fan-out when a worker dies.
+
+``DistGroup`` (torch.distributed, one process per GPU, NCCL over NVLink/NVSwitch):
+  the transport is an all-gather of the fixed-size partial vector on the BN sub-group's
+  communicator (contiguous rank blocks of ``bn_group_size``, collectives.py:98-126).
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Any, Callable
+
+import torch
+
+from . import _lib
+
+DEFAULT_TIMEOUT_S = 30.0
+
+SCOPE_WORLD = "world"
+SCOPE_BN_GROUP = "bn_group"
+_SCOPE_NAMES = (SCOPE_WORLD, SCOPE_BN_GROUP)
+
+
+class CollectiveError(RuntimeError):
+    """Base class for collective failures (collectives.py:31-32)."""
+
+
+class CollectiveProtocolError(CollectiveError):
+    """Mismatched collective calls, payload disagreement, or invalid scope."""
+
+    def __init__(self, msg, from_abort=False):
+        super().__init__(msg)
+        self.from_abort = from_abort
+
+
+class CollectiveTimeoutError(CollectiveError):
+    """A rank waited longer than the configured timeout for its peers."""
+
+
+# ------------------------------------------------------------------------------------
+# Rendezvous (threaded transport)
+
+
+@dataclass
+class _Post:
+    rank: int
+    kind: str
+    meta: tuple  # (length, dtype string) of the exchanged vector
+    tensor: Any
+    event: Any
+    info: Any = None  # host-side per-rank info (e.g. the local element count)
+
+
+class _Board:
+    """Per-scope exchange board: posts keyed by sequence number."""
+
+    def __init__(self, ranks):
+        self.ranks = list(ranks)
+        self.cv = threading.Condition()
+        self.posts: dict[int, dict[int, _Post]] = {}
+        self.taken: dict[int, int] = {}
+        self.abort_note: str | None = None
+
+    def exchange(self, scope_key: str, seq: int, post: _Post, timeout_s: float) -> dict:
+        g = len(self.ranks)
+        with self.cv:
+            if self.abort_note is not None:
+                raise CollectiveProtocolError(self.abort_note, from_abort=True)
+            slot = self.posts.setdefault(seq, {})
+            slot[post.rank] = post
+            self.cv.notify_all()
+            deadline = time.monotonic() + timeout_s
+            while len(slot) < g and self.abort_note is None:
+                remaining = deadline - time.monotonic()
+                if remaining <= 0:
+                    missing = sorted(set(self.ranks) - set(slot))
+                    note = (f"{post.kind}[{scope_key}#{seq}]: rank {post.rank} timed out "
+                            f"after {timeout_s}s waiting for rank(s) {missing}")
+                    raise CollectiveTimeoutError(note)
+                self.cv.wait(remaining)
+            if len(slot) < g:
+                raise CollectiveProtocolError(self.abort_note, from_abort=True)
+            got = dict(slot)
+            self.taken[seq] = self.taken.get(seq, 0) + 1
+            if self.taken[seq] == g:
+                del self.posts[seq]
+                del self.taken[seq]
+        kinds = {p.kind for p in got.values()}
+        if len(kinds) != 1:
+            detail = ", ".join(f"rank {r}: {got[r].kind}" for r in self.ranks)
+            raise CollectiveProtocolError(
+                f"collective mismatch in {scope_key}#{seq}: ranks issued different "
+                f"collectives ({detail})")
+        metas = {p.meta for p in got.values()}
+        if len(metas) != 1:
+            detail = ", ".join(f"rank {r}: len {got[r].meta[0]} ({got[r].meta[1]})"
+                               for r in self.ranks)
+            raise CollectiveProtocolError(
+                f"{post.kind}[{scope_key}#{seq}]: payload mismatch across ranks ({detail})")
+        return got
+
+    def abort(self, note: str):
+        with self.cv:
+            if self.abort_note is None:
+                self.abort_note = note
+            self.cv.notify_all()
+
+
+# ------------------------------------------------------------------------------------
+# Handles
+
+
+class _HandleBase:
+    """Common scope bookkeeping (collectives.py:56-95)."""
+
+    rank: int
+    world_size: int
+    bn_group_size: int
+
+    @property
+    def bn_group_index(self) -> int:
+        return self.rank // self.bn_group_size
+
+    @property
+    def bn_group_ranks(self) -> list[int]:
+        g = self.bn_group_size
+        start = self.bn_group_index * g
+        return list(range(start, start + g))
+
+    def _scope_info(self, scope: str) -> tuple[str, list[int]]:
+        if scope == SCOPE_WORLD:
+            return "world", list(range(self.world_size))
+        if scope == SCOPE_BN_GROUP:
+            return f"bn{self.bn_group_index}", self.bn_group_ranks
+        raise CollectiveProtocolError(
+            f"rank {self.rank}: unknown scope {scope!r}; expected one of {_SCOPE_NAMES}")
+
+    def _next_seq(self, scope_key: str) -> int:
+        seq = self._seq.get(scope_key, 0)
+        self._seq[scope_key] = seq + 1
+        return seq
+
+    def exchange(self, scope: str, kind: str, vec: torch.Tensor, info=None):
+        """Make every rank's 1-D ``vec`` of ``scope`` visible on this rank's device, in
+        ascending rank order, ordered after each producer's writes on this rank's
+        current stream. Transport only — the fold is done by the consumer kernel.
+
+        Returns ``(vectors, infos)``: ``infos`` is the per-rank list of the host-side
+        ``info`` objects when the transport carries them (threaded group), else None.
+        """
+        raise NotImplementedError
+
+    @property
+    def device(self) -> torch.device:
+        raise NotImplementedError
+
+
+class DeviceHandle(_HandleBase):
+    """One rank of a threaded ``DeviceGroup`` (collectives.py:56-95).
+
+    A handle belongs to exactly one group and must only be used from its own worker
+    thread; inside ``DeviceGroup.run`` the worker's current CUDA stream is the handle's
+    own stream.
+    """
+
+    def __init__(self, group: "DeviceGroup", rank: int, device: torch.device):
+        self.group = group
+        self.rank = rank
+        self.world_size = group.world_size
+        self.bn_group_size = group.bn_group_size
+        self._device = device
+        self._seq: dict[str, int] = {}
+        self.stream = None  # created in the worker thread
+
+    def __repr__(self):
+        return f"DeviceHandle(rank={self.rank}, world={self.world_size}, device={self._device})"
+
+    @property
+    def device(self) -> torch.device:
+        return self._device
+
+    def exchange(self, scope: str, kind: str, vec: torch.Tensor, info=None):
+        scope_key, ranks = self._scope_info(scope)
+        seq = self._next_seq(scope_key)
+        if vec.dim() != 1:
+            raise CollectiveProtocolError(f"rank {self.rank}: collective payload must be a 1-D vector")
+        event = None
+        if vec.is_cuda:
+            event = torch.cuda.Event()
+            event.record(torch.cuda.current_stream(vec.device))
+        post = _Post(self.rank, kind, (int(vec.numel()), str(vec.dtype)), vec, event, info)
+        got = self.group._boards[scope_key].exchange(scope_key, seq, post, self.group.timeout_s)
+        out = []
+        if vec.is_cuda:
+            cur = torch.cuda.current_stream(vec.device)
+            for r in ranks:
+                p = got[r]
+                if r != self.rank:
+                    cur.wait_event(p.event)
+                t = p.tensor
+                if t.device != vec.device:
+                    t = t.to(vec.device, non_blocking=True)
+                elif r != self.rank:
+                    t.record_stream(cur)
+                out.append(t)
+        else:
+            out = [got[r].tensor for r in ranks]
+        return out, [got[r].info for r in ranks]
+
+
+class DeviceGroup:
+    """A fixed set of ranks 0..n-1 run as threads of this process (collectives.py:98-199).
+
+    Ranks are partitioned into contiguous BN sub-groups of ``bn_group_size``
+    ([0..g), [g..2g), ...); ``bn_group_size`` must divide ``world_size``. ``devices``
+    maps ranks to CUDA devices (default: every rank on the current device — the
+    "G shards on one GPU" mode).
+    """
+
+    def __init__(self, world_size: int, bn_group_size: int | None = None, seed: int = 0,
+                 timeout_s: float = DEFAULT_TIMEOUT_S, devices=None):
+        if world_size < 1:
+            raise ValueError(f"world_size must be >= 1, got {world_size}")
+        bn_group_size = world_size if bn_group_size is None else bn_group_size
+        if bn_group_size < 1 or world_size % bn_group_size != 0:
+            raise ValueError(
+                f"bn_group_size {bn_group_size} must divide world_size {world_size}")
+        self.world_size = world_size
+        self.bn_group_size = bn_group_size
+        self.seed = seed
+        self.timeout_s = timeout_s
+        if devices is None:
+            if torch.cuda.is_available():
+                devices = [torch.device("cuda", torch.cuda.current_device())] * world_size
+            else:
+                devices = [torch.device("cpu")] * world_size
+        devices = [torch.device(d) for d in devices]
+        if len(devices) != world_size:
+            raise ValueError(f"need {world_size} devices, got {len(devices)}")
+        self.devices = devices
+        self._boards = {"world": _Board(range(world_size))}
+        for i in range(world_size // bn_group_size):
+            self._boards[f"bn{i}"] = _Board(range(i * bn_group_size, (i + 1) * bn_group_size))
+        self.handles = [DeviceHandle(self, r, devices[r]) for r in range(world_size)]
+
+    def _abort_all(self, note: str):
+        for b in self._boards.values():
+            b.abort(note)
+
+    def run(self, fn: Callable[[DeviceHandle], Any], timeout_s: float | None = None,
+            return_exceptions: bool = False) -> list:
+        """Run ``fn(handle)`` concurrently on every rank; return per-rank results.
+
+        Same contract as the reference (collectives.py:146-199): exceptions are
+        re-raised preferring the rank with the original diagnostic over ranks that were
+        merely aborted; ``return_exceptions`` returns them in the list instead. Each
+        rank's device work is complete when ``run`` returns.
+        """
+        # fresh boards per run so a previous abort does not leak into this one
+        self._boards = {k: _Board(b.ranks) for k, b in self._boards.items()}
+        for h in self.handles:
+            h._seq = {}
+        results: list[Any] = [None] * self.world_size
+        errors: list[BaseException | None] = [None] * self.world_size
+
+        def runner(handle: DeviceHandle):
+            try:
+                if handle.device.type == "cuda":
+                    torch.cuda.set_device(handle.device)
+                    handle.stream = torch.cuda.Stream(device=handle.device)
+                    with torch.cuda.stream(handle.stream):
+                        results[handle.rank] = fn(handle)
+                    handle.stream.synchronize()
+                else:
+                    results[handle.rank] = fn(handle)
+            except BaseException as exc:  # noqa: BLE001 - reported to caller
+                errors[handle.rank] = exc
+                if not isinstance(exc, CollectiveError):
+                    self._abort_all(f"aborted: rank {handle.rank} failed with "
+                                    f"{type(exc).__name__}: {exc}")
+                elif isinstance(exc, CollectiveTimeoutError):
+                    self._abort_all(str(exc))
+
+        threads = [threading.Thread(target=runner, args=(h,), daemon=True,
+                                    name=f"cgbn-rank-{h.rank}") for h in self.handles]
+        for t in threads:
+            t.start()
+        join_deadline = self.timeout_s + 10.0 if timeout_s is None else timeout_s
+        for r, t in enumerate(threads):
+            t.join(timeout=join_deadline)
+            if t.is_alive():
+                errors[r] = CollectiveTimeoutError(f"rank {r}: worker did not finish")
+        if return_exceptions:
+            return [errors[r] if errors[r] is not None else results[r]
+                    for r in range(self.world_size)]
+        primary = None
+        for exc in errors:
+            if exc is None:
+                continue
+            if not (isinstance(exc, CollectiveProtocolError) and exc.from_abort):
+                raise exc
+            primary = primary or exc
+        if primary is not None:
+            raise primary
+        return results
+
+
+class SoloHandle(_HandleBase):
+    """A one-rank group (world 1): the exchange is the identity, as the reference's
+    local path binds reduce_vec to ``lambda v: v`` (batchnorm.py:157, 218)."""
+
+    def __init__(self, device=None):
+        self.rank = 0
+        self.world_size = 1
+        self.bn_group_size = 1
+        self._seq = {}
+        self._device = (torch.device(device) if device is not None
+                        else torch.device("cuda", torch.cuda.current_device()))
+
+    @property
+    def device(self) -> torch.device:
+        return self._device
+
+    def exchange(self, scope: str, kind: str, vec: torch.Tensor, info=None):
+        self._scope_info(scope)
+        return [vec], [info]
+
+
+# ------------------------------------------------------------------------------------
+# torch.distributed transport (one process per GPU)
+
+
+class DistHandle(_HandleBase):
+    """This process's rank in a torch.distributed job, with BN sub-groups of
+    ``bn_group_size`` contiguous ranks. The exchange is an all-gather of the packed
+    partial on the scope's communicator (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, bn_group_size: int | None = None, validate: bool = False):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialised before DistHandle")
+        self.rank = dist.get_rank()
+        self.world_size = dist.get_world_size()
+        g = self.world_size if bn_group_size is None else bn_group_size
+        if g < 1 or self.world_size % g != 0:
+            raise ValueError(f"bn_group_size {g} must divide world_size {self.world_size}")
+        self.bn_group_size = g
+        self.validate = validate
+        self._seq = {}
+        # every rank must create every sub-group, in the same order
+        self._groups = {"world": None}
+        if g == self.world_size:
+            self._groups[f"bn0"] = None
+        else:
+            for i in range(self.world_size // g):
+                pg = dist.new_group(list(range(i * g, (i + 1) * g)))
+                self._groups[f"bn{i}"] = pg
+        backend = dist.get_backend()
+        self._device = (torch.device("cuda", torch.cuda.current_device())
+                        if backend == "nccl" else torch.device("cpu"))
+
+    def __repr__(self):
+        return f"DistHandle(rank={self.rank}, world={self.world_size}, g={self.bn_group_size})"
+
+    @property
+    def device(self) -> torch.device:
+        return self._device
+
+    def exchange(self, scope: str, kind: str, vec: torch.Tensor, info=None):
+        import torch.distributed as dist
+        scope_key, ranks = self._scope_info(scope)
+        seq = self._next_seq(scope_key)
+        pg = self._groups[scope_key]
+        g = len(ranks)
+        if self.validate:
+            self._validate(pg, ranks, scope_key, seq, kind, vec)
+        if g == 1:
+            return [vec], None
+        out = torch.empty((g, vec.numel()), dtype=vec.dtype, device=vec.device)
+        if vec.is_cuda:
+            dist.all_gather_into_tensor(out, vec.contiguous(), group=pg)
+        else:  # gloo (CPU tests of the transport)
+            dist.all_gather(list(out.unbind(0)), vec.contiguous(), group=pg)
+        return [out[i] for i in range(g)], None
+
+    def _validate(self, pg, ranks, scope_key, seq, kind, vec):
+        """Optional host-side protocol check (one extra tiny all-gather): every rank
+        must issue the same collective with the same payload length, as the reference
+        diagnoses at its root (collectives.py:243-292)."""
+        import torch.distributed as dist
+        kind_id = sum(ord(ch) * (i + 1) for i, ch in enumerate(kind)) % (1 << 30)
+        dt_id = {torch.float32: 0, torch.float64: 1}.get(vec.dtype, 2)
+        meta = torch.tensor([seq, kind_id, vec.numel(), dt_id], dtype=torch.int64,
+                            device=vec.device)
+        allm = torch.empty((len(ranks), 4), dtype=torch.int64, device=vec.device)
+        dist.all_gather_into_tensor(allm, meta, group=pg)
+        allm = allm.cpu().tolist()
+        if any(m[:2] != allm[0][:2] for m in allm):
+            raise CollectiveProtocolError(
+                f"collective mismatch in {scope_key}#{seq}: per-rank (seq, kind) = "
+                + ", ".join(f"rank {r}: {tuple(m[:2])}" for r, m in zip(ranks, allm)))
+        if any(m[2:] != allm[0][2:] for m in allm):
+            raise CollectiveProtocolError(
+                f"{kind}[{scope_key}#{seq}]: payload mismatch across ranks ("
+                + ", ".join(f"rank {r}: len {m[2]}" for r, m in zip(ranks, allm)) + ")")
+
+
+# ------------------------------------------------------------------------------------
+# allreduce_sum on device vectors
+
+
+def allreduce_sum(handle: _HandleBase, scope: str, v) -> torch.Tensor:
+    """Elementwise sum of every rank's 1-D device vector; all ranks receive the result.
+
+    Accumulation runs in ascending rank order (collectives.py:260-298), so the result is
+    bitwise identical on every rank and across runs. ``v`` must be a CUDA float32 or
+    float64 tensor (no CPU fallback).
+    """
+    if not isinstance(v, torch.Tensor):
+        raise CollectiveProtocolError(f"rank {handle.rank}: payload must be a torch.Tensor")
+    if v.dim() != 1:
+        raise CollectiveProtocolError(f"rank {handle.rank}: collective payload must be a 1-D vector")
+    if not v.is_cuda:
+        raise CollectiveProtocolError(
+            f"rank {handle.rank}: allreduce_sum needs a CUDA tensor (there is no CPU path)")
+    if v.dtype not in (torch.float32, torch.float64):
+        raise CollectiveProtocolError(f"rank {handle.rank}: payload dtype {v.dtype} unsupported")
+    v = v.contiguous()
+    parts, _ = handle.exchange(scope, "allreduce", v)
+    out = torch.empty_like(v)
+    lib = _lib.load()
+    arr, keep = _lib.ptr_array([p.data_ptr() for p in parts])
+    dt = _lib.DTYPE_F64 if v.dtype == torch.float64 else _lib.DTYPE_F32
+    _lib.check(lib.cgbn_fold_sum(arr, len(parts), v.numel(), dt, out.data_ptr(),
+                                 torch.cuda.current_stream(v.device).cuda_stream),
+               "cgbn_fold_sum")
+    return out

@@ -1,0 +1,157 @@
+"""Activation layout handling and the device counterparts of the reference's channel
+primitives (``channel_sum``, ``channel_affine``; /root/reference/pkg/src/bigbatch/tensor.py).
+
+The reference's ``Tensor`` (tensor.py:39-87) is an immutable f64/f32 numpy array that
+rejects NaN/Inf on construction. Here activations are torch CUDA fp32 tensors, NCHW
+contiguous (or channels_last = NHWC, or 2-D (N, C)); the finiteness contract is kept by
+the statistics kernels, which report non-finite statistics through a device status
+word instead of an O(E) host scan (see batchnorm.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+
+class TensorError(ValueError):
+    """Invalid shape, layout, or argument for a tensor operation (tensor.py:19-20)."""
+
+
+class NonFiniteError(FloatingPointError):
+    """A public operation produced or received NaN/Inf values (tensor.py:23-24)."""
+
+
+@dataclass
+class Geometry:
+    x: torch.Tensor  # the (possibly made-contiguous) tensor the kernels read
+    N: int
+    C: int
+    HW: int
+    layout: int
+
+    @property
+    def count(self) -> int:
+        return self.N * self.HW
+
+
+def geometry(x, what: str = "x", err=TensorError) -> Geometry:
+    """Validate an activation and describe it for the C ABI.
+
+    Layouts (tensor.py:121-128 supports (N, C) and (N, C, H, W)): 2-D (N, C) is NCHW
+    with HW = 1; 4-D NCHW-contiguous -> CGBN_LAYOUT_NCHW; 4-D channels_last ->
+    CGBN_LAYOUT_NHWC; any other strides are made NCHW-contiguous.
+    """
+    if not isinstance(x, torch.Tensor):
+        raise err(f"{what} must be a torch.Tensor, got {type(x).__name__}")
+    if x.dim() not in (2, 4):
+        raise err(f"expected layout (N,C) or (N,C,H,W), got shape {tuple(x.shape)}")
+    if any(e <= 0 for e in x.shape):
+        raise err(f"tensor extents must be positive, got shape {tuple(x.shape)}")
+    if not x.is_cuda:
+        raise err(f"{what} must be a CUDA tensor (the CGBN path has no CPU fallback)")
+    if x.dtype != torch.float32:
+        raise err(f"{what} must be float32, got {x.dtype}")
+    if x.dim() == 2:
+        x = x.contiguous()
+        return Geometry(x, int(x.shape[0]), int(x.shape[1]), 1, _lib.LAYOUT_NCHW)
+    n, c, h, w = (int(e) for e in x.shape)
+    if x.is_contiguous():
+        return Geometry(x, n, c, h * w, _lib.LAYOUT_NCHW)
+    if x.is_contiguous(memory_format=torch.channels_last):
+        return Geometry(x, n, c, h * w, _lib.LAYOUT_NHWC)
+    x = x.contiguous()
+    return Geometry(x, n, c, h * w, _lib.LAYOUT_NCHW)
+
+
+def same_layout_like(g: Geometry) -> torch.Tensor:
+    """Uninitialised output with the input's shape and memory layout."""
+    if g.layout == _lib.LAYOUT_NHWC:
+        return torch.empty_like(g.x, memory_format=torch.channels_last)
+    return torch.empty_like(g.x, memory_format=torch.contiguous_format)
+
+
+def stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+# Workspaces (zero-initialised; the kernels return their tickets to zero) and device
+# status words, one per (device, stream).
+_ws_cache: dict = {}
+_status_cache: dict = {}
+
+
+def workspace(device, nbytes: int) -> torch.Tensor:
+    st = torch.cuda.current_stream(device)
+    key = (st.device_index, st.cuda_stream)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        size = max(nbytes, 1 << 16)
+        if buf is not None:
+            size = max(size, 2 * buf.numel())
+        buf = torch.zeros(size, dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def status_word(device) -> torch.Tensor:
+    st = torch.cuda.current_stream(device)
+    key = (st.device_index, st.cuda_stream)
+    buf = _status_cache.get(key)
+    if buf is None:
+        buf = torch.zeros(1, dtype=torch.int32, device=device)
+        _status_cache[key] = buf
+    return buf
+
+
+@dataclass
+class ChannelStats:
+    """Per-channel reduction result (tensor.py:101-118); sums are fp64 device tensors."""
+
+    count: int
+    sum: torch.Tensor
+    sum_sq: torch.Tensor | None = None
+
+    def __post_init__(self):
+        if self.count <= 0:
+            raise TensorError(f"ChannelStats.count must be positive, got {self.count}")
+        if self.sum_sq is not None and self.sum_sq.shape != self.sum.shape:
+            raise TensorError("ChannelStats.sum and sum_sq must have equal length")
+
+
+def channel_sum(x: torch.Tensor, with_sum_sq: bool = False) -> ChannelStats:
+    """Per-channel sums over all non-channel axes (tensor.py:143-153), on the device.
+
+    The reference pins a strict left-to-right fold; the kernel uses a fixed tree (same
+    input -> bitwise-identical sums, run to run) accumulated in fp64.
+    """
+    g = geometry(x)
+    lib = _lib.load()
+    s = torch.empty(g.C, dtype=torch.float64, device=g.x.device)
+    ss = torch.empty(g.C, dtype=torch.float64, device=g.x.device) if with_sum_sq else None
+    nb = lib.cgbn_workspace_bytes(g.N, g.C, g.HW, g.layout)
+    ws = workspace(g.x.device, nb)
+    _lib.check(lib.cgbn_channel_sum(g.x.data_ptr(), g.N, g.C, g.HW, g.layout, s.data_ptr(),
+                                    ss.data_ptr() if ss is not None else None, ws.data_ptr(),
+                                    ws.numel(), stream_ptr(g.x.device)), "cgbn_channel_sum")
+    return ChannelStats(count=g.count, sum=s, sum_sq=ss)
+
+
+def channel_affine(x: torch.Tensor, scale, shift) -> torch.Tensor:
+    """Per-channel affine map out[n,c,...] = scale[c] * x[n,c,...] + shift[c]
+    (tensor.py:156-170), fp64 coefficients, one rounding to fp32."""
+    g = geometry(x)
+    scale = torch.as_tensor(scale, dtype=torch.float64, device=g.x.device).contiguous()
+    shift = torch.as_tensor(shift, dtype=torch.float64, device=g.x.device).contiguous()
+    if tuple(scale.shape) != (g.C,) or tuple(shift.shape) != (g.C,):
+        raise TensorError(f"scale/shift must have length C={g.C}, got {tuple(scale.shape)} "
+                          f"and {tuple(shift.shape)}")
+    out = same_layout_like(g)
+    lib = _lib.load()
+    _lib.check(lib.cgbn_channel_affine(g.x.data_ptr(), g.N, g.C, g.HW, g.layout,
+                                       scale.data_ptr(), shift.data_ptr(), out.data_ptr(),
+                                       stream_ptr(g.x.device)), "cgbn_channel_affine")
+    return out

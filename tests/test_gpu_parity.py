@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors
+and the pinned oracle, on the same seeded inputs split identically across ranks.
+
+Tolerances (stated, fp32 path vs the f64 reference; metric = the reference's rel_err,
+max|a-b| / max(|a|,|b|,1e-3), pkg/tests/helpers.py:158-163):
+    mean, var, y, x_hat, running_mean, running_var : 1e-5
+    dx, dgamma, dbeta                              : 1e-4
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_cases import case_names, load_case
+from oracle import cgbn_oracle as O
+
+import paper_1711_07240_b200 as cg
+
+pytestmark = pytest.mark.gpu
+
+TOL_FWD = 1e-5
+TOL_BWD = 1e-4
+
+
+def _dev():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return torch.device("cuda", 0)
+
+
+def run_group(world, g, xs, dys, gamma, beta, eps=1e-5, momentum=0.1, rm0=None, rv0=None,
+              one_pass=False, relu=False, channels_last=False):
+    dev = _dev()
+    xs_t = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in xs]
+    dys_t = [torch.from_numpy(np.ascontiguousarray(d)).to(dev) for d in dys] if dys else None
+    if channels_last:
+        xs_t = [x.contiguous(memory_format=torch.channels_last) for x in xs_t]
+        if dys_t:
+            dys_t = [d.contiguous(memory_format=torch.channels_last) for d in dys_t]
+
+    def worker(h):
+        st = cg.BNLayerState(gamma=gamma, beta=beta, eps=eps, running_mean=rm0,
+                             running_var=rv0, running_momentum=momentum)
+        y, cache = cg.sync_bn_forward(h, xs_t[h.rank], st, one_pass=one_pass, relu=relu)
+        out = dict(y=y, mu=cache.mu, var=cache.var, m=cache.total_count,
+                   running_mean=st.running_mean, running_var=st.running_var,
+                   x_hat=cache.x_hat)
+        if dys_t is not None:
+            dx, dgamma, dbeta = cg.sync_bn_backward(h, dys_t[h.rank], cache, st)
+            out.update(dx=dx, dgamma=dgamma, dbeta=dbeta)
+        return {k: (v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else v)
+                for k, v in out.items()}
+
+    return cg.DeviceGroup(world, bn_group_size=g, timeout_s=60.0).run(worker)
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_golden_parity(name):
+    meta, a = load_case(name)
+    world = meta["world"]
+    xs = [a[f"x_{r}"] for r in range(world)]
+    dys = [a[f"dy_{r}"] for r in range(world)]
+    outs = run_group(world, meta["bn_group"], xs, dys, a["gamma"], a["beta"], meta["eps"],
+                     meta["momentum"], a["running_mean0"], a["running_var0"],
+                     meta["one_pass"], meta["relu"])
+    for r in range(world):
+        o = outs[r]
+        for key in ("y", "mu", "var", "x_hat", "running_mean", "running_var"):
+            e = O.rel_err(o[key], a[f"{key}_{r}"])
+            assert e <= TOL_FWD, (name, r, key, e)
+        for key in ("dx", "dgamma", "dbeta"):
+            e = O.rel_err(o[key], a[f"{key}_{r}"])
+            assert e <= TOL_BWD, (name, r, key, e)
+        assert o["m"] == int(a[f"m_{r}"])
+
+
+@pytest.mark.parametrize("name", ["config1_mini", "hw49", "relu", "two_d"])
+def test_golden_parity_channels_last(name):
+    meta, a = load_case(name)
+    if len(meta["shapes"][0]) != 4:
+        pytest.skip("2-D input has no channels_last form")
+    world = meta["world"]
+    outs = run_group(world, meta["bn_group"], [a[f"x_{r}"] for r in range(world)],
+                     [a[f"dy_{r}"] for r in range(world)], a["gamma"], a["beta"], meta["eps"],
+                     meta["momentum"], a["running_mean0"], a["running_var0"],
+                     meta["one_pass"], meta["relu"], channels_last=True)
+    for r in range(world):
+        for key in ("y", "mu", "var"):
+            assert O.rel_err(outs[r][key], a[f"{key}_{r}"]) <= TOL_FWD
+        for key in ("dx", "dgamma", "dbeta"):
+            assert O.rel_err(outs[r][key], a[f"{key}_{r}"]) <= TOL_BWD
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_golden_eval(name):
+    meta, a = load_case(name)
+    dev = _dev()
+    st = cg.BNLayerState(gamma=a["gamma"], beta=a["beta"], eps=meta["eps"],
+                         running_mean=a["running_mean_0"].astype(np.float32),
+                         running_var=a["running_var_0"].astype(np.float32),
+                         running_momentum=meta["momentum"])
+    rm_before = st.running_mean.clone()
+    y, cache = cg.bn_forward_local(torch.from_numpy(a["x_0"]).to(dev), st, mode="eval")
+    assert O.rel_err(y.cpu().numpy(), a["eval_y_0"]) <= TOL_FWD
+    assert torch.equal(st.running_mean, rm_before)  # eval leaves the state untouched
+    assert cache.train is False
+    with pytest.raises(cg.BatchNormError, match="training-mode"):
+        cg.bn_backward_local(torch.from_numpy(a["x_0"]).to(dev), cache, st)
+
+
+def _oracle_case(shapes, seed, loc=0.0, g=None, relu=False):
+    rng = np.random.default_rng(seed)
+    c = shapes[0][1]
+    xs = [(loc + rng.standard_normal(s)).astype(np.float32) for s in shapes]
+    dys = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    beta = rng.standard_normal(c).astype(np.float32)
+    g = len(shapes) if g is None else g
+    ref = O.cgbn_world([x.astype(np.float64) for x in xs], gamma.astype(np.float64),
+                       beta.astype(np.float64), g, relu=relu,
+                       dys=[d.astype(np.float64) for d in dys])
+    return xs, dys, gamma, beta, g, ref
+
+
+@pytest.mark.parametrize("shape,world,loc", [
+    ((2, 64, 56, 56), 4, 0.0),     # config 1: 4 simulated devices on one GPU
+    ((1, 2048, 7, 7), 8, 0.0),     # config 5 shape, G=8 emulated
+    ((2, 256, 13, 21), 2, 0.0),    # FPN P6, HW % 4 == 1
+    ((2, 256, 25, 42), 2, 3.0),    # FPN P5, HW % 4 == 2, shifted mean
+    ((4, 128, 28, 28), 2, 0.0),
+    ((2, 64, 56, 56), 2, 1000.0),  # adversarial mean (|mu| >> sigma)
+])
+def test_oracle_parity_shapes(shape, world, loc):
+    xs, dys, gamma, beta, g, ref = _oracle_case([shape] * world, seed=sum(shape) + world,
+                                                loc=loc)
+    outs = run_group(world, g, xs, dys, gamma, beta)
+    for r in range(world):
+        for key in ("y", "mu", "var", "running_mean", "running_var"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_FWD, (key, r)
+        for key in ("dx", "dgamma", "dbeta"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_BWD, (key, r)
+
+
+def test_relu_fused_parity_config1():
+    xs, dys, gamma, beta, g, ref = _oracle_case([(2, 64, 56, 56)] * 4, seed=7, relu=True)
+    outs = run_group(4, g, xs, dys, gamma, beta, relu=True)
+    for r in range(4):
+        assert O.rel_err(outs[r]["y"], ref[r]["y"]) <= TOL_FWD
+        assert O.rel_err(outs[r]["dx"], ref[r]["dx"]) <= TOL_BWD
+        assert O.rel_err(outs[r]["dgamma"], ref[r]["dgamma"]) <= TOL_BWD
+
+
+def test_stats_bitwise_identical_across_ranks():
+    # test_batchnorm.py:233-239, 277-287, 398-412
+    xs, dys, gamma, beta, g, _ = _oracle_case(
+        [(3, 32, 9, 9), (1, 32, 9, 9), (2, 32, 9, 9), (4, 32, 9, 9)], seed=42)
+    outs = run_group(4, 4, xs, dys, gamma, beta)
+    for r in range(1, 4):
+        for key in ("mu", "var", "running_mean", "running_var", "dgamma", "dbeta"):
+            assert np.array_equal(outs[r][key], outs[0][key]), key
+
+
+def test_subgroups_isolated():
+    xs, dys, gamma, beta, _, _ = _oracle_case([(2, 8, 5, 5)] * 4, seed=61)
+    outs = run_group(4, 2, xs, dys, gamma, beta)
+    assert np.array_equal(outs[0]["dgamma"], outs[1]["dgamma"])
+    assert np.array_equal(outs[2]["dgamma"], outs[3]["dgamma"])
+    assert not np.array_equal(outs[0]["dgamma"], outs[2]["dgamma"])
+    assert not np.array_equal(outs[0]["mu"], outs[2]["mu"])
+
+
+def test_group_of_one_bitwise_equals_local():
+    # test_batchnorm.py:241-250
+    dev = _dev()
+    rng = np.random.default_rng(43)
+    x = rng.normal(size=(4, 3, 2, 2)).astype(np.float32)
+    outs = run_group(2, 1, [x, rng.normal(size=(4, 3, 2, 2)).astype(np.float32)], None,
+                     np.ones(3, np.float32), np.zeros(3, np.float32))
+    y_local, cache_local = cg.bn_forward_local(torch.from_numpy(x).to(dev),
+                                               cg.BNLayerState.create(3))
+    assert np.array_equal(outs[0]["y"], y_local.cpu().numpy())
+    assert np.array_equal(outs[0]["mu"], cache_local.mu.cpu().numpy())
+    assert np.array_equal(outs[0]["var"], cache_local.var.cpu().numpy())
+
+
+def test_run_to_run_bitwise():
+    xs, dys, gamma, beta, g, _ = _oracle_case([(8, 64, 28, 28)] * 2, seed=5)
+    a = run_group(2, 2, xs, dys, gamma, beta)
+    b = run_group(2, 2, xs, dys, gamma, beta)
+    for r in range(2):
+        for key in ("y", "mu", "var", "dx", "dgamma", "dbeta"):
+            assert np.array_equal(a[r][key], b[r][key]), key
+
+
+def test_concat_equivalence_large():
+    # Full-size property: 4 shards of [8,64,56,56] == local BN over the concatenation
+    xs, dys, gamma, beta, _, _ = _oracle_case([(8, 64, 56, 56)] * 4, seed=9)
+    outs = run_group(4, 4, xs, dys, gamma, beta)
+    one = run_group(1, 1, [np.concatenate(xs)], [np.concatenate(dys)], gamma, beta)
+    y = np.concatenate([o["y"] for o in outs])
+    dx = np.concatenate([o["dx"] for o in outs])
+    assert O.rel_err(y, one[0]["y"]) <= TOL_FWD
+    assert O.rel_err(dx, one[0]["dx"]) <= TOL_BWD
+    assert O.rel_err(outs[0]["mu"], one[0]["mu"]) <= 1e-7
+    assert O.rel_err(outs[0]["var"], one[0]["var"]) <= 1e-7
+
+
+def test_errors_match_reference():
+    dev = _dev()
+    st = cg.BNLayerState.create(3)
+    with pytest.raises(cg.BatchNormError, match="at least 2"):
+        cg.bn_forward_local(torch.ones((1, 3), device=dev), st)
+    with pytest.raises(cg.BatchNormError):
+        cg.bn_forward_local(torch.ones((4, 2), device=dev), st)  # channel mismatch
+    with pytest.raises(cg.BatchNormError):
+        cg.bn_forward_local(torch.ones((4, 3), device=dev), st, mode="test")
+    x = torch.randn(4, 3, device=dev)
+    x[1, 2] = float("nan")
+    with pytest.raises(cg.NonFiniteError):
+        cg.bn_forward_local(x, cg.BNLayerState.create(3))
+    with pytest.raises(cg.BatchNormError, match="cotangent"):
+        _, cache = cg.bn_forward_local(torch.randn(4, 3, device=dev), cg.BNLayerState.create(3))
+        cg.bn_backward_local(torch.ones((3, 3), device=dev), cache, cg.BNLayerState.create(3))
+
+    def mismatch(h):
+        c = 3 if h.rank == 0 else 4
+        return cg.sync_bn_forward(h, torch.ones((2, c), device=dev), cg.BNLayerState.create(c))
+
+    with pytest.raises(cg.CollectiveProtocolError):
+        cg.DeviceGroup(2, timeout_s=5.0).run(mismatch)
+
+    def small(h):
+        return cg.sync_bn_forward(h, torch.ones((1, 3), device=dev), cg.BNLayerState.create(3))
+
+    with pytest.raises(cg.BatchNormError, match="at least 2"):
+        cg.DeviceGroup(1).run(small)
+
+    def foreign(h):
+        _, cache = cg.bn_forward_local(torch.randn(4, 2, device=dev), cg.BNLayerState.create(2))
+        return cg.sync_bn_backward(h, torch.randn(4, 2, device=dev), cache,
+                                   cg.BNLayerState.create(2))
+
+    with pytest.raises(cg.BatchNormError):
+        cg.DeviceGroup(1).run(foreign)
+
+
+def test_allreduce_sum_ascending_fold_bitwise():
+    # collectives.py:293-295 / test_collectives.py:43-51
+    dev = _dev()
+    vals = [torch.tensor([1e16, -0.0], dtype=torch.float64, device=dev),
+            torch.tensor([1.0, -0.0], dtype=torch.float64, device=dev),
+            torch.tensor([-1e16, -0.0], dtype=torch.float64, device=dev)]
+
+    def fn(h):
+        return cg.allreduce_sum(h, cg.SCOPE_WORLD, vals[h.rank]).cpu().numpy()
+
+    outs = cg.DeviceGroup(3).run(fn)
+    for o in outs:
+        assert o[0] == 0.0 and np.signbit(o[1])
+
+
+def test_channel_primitives():
+    dev = _dev()
+    rng = np.random.default_rng(17)
+    x = rng.normal(size=(3, 2, 2, 2)).astype(np.float32)
+    st = cg.channel_sum(torch.from_numpy(x).to(dev), with_sum_sq=True)
+    cnt, s, ss = O.channel_sum(x.astype(np.float64), with_sum_sq=True)
+    assert st.count == cnt
+    assert O.rel_err(st.sum.cpu().numpy(), s) <= 1e-12
+    assert O.rel_err(st.sum_sq.cpu().numpy(), ss) <= 1e-12
+    out = cg.channel_affine(torch.from_numpy(x).to(dev), [2.0, -1.0], [0.5, 0.25])
+    want = O.channel_affine(x.astype(np.float64), [2.0, -1.0], [0.5, 0.25])
+    assert O.rel_err(out.cpu().numpy(), want) <= 1e-7
