@@ -5,10 +5,11 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude --expt-re
 PKG := paper_1711_07240_b200
 LIB := $(PKG)/libcgbn.so
 SRCS := $(PKG)/csrc/cgbn.cu
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/cgbn.h
 
 all: $(LIB)
 
-$(LIB): $(SRCS) include/cgbn.h
+$(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -shared -o $@ $(SRCS) 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
 
 sass: $(LIB)

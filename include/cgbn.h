@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CGBN_ABI_VERSION 1
+#define CGBN_ABI_VERSION 2
 
 #define CGBN_LAYOUT_NCHW 0
 #define CGBN_LAYOUT_NHWC 1
@@ -52,6 +52,7 @@ extern "C" {
 #define CGBN_OK 0
 #define CGBN_ERR_INVALID 1 /* bad argument (shape, alignment, group size, ws too small) */
 #define CGBN_ERR_CUDA 2    /* CUDA launch / runtime error */
+#define CGBN_ERR_UNSUPPORTED 3 /* fused entry point: shape/layout not eligible (use split) */
 
 #define CGBN_STATUS_NONFINITE 1u  /* NaN/Inf reached the statistics (tensor.py:59-60) */
 #define CGBN_STATUS_SMALL_COUNT 2u /* total count < 2 (batchnorm.py:133-137) */
@@ -69,10 +70,12 @@ const char* cgbn_last_error(void);
 /* Number of SMs of the current device (cached per device). */
 int cgbn_num_sms(void);
 
-/* Bytes of zero-initialised workspace the reduction kernels (cgbn_fwd_stats,
- * cgbn_bwd_reduce) need for this shape. The workspace holds per-CTA partials and
- * per-channel arrival tickets; the kernels leave the tickets at zero on exit, so one
- * zeroed buffer can be reused by every later call on the same stream. */
+/* Bytes of zero-initialised workspace every kernel entry point below needs for this
+ * shape (depends on C only). It holds per-channel arrival tickets, per-CTA partial
+ * slots and the per-channel coefficient table that connects a reduction to the
+ * elementwise pass that follows it; the kernels leave the tickets at zero on exit, so
+ * one zeroed buffer per stream can be reused by every later call on that stream
+ * (calls on one stream are ordered; concurrent streams need separate workspaces). */
 size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout);
 
 /* Forward, step 1: this rank's per-channel partial statistics.
@@ -83,9 +86,11 @@ size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout);
 int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                    double* partial, void* ws, size_t ws_bytes, void* stream);
 
-/* Forward, step 2: fold the G gathered partials (ascending rank order), finalise
- * mean/var/inv_std, update the running statistics in place, and write
- * y = gamma * (x - mean) * inv_std + beta (optionally ReLU'd).
+/* Forward, step 2 (G ranks): fold the G gathered partials (ascending rank order),
+ * finalise mean/var/inv_std, update the running statistics in place, and write
+ * y = gamma * (x - mean) * inv_std + beta (optionally ReLU'd). Two launches: a per-channel
+ * finalize kernel that writes the coefficient table into `ws`, then a memory-order
+ * elementwise pass over the whole tensor.
  * Replaces _train_forward's post-reduction half (batchnorm.py:121-143): mu/var
  * (:122-124, :128-132), the m < 2 check (:133-137), inv_std (:138), the two
  * channel_affine calls (:139-140, tensor.py:156-170) and bn_update_running
@@ -99,14 +104,24 @@ int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int lay
                        const double* const* partials, int G,
                        const float* gamma, const float* beta, double eps, double momentum,
                        float* running_mean, float* running_var, double* saved, int relu,
-                       float* y, unsigned* status, void* stream);
+                       float* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+
+/* Single-rank training forward (G == 1: bn_forward_local, batchnorm.py:147-157, or a BN
+ * group of one): the statistics kernel's last CTA per channel finalises the channel
+ * directly (no partial, no exchange), then the elementwise pass. Two launches. Same
+ * outputs and contract as cgbn_fwd_stats + cgbn_fwd_normalize with G == 1. */
+int cgbn_fwd_train_local(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                         const float* gamma, const float* beta, double eps, double momentum,
+                         float* running_mean, float* running_var, double* saved, int relu,
+                         float* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
 
 /* Eval-mode forward: y = gamma * (x - running_mean) / sqrt(running_var + eps) + beta.
  * Replaces bn_forward_local(mode="eval") (batchnorm.py:158-166); no collective and the
  * running statistics are left untouched. */
 int cgbn_fwd_eval(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                   const float* gamma, const float* beta, const float* running_mean,
-                  const float* running_var, double eps, int relu, float* y, void* stream);
+                  const float* running_var, double eps, int relu, float* y, void* ws,
+                  size_t ws_bytes, void* stream);
 
 /* Backward, step 1: this rank's partial [sum g, sum g*(x-mean)] with g = dy (times the
  * ReLU mask recomputed from x when relu != 0). Replaces the two sequential_sum_rows
@@ -115,20 +130,30 @@ int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64
                     int layout, const double* saved, const float* gamma, const float* beta,
                     int relu, double* partial, void* ws, size_t ws_bytes, void* stream);
 
-/* Backward, step 2: fold the G gathered backward partials (ascending rank order) into
- * the BN-group sums dbeta = sum g, dgamma = sum g*x_hat (identical on every rank, as in
- * batchnorm.py:203) and write dx = gamma/sqrt(var+eps)*(g - dbeta/m - x_hat*dgamma/m)
- * (batchnorm.py:204-209). As in the reference, `eps` is the backward state's eps while
- * x_hat keeps the forward's normalisation. dgamma/dbeta (C floats each) may be NULL. */
+/* Backward, step 2 (G ranks): fold the G gathered backward partials (ascending rank
+ * order) into the BN-group sums dbeta = sum g, dgamma = sum g*x_hat (identical on every
+ * rank, as in batchnorm.py:203) and write dx = gamma/sqrt(var+eps)*(g - dbeta/m -
+ * x_hat*dgamma/m) (batchnorm.py:204-209). As in the reference, `eps` is the backward
+ * state's eps while x_hat keeps the forward's normalisation. dgamma/dbeta (C floats
+ * each) may be NULL. Two launches (finalize, memory-order elementwise). */
 int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                 const double* const* partials, int G, const double* saved,
                 const float* gamma, const float* beta, double eps, int relu, float* dx,
-                float* dgamma, float* dbeta, unsigned* status, void* stream);
+                float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
+                void* stream);
+
+/* Single-rank backward (G == 1: bn_backward_local, batchnorm.py:213-218, or a BN group
+ * of one): reduce kernel that finalises each channel, then the elementwise dx pass.
+ * Same outputs as cgbn_bwd_reduce + cgbn_bwd_dx with G == 1. */
+int cgbn_bwd_local(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW,
+                   int layout, const double* saved, const float* gamma, const float* beta,
+                   double eps, int relu, float* dx, float* dgamma, float* dbeta,
+                   unsigned* status, void* ws, size_t ws_bytes, void* stream);
 
 /* x_hat = (x - mean) * inv_std from a saved forward context (the reference caches
  * x_hat in BNForwardCache, batchnorm.py:142; here it is recomputed on demand). */
 int cgbn_xhat(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
-              const double* saved, float* xhat, void* stream);
+              const double* saved, float* xhat, void* ws, size_t ws_bytes, void* stream);
 
 /* Ascending-rank fold of G device vectors of n elements (dtype CGBN_DTYPE_F32/F64):
  * out = v[0] + v[1] + ... + v[G-1], evaluated left to right. This is the arithmetic of
@@ -143,10 +168,32 @@ int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void*
 int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                      double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream);
 
-/* Per-channel affine map out = scale[c] * x + shift[c] (fp64 coefficients).
- * Device counterpart of the reference's channel_affine (tensor.py:156-170). */
+/* Per-channel affine map out = scale[c] * x + shift[c] (fp64 coefficients, device
+ * arrays of C doubles). Device counterpart of the reference's channel_affine
+ * (tensor.py:156-170). */
 int cgbn_channel_affine(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                         const double* scale, const double* shift, float* out, void* stream);
+
+/* Single-launch fused forward / backward for a single-rank group (G == 1:
+ * bn_forward_local / bn_backward_local, or a BN group of one). One cooperative kernel
+ * per direction (opt-in): the activation slice of every SM is loaded
+ * into shared memory once (cp.async, tracked by mbarriers), reduced, a grid barrier publishes the per-channel partials, and the
+ * elementwise pass reads the slice back from shared memory — x (and dy) cross HBM once
+ * (forward 8 B/elem instead of 12, backward 12 instead of 20). Same outputs and
+ * contracts as cgbn_fwd_stats + cgbn_fwd_normalize (resp. cgbn_bwd_reduce +
+ * cgbn_bwd_dx) with G == 1. Returns CGBN_ERR_UNSUPPORTED when the activation does not
+ * fit on chip or the layout is not NCHW with HW % 4 == 0 (callers then use the split
+ * entry points). cgbn_fused_supported() answers that question without launching
+ * (backward != 0: the backward variant). */
+int cgbn_fused_supported(int64_t N, int64_t C, int64_t HW, int layout, int backward);
+int cgbn_fwd_fused(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                   const float* gamma, const float* beta, double eps, double momentum,
+                   float* running_mean, float* running_var, double* saved, int relu, float* y,
+                   unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_fused(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                   const double* saved, const float* gamma, const float* beta, double eps,
+                   int relu, float* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
+                   size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ MAX_GROUP = 64
 OK = 0
 ERR_INVALID = 1
 ERR_CUDA = 2
+ERR_UNSUPPORTED = 3
 STATUS_NONFINITE = 1
 STATUS_SMALL_COUNT = 2
 DTYPE_F32 = 0
@@ -42,15 +43,24 @@ SIGNATURES = {
     "cgbn_workspace_bytes": (_sz, [_i64, _i64, _i64, _i]),
     "cgbn_fwd_stats": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _sz, _p]),
     "cgbn_fwd_normalize": (_i, [_p, _i64, _i64, _i64, _i, _pp, _i, _p, _p, _d, _d, _p, _p, _p,
-                                _i, _p, _p, _p]),
-    "cgbn_fwd_eval": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p, _d, _i, _p, _p]),
+                                _i, _p, _p, _p, _sz, _p]),
+    "cgbn_fwd_train_local": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _d, _d, _p, _p, _p, _i, _p,
+                                  _p, _p, _sz, _p]),
+    "cgbn_fwd_eval": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p, _d, _i, _p, _p, _sz, _p]),
     "cgbn_bwd_reduce": (_i, [_p, _p, _i64, _i64, _i64, _i, _p, _p, _p, _i, _p, _p, _sz, _p]),
-    "cgbn_bwd_dx": (_i, [_p, _p, _i64, _i64, _i64, _i, _pp, _i, _p, _p, _p, _d, _i, _p, _p,
-                         _p, _p, _p]),
-    "cgbn_xhat": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p]),
+    "cgbn_bwd_dx": (_i, [_p, _p, _i64, _i64, _i64, _i, _pp, _i, _p, _p, _p, _d, _i, _p, _p, _p,
+                         _p, _p, _sz, _p]),
+    "cgbn_bwd_local": (_i, [_p, _p, _i64, _i64, _i64, _i, _p, _p, _p, _d, _i, _p, _p, _p, _p, _p,
+                            _sz, _p]),
+    "cgbn_xhat": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
     "cgbn_fold_sum": (_i, [_pp, _i, _i64, _i, _p, _p]),
     "cgbn_channel_sum": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
     "cgbn_channel_affine": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p]),
+    "cgbn_fused_supported": (_i, [_i64, _i64, _i64, _i, _i]),
+    "cgbn_fwd_fused": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _d, _d, _p, _p, _p, _i, _p, _p, _p,
+                            _sz, _p]),
+    "cgbn_bwd_fused": (_i, [_p, _p, _i64, _i64, _i64, _i, _p, _p, _p, _d, _i, _p, _p, _p, _p, _p,
+                            _sz, _p]),
 }
 
 _lib = None

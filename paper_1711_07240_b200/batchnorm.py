@@ -73,6 +73,18 @@ class _Span:
         return False
 
 
+_fused = False
+
+
+def set_fused(flag: bool) -> bool:
+    """Enable/disable the single-launch fused kernels for single-rank groups (G == 1);
+    returns the previous setting. Disabled, G == 1 runs the split two-kernel path."""
+    global _fused
+    prev = _fused
+    _fused = bool(flag)
+    return prev
+
+
 def set_strict(flag: bool) -> bool:
     """Enable/disable synchronous device-status checks; returns the previous setting."""
     global _strict
@@ -207,9 +219,10 @@ class BNForwardCache:
         g = geometry(self.x, "x", BatchNormError)
         out = same_layout_like(g)
         lib = _lib.load()
+        ws = workspace(g.x.device, lib.cgbn_workspace_bytes(g.N, g.C, g.HW, g.layout))
         _lib.check(lib.cgbn_xhat(g.x.data_ptr(), g.N, g.C, g.HW, g.layout,
-                                 self.saved.data_ptr(), out.data_ptr(),
-                                 stream_ptr(g.x.device)), "cgbn_xhat")
+                                 self.saved.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), stream_ptr(g.x.device)), "cgbn_xhat")
         return out
 
 
@@ -254,19 +267,53 @@ def _local_exchange(vec, info):
     return [vec], [info]
 
 
-def _train_forward(x, state: BNLayerState, exchange, scope_key, one_pass: bool, relu: bool,
-                   what: str):
-    """The CGBN forward (batchnorm.py:115-144): local partial -> exchange -> fold +
-    finalise + normalise + running update, all on the device."""
+def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
+                   one_pass: bool, relu: bool, what: str):
+    """The CGBN forward (batchnorm.py:115-144) on the device.
+
+    G > 1: stats kernel -> exchange of the per-rank partials -> finalize (fold + running
+    update + coefficients) and elementwise normalise. G == 1: the stats kernel finalises
+    each channel itself (cgbn_fwd_train_local), or one fused cooperative kernel when
+    enabled (set_fused) and the activation fits on chip.
+    """
     g = _check_layout(x, state)
     c = g.C
     dev = g.x.device
     lib = _lib.load()
     st = stream_ptr(dev)
-    partial = torch.empty(2 * c + 1, dtype=torch.float64, device=dev)
+    e = g.N * c * g.HW
+    saved = torch.empty(3 * c + 1, dtype=torch.float64, device=dev)
+    y = same_layout_like(g)
+    status = status_word(dev)
     nb = lib.cgbn_workspace_bytes(g.N, c, g.HW, g.layout)
     ws = workspace(dev, nb)
-    e = g.N * c * g.HW
+    rm, rv = state.running_mean.data_ptr(), state.running_var.data_ptr()
+    if group_size == 1:
+        total = g.count
+        if total < 2:
+            raise BatchNormError(
+                f"training-mode statistics need at least 2 elements per channel, got {total}")
+        if _fused and lib.cgbn_fused_supported(g.N, c, g.HW, g.layout, 0):
+            with _Span("fwd_fused", 8 * e):
+                _lib.check(lib.cgbn_fwd_fused(
+                    g.x.data_ptr(), g.N, c, g.HW, g.layout, state.gamma.data_ptr(),
+                    state.beta.data_ptr(), float(state.eps), float(state.running_momentum), rm,
+                    rv, saved.data_ptr(), int(bool(relu)), y.data_ptr(), status.data_ptr(),
+                    ws.data_ptr(), ws.numel(), st), "cgbn_fwd_fused")
+            _raise_status(what, status, total)
+            return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
+                                     relu=bool(relu), one_pass=bool(one_pass),
+                                     _total_count=total)
+        with _Span("fwd_local", 12 * e):
+            _lib.check(lib.cgbn_fwd_train_local(
+                g.x.data_ptr(), g.N, c, g.HW, g.layout, state.gamma.data_ptr(),
+                state.beta.data_ptr(), float(state.eps), float(state.running_momentum), rm, rv,
+                saved.data_ptr(), int(bool(relu)), y.data_ptr(), status.data_ptr(),
+                ws.data_ptr(), ws.numel(), st), "cgbn_fwd_train_local")
+        _raise_status(what, status, total)
+        return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
+                                 relu=bool(relu), one_pass=bool(one_pass), _total_count=total)
+    partial = torch.empty(2 * c + 1, dtype=torch.float64, device=dev)
     with _Span("fwd_stats", 4 * e):
         _lib.check(lib.cgbn_fwd_stats(g.x.data_ptr(), g.N, c, g.HW, g.layout, partial.data_ptr(),
                                       ws.data_ptr(), ws.numel(), st), "cgbn_fwd_stats")
@@ -277,16 +324,13 @@ def _train_forward(x, state: BNLayerState, exchange, scope_key, one_pass: bool, 
         if total < 2:
             raise BatchNormError(
                 f"training-mode statistics need at least 2 elements per channel, got {total}")
-    saved = torch.empty(3 * c + 1, dtype=torch.float64, device=dev)
-    y = same_layout_like(g)
-    status = status_word(dev)
     arr, keep = _lib.ptr_array([p.data_ptr() for p in parts])
     with _Span("fwd_normalize", 8 * e):
         _lib.check(lib.cgbn_fwd_normalize(
             g.x.data_ptr(), g.N, c, g.HW, g.layout, arr, len(parts), state.gamma.data_ptr(),
-            state.beta.data_ptr(), float(state.eps), float(state.running_momentum),
-            state.running_mean.data_ptr(), state.running_var.data_ptr(), saved.data_ptr(),
-            int(bool(relu)), y.data_ptr(), status.data_ptr(), st), "cgbn_fwd_normalize")
+            state.beta.data_ptr(), float(state.eps), float(state.running_momentum), rm, rv,
+            saved.data_ptr(), int(bool(relu)), y.data_ptr(), status.data_ptr(), ws.data_ptr(),
+            ws.numel(), st), "cgbn_fwd_normalize")
     _raise_status(what, status, total)
     cache = BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
                            relu=bool(relu), one_pass=bool(one_pass), _total_count=total)
@@ -302,18 +346,19 @@ def bn_forward_local(x, state: BNLayerState, mode: str = "train",
     state untouched.
     """
     if mode == "train":
-        return _train_forward(x, state, _local_exchange, None, one_pass=False, relu=relu,
+        return _train_forward(x, state, _local_exchange, 1, None, one_pass=False, relu=relu,
                               what="bn_forward_local")
     g = _check_layout(x, state)
     if mode != "eval":
         raise BatchNormError(f"mode must be 'train' or 'eval', got {mode!r}")
     lib = _lib.load()
     y = same_layout_like(g)
+    ws = workspace(g.x.device, lib.cgbn_workspace_bytes(g.N, g.C, g.HW, g.layout))
     _lib.check(lib.cgbn_fwd_eval(g.x.data_ptr(), g.N, g.C, g.HW, g.layout,
                                  state.gamma.data_ptr(), state.beta.data_ptr(),
                                  state.running_mean.data_ptr(), state.running_var.data_ptr(),
-                                 float(state.eps), int(bool(relu)), y.data_ptr(),
-                                 stream_ptr(g.x.device)), "cgbn_fwd_eval")
+                                 float(state.eps), int(bool(relu)), y.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), stream_ptr(g.x.device)), "cgbn_fwd_eval")
     c = g.C
     saved = torch.empty(3 * c + 1, dtype=torch.float64, device=g.x.device)
     saved[:c] = state.running_mean.double()
@@ -340,12 +385,15 @@ def sync_bn_forward(handle, x_local, state: BNLayerState, one_pass: bool = False
     return _train_forward(
         x_local, state,
         lambda v, info: handle.exchange(SCOPE_BN_GROUP, "bn_forward", v, info),
-        scope_key, one_pass=one_pass, relu=relu, what="sync_bn_forward")
+        handle.bn_group_size, scope_key, one_pass=one_pass, relu=relu, what="sync_bn_forward")
 
 
-def _backward_core(dy, cache: BNForwardCache, state: BNLayerState, exchange, what: str):
+def _backward_core(dy, cache: BNForwardCache, state: BNLayerState, exchange, group_size: int,
+                   what: str):
     """batchnorm.py:188-210 on the device: partial [sum g, sum g*(x-mean)] -> exchange ->
-    fold + dgamma/dbeta + dx."""
+    finalize (fold + dgamma/dbeta + dx coefficients) + elementwise dx. G == 1: the reduce
+    kernel finalises each channel itself (cgbn_bwd_local), or one fused cooperative
+    kernel when enabled (set_fused) and dy, x fit on chip."""
     if not cache.train:
         raise BatchNormError("backward requires a training-mode forward cache")
     if not isinstance(dy, torch.Tensor):
@@ -368,27 +416,47 @@ def _backward_core(dy, cache: BNForwardCache, state: BNLayerState, exchange, wha
     dev = gx.x.device
     lib = _lib.load()
     st = stream_ptr(dev)
-    partial = torch.empty(2 * c, dtype=torch.float64, device=dev)
+    e = gx.N * c * gx.HW
     nb = lib.cgbn_workspace_bytes(gx.N, c, gx.HW, gx.layout)
     ws = workspace(dev, nb)
-    e = gx.N * c * gx.HW
+    dx = same_layout_like(gx)
+    dgamma = torch.empty(c, dtype=torch.float32, device=dev)
+    dbeta = torch.empty(c, dtype=torch.float32, device=dev)
+    status = status_word(dev)
+    if group_size == 1 and _fused and lib.cgbn_fused_supported(gx.N, c, gx.HW, gx.layout, 1):
+        with _Span("bwd_fused", 12 * e):
+            _lib.check(lib.cgbn_bwd_fused(
+                gd.x.data_ptr(), gx.x.data_ptr(), gx.N, c, gx.HW, gx.layout,
+                cache.saved.data_ptr(), state.gamma.data_ptr(), state.beta.data_ptr(),
+                float(state.eps), int(cache.relu), dx.data_ptr(), dgamma.data_ptr(),
+                dbeta.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                "cgbn_bwd_fused")
+        _raise_status(what, status)
+        return dx, dgamma, dbeta
+    if group_size == 1:
+        with _Span("bwd_local", 20 * e):
+            _lib.check(lib.cgbn_bwd_local(
+                gd.x.data_ptr(), gx.x.data_ptr(), gx.N, c, gx.HW, gx.layout,
+                cache.saved.data_ptr(), state.gamma.data_ptr(), state.beta.data_ptr(),
+                float(state.eps), int(cache.relu), dx.data_ptr(), dgamma.data_ptr(),
+                dbeta.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                "cgbn_bwd_local")
+        _raise_status(what, status)
+        return dx, dgamma, dbeta
+    partial = torch.empty(2 * c, dtype=torch.float64, device=dev)
     with _Span("bwd_reduce", 8 * e):
         _lib.check(lib.cgbn_bwd_reduce(
             gd.x.data_ptr(), gx.x.data_ptr(), gx.N, c, gx.HW, gx.layout, cache.saved.data_ptr(),
             state.gamma.data_ptr(), state.beta.data_ptr(), int(cache.relu), partial.data_ptr(),
             ws.data_ptr(), ws.numel(), st), "cgbn_bwd_reduce")
-    parts, _ = exchange(partial, gx.count)
-    dx = same_layout_like(gx)
-    dgamma = torch.empty(c, dtype=torch.float32, device=dev)
-    dbeta = torch.empty(c, dtype=torch.float32, device=dev)
-    status = status_word(dev)
+    parts = exchange(partial, gx.count)[0]
     arr, keep = _lib.ptr_array([p.data_ptr() for p in parts])
     with _Span("bwd_dx", 12 * e):
         _lib.check(lib.cgbn_bwd_dx(
             gd.x.data_ptr(), gx.x.data_ptr(), gx.N, c, gx.HW, gx.layout, arr, len(parts),
             cache.saved.data_ptr(), state.gamma.data_ptr(), state.beta.data_ptr(),
             float(state.eps), int(cache.relu), dx.data_ptr(), dgamma.data_ptr(),
-            dbeta.data_ptr(), status.data_ptr(), st), "cgbn_bwd_dx")
+            dbeta.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), st), "cgbn_bwd_dx")
     _raise_status(what, status)
     return dx, dgamma, dbeta
 
@@ -397,7 +465,7 @@ def bn_backward_local(dy, cache: BNForwardCache, state: BNLayerState):
     """Backward pass matching a local training-mode forward (batchnorm.py:213-218)."""
     if cache.scope_key is not None:
         raise BatchNormError("cache came from a synchronized forward; use sync_bn_backward")
-    return _backward_core(dy, cache, state, _local_exchange, "bn_backward_local")
+    return _backward_core(dy, cache, state, _local_exchange, 1, "bn_backward_local")
 
 
 def sync_bn_backward(handle, dy_local, cache: BNForwardCache, state: BNLayerState):
@@ -412,7 +480,7 @@ def sync_bn_backward(handle, dy_local, cache: BNForwardCache, state: BNLayerStat
     return _backward_core(
         dy_local, cache, state,
         lambda v, info: handle.exchange(SCOPE_BN_GROUP, "bn_backward", v, info),
-        "sync_bn_backward")
+        handle.bn_group_size, "sync_bn_backward")
 
 
 def bn_update_running(state: BNLayerState, mu, var, count: int) -> BNLayerState:

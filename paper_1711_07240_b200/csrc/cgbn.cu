@@ -1,34 +1,40 @@
 // cgbn.cu — sm_100a kernels and the C ABI (include/cgbn.h) of the CGBN hot path.
 //
-// The path is HBM-bandwidth bound (no contraction; tensor cores do not apply), so every
-// kernel is a streaming pass over the activation with 128-bit coalesced loads, several
-// independent loads in flight per thread (predicated unrolled rounds: loads first,
-// then arithmetic), and a deterministic reduction tree.
+// The path is HBM-bandwidth bound (no contraction; tensor cores do not apply). Each BN
+// direction is a per-channel reduction followed by an elementwise pass:
 //
-// A channel's "stream" is the concatenation of its N planes (NCHW: N runs of HW floats,
-// C*HW apart), Lv vector units long. Two work decompositions, chosen per shape:
+//  * reduction kernels (statistics; backward sums) stream a channel's "stream" — its N
+//    planes of HW floats, C*HW apart in NCHW — with 128-bit loads, several independent
+//    loads in flight per thread (predicated unrolled rounds), and fp64 accumulation per
+//    element. Two work decompositions, chosen per shape:
+//      flat (channel stream > kTeamMaxLv units): persistent grid of resident CTAs; the
+//        channel-major stream is split into equal contiguous CTA slices; a channel
+//        covered by CTAs b0..b1 publishes one partial per CTA in workspace slot (b + c)
+//        and the last CTA to arrive (arrival ticket) folds the slots in index order;
+//      team (small planes): a power-of-two team of 32..256 threads owns a channel.
+//    The CTA that completes a channel also *finishes* it: for a single-rank group
+//    (G == 1) it computes mean/var/inv_std (resp. dgamma/dbeta), updates the running
+//    statistics and writes the channel's affine coefficients into a table in the
+//    workspace; for G > 1 it writes the rank partial that the group exchanges, and a
+//    small finalize kernel folds the G partials (ascending rank order) into the same
+//    table after the exchange.
+//  * elementwise kernels (normalise, dx) are a memory-order grid-stride sweep over the
+//    whole tensor in float4 units (fully coalesced for every layout — NCHW with any HW,
+//    NHWC, (N, C)), looking up each element's channel coefficients in the table.
 //
-//  * flat (Lv > kTeamMaxLv): persistent grid of at most (#SMs x resident CTAs/SM). The
-//    channel-major stream of T = C*Lv units is split into equal contiguous CTA slices;
-//    a slice may cover the tail of one channel, whole channels and the head of another
-//    ("segments"). A channel covered by CTAs b0..b1 gets one partial per CTA in
-//    workspace slot (b + c); the last CTA to arrive (arrival ticket) folds slots
-//    b0+c..b1+c in index order.
-//  * team (Lv <= kTeamMaxLv, small spatial extent): a power-of-two team of tpc threads
-//    (32..256) owns one whole channel; a CTA holds 256/tpc teams and loops over channel
-//    tiles. No cross-CTA combine at all.
-//
-// All reductions accumulate in fp64 per element and fold in a fixed order, so results
-// are bitwise run-to-run reproducible without float atomics.
+// Every reduction folds in a fixed order, so results are bitwise run-to-run
+// reproducible without float atomics, and all ranks of a group compute identical
+// statistics from the identical gathered partials.
 //
 // Reference being replaced (file:line under /root/reference/pkg/src/bigbatch):
 //   channel_sum / sequential_sum_rows      tensor.py:121-153   -> reduce kernels, StatsOp
-//   _train_forward post-reduction + affine batchnorm.py:121-143 -> affine kernels, kTrain
-//   bn_update_running                      batchnorm.py:239-252 (fused into kTrain prologue)
+//   _train_forward finalise                batchnorm.py:121-138 -> finalize_fwd_channel
+//   channel_affine (x_hat, y)              batchnorm.py:139-140, tensor.py:156-170 -> k_ew_affine
+//   bn_update_running                      batchnorm.py:239-252 (in finalize_fwd_channel)
 //   _backward_core sums                    batchnorm.py:198-201 -> reduce kernels, BwdOp
-//   _backward_core dx                      batchnorm.py:203-209 -> dx kernels
-//   allreduce_sum root fold                collectives.py:293-295 (ascending-rank fold,
-//                                          done by every consumer kernel's prologue)
+//   _backward_core dgamma/dbeta, dx        batchnorm.py:203-209 -> finalize_bwd_channel, k_ew_dx
+//   allreduce_sum root fold                collectives.py:293-295 (ascending-rank fold in
+//                                          k_finalize_* / merge_fwd_partials)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -48,10 +54,13 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kTeamMaxLv = 2048;   // channels up to this many units use team kernels
+constexpr uint32_t kTeamMaxLv = 2048;  // channels up to this many units use team kernels
 constexpr int64_t kMinElemsPerCta = 2048;
-constexpr int kMaxCtasPerSm = 8;        // 2048 threads / 256
-constexpr size_t kTicketBytes = 65536 * sizeof(unsigned);  // fixed: independent of C
+constexpr int kMaxCtasPerSm = 8;  // 2048 threads / 256
+// Workspace head: 65536 per-channel tickets (fixed size: independent of C), then 64
+// words of grid-barrier state for the fused cooperative kernels.
+constexpr size_t kTicketWords = 65536;
+constexpr size_t kTicketBytes = (kTicketWords + 64) * sizeof(unsigned);
 
 // ----------------------------------------------------------------------------------
 // Errors
@@ -78,21 +87,27 @@ int check_launch(const char* what) {
 // ----------------------------------------------------------------------------------
 // Geometry
 
-// Unsigned division by a runtime-constant divisor for n < 2^31 (Granlund-Montgomery):
-// q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
+// Unsigned 32-bit division by a runtime-constant divisor, valid for every n < 2^32
+// (Hacker's Delight round-up method): t = umulhi(n, m), q = (t + ((n - t) >> s1)) >> s2
+// with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1, s1 = min(l, 1), s2 = l - s1.
 struct FastDiv {
-  uint32_t m, l;
+  uint32_t m, s1, s2;
   void init(uint32_t d) {
-    uint32_t ll = 0;
-    while ((1ull << ll) < d) ++ll;
-    l = ll;
-    m = (uint32_t)(((1ull << 32) * ((1ull << ll) - d)) / d + 1);
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    s1 = l < 1 ? l : 1;
+    s2 = l - s1;
   }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t = __umulhi(n, m);
+    return (t + ((n - t) >> s1)) >> s2;
+  }
 };
 
-// Element offset of vector unit j of channel c: (c*HWv + j + (j / HWv) * gap) * VEC with
-// gap = (C-1)*HWv. NCHW: HWv = HW/VEC. NHWC and 2-D (N, C): HWv = 1, VEC = 1.
+// Reduction-kernel geometry. Element offset of vector unit j of channel c:
+// (c*HWv + j + (j / HWv) * gap) * VEC with gap = (C-1)*HWv. NCHW: HWv = HW/VEC.
+// NHWC and 2-D (N, C): HWv = 1, VEC = 1.
 struct Geom {
   uint32_t C;
   uint32_t Lv;        // vector units per channel stream (N*HW/VEC)
@@ -140,7 +155,7 @@ struct Parts {
 };
 
 // ----------------------------------------------------------------------------------
-// Vector load / store
+// Vector load
 
 template <int VEC>
 __device__ __forceinline__ void ldv(const float* __restrict__ p, float (&v)[VEC]) {
@@ -155,25 +170,13 @@ __device__ __forceinline__ void ldv(const float* __restrict__ p, float (&v)[VEC]
   }
 }
 
-template <int VEC>
-__device__ __forceinline__ void stv(float* __restrict__ p, const float (&v)[VEC]) {
-  if constexpr (VEC == 4) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  } else if constexpr (VEC == 2) {
-    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
-  } else {
-    *p = v[0];
-  }
-}
-
 // Loads in flight per thread per round: ~128 B for one input stream, ~128 B total for
 // two (NIN = number of input streams).
 template <int VEC, int NIN = 1>
 constexpr int unroll_for() { return (NIN == 1 || VEC == 1) ? 8 : 4; }
 
 // Visit units j = start, start+stride, ... < end of channel c in rounds of U: the U
-// (predicated) loads of a round are issued before any of them is used. The body gets
-// the unit index and recomputes its offset (cheaper than holding U 64-bit offsets).
+// (predicated) loads of a round are issued before any of them is used.
 template <int U, class Op, class Body>
 __device__ __forceinline__ void strided_rounds(const Geom& g, uint32_t c, uint32_t start,
                                                uint32_t end, uint32_t stride, const Op& op,
@@ -194,9 +197,9 @@ __device__ __forceinline__ void strided_rounds(const Geom& g, uint32_t c, uint32
 }
 
 // ----------------------------------------------------------------------------------
-// Shared per-channel arithmetic (fp64). The same inline functions are used by the
-// forward and the backward so that the ReLU mask recomputed in the backward is
-// bitwise the forward's.
+// Shared per-channel arithmetic (fp64). The same inline functions produce the forward
+// coefficients and the ReLU mask the backward recomputes, so the mask is bitwise the
+// forward's.
 
 // Chan et al. pairwise merge of (n, mean, M2) partials, folded in ascending rank order.
 __device__ __forceinline__ void merge_fwd_partials(const Parts& P, uint32_t c, uint32_t C,
@@ -232,7 +235,112 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ----------------------------------------------------------------------------------
-// Reduction ops: per-channel sums of two quantities, fp64 per element.
+// Channel finishers: the group statistics of one channel -> everything downstream.
+
+// Forward: outputs of one channel once its group (n, mean, M2) is known
+// (batchnorm.py:121-141): biased var, inv_std = 1/sqrt(var+eps), coefficient table
+// P/Q, saved statistics for the backward, running-stat update with the unbiased
+// m/(m-1) correction (batchnorm.py:239-252) and the device status word.
+struct FwdFinal {
+  const float* gamma;
+  const float* beta;
+  double eps, momentum;
+  float* rmean;  // may be null (no running update)
+  float* rvar;
+  double* saved;  // [mean C | var C | inv_std C | m]
+  double* P;      // coefficient table (null when the caller keeps the coefficients)
+  double* Q;
+  unsigned* status;
+  uint32_t C;
+};
+
+__device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
+                                                     double mean, double M2, bool write,
+                                                     double& P, double& Q) {
+  const double var = fmax(M2 / n, 0.0);
+  const double inv_std = 1.0 / sqrt(var + F.eps);
+  affine_coeffs(mean, inv_std, (double)F.gamma[c], (double)F.beta[c], P, Q);
+  if (F.P) { F.P[c] = P; F.Q[c] = Q; }
+  if (!write) return;
+  const uint32_t C = F.C;
+  F.saved[c] = mean;
+  F.saved[C + c] = var;
+  F.saved[2 * C + c] = inv_std;
+  if (c == 0) F.saved[3 * C] = n;
+  unsigned bad = 0;
+  if (!isfinite(mean) || !isfinite(var)) bad |= CGBN_STATUS_NONFINITE;
+  if (n < 2.0) bad |= CGBN_STATUS_SMALL_COUNT;
+  if (bad) {
+    if (F.status) atomicOr(F.status, bad);
+  } else if (F.rmean) {
+    const double rho = F.momentum;
+    const double unbiased = var * (n / (n - 1.0));
+    F.rmean[c] = (float)((1.0 - rho) * (double)F.rmean[c] + rho * mean);
+    F.rvar[c] = (float)((1.0 - rho) * (double)F.rvar[c] + rho * unbiased);
+  }
+}
+
+// Backward: group sums [sum g, sum g*(x-mean)] of one channel -> dbeta, dgamma
+// (group sums, identical on every rank: batchnorm.py:203) and the dx coefficient table
+// dx = A*g + B*x + Cc with A = gamma/sqrt(var+eps) (the backward state's eps,
+// batchnorm.py:205), B = -A*inv_std*dgamma/m, Cc = -A*dbeta/m - B*mean, plus the
+// forward's affine P/Q for the ReLU mask.
+struct BwdFinal {
+  const double* saved;
+  const float* gamma;
+  const float* beta;
+  double eps;
+  int relu;
+  double* A;  // coefficient table (null when the caller keeps the coefficients)
+  double* B;
+  double* Cc;
+  double* P;
+  double* Q;
+  float* dgamma;  // may be null
+  float* dbeta;
+  unsigned* status;
+  uint32_t C;
+};
+
+struct DxCoef {
+  double A, B, Cc, P, Q;
+};
+
+__device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32_t c, double sdy,
+                                                       double sdyx, bool write) {
+  const uint32_t C = F.C;
+  const double mean = F.saved[c];
+  const double inv_std = F.saved[2 * C + c];
+  const double m = F.saved[3 * C];
+  const double dbeta = sdy;
+  const double dgamma = sdyx * inv_std;
+  const double gam = (double)F.gamma[c];
+  DxCoef k;
+  k.A = gam / sqrt(F.saved[C + c] + F.eps);
+  k.B = -k.A * inv_std * (dgamma / m);
+  k.Cc = -k.A * (dbeta / m) - k.B * mean;
+  k.P = k.Q = 0.0;
+  if (F.relu) affine_coeffs(mean, inv_std, gam, (double)F.beta[c], k.P, k.Q);
+  if (F.A) {
+    F.A[c] = k.A;
+    F.B[c] = k.B;
+    F.Cc[c] = k.Cc;
+    F.P[c] = k.P;
+    F.Q[c] = k.Q;
+  }
+  if (write) {
+    if (F.dgamma) F.dgamma[c] = (float)dgamma;
+    if (F.dbeta) F.dbeta[c] = (float)dbeta;
+    if (F.status && (!isfinite(dbeta) || !isfinite(dgamma)))
+      atomicOr(F.status, CGBN_STATUS_NONFINITE);
+  }
+  return k;
+}
+
+// ----------------------------------------------------------------------------------
+// Reduction ops: per-channel fp64 sums of two quantities.
+
+enum FinishMode { kPartial = 0, kRawSums = 1, kLocalFinal = 2 };
 
 // Forward statistics: sums of d = x - K (K = first element of the channel on this rank,
 // the same for every CTA of the channel; d is exact in fp64) -> (mean, M2, count).
@@ -243,8 +351,9 @@ struct StatsOp {
   const float* __restrict__ x;
   double K;
   bool shift;
-  int mode;                   // 0: forward partial [mean | M2 | count]; 1: raw [sum | sum_sq]
-  double* __restrict__ out2;  // mode 1: sum_sq destination (may be null)
+  int mode;                   // FinishMode
+  double* __restrict__ out2;  // kRawSums: sum_sq destination (may be null)
+  FwdFinal F;                 // kLocalFinal
   struct Regs { float v[VEC]; };
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
     K = shift ? (double)__ldg(x + (size_t)c * g.HWv * VEC) : 0.0;
@@ -261,15 +370,20 @@ struct StatsOp {
   __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
                                          double* __restrict__ out) const {
     const double n = g.count;
-    if (mode == 0) {
-      const double mean = K + S1 / n;
-      const double M2 = fmax(S2 - S1 * (S1 / n), 0.0);
+    if (mode == kRawSums) {
+      out[c] = S1;
+      if (out2) out2[c] = S2;
+      return;
+    }
+    const double mean = K + S1 / n;
+    const double M2 = fmax(S2 - S1 * (S1 / n), 0.0);
+    if (mode == kPartial) {
       out[c] = mean;
       out[g.C + c] = M2;
       if (c == 0) out[2 * g.C] = n;
     } else {
-      out[c] = S1;
-      if (out2) out2[c] = S2;
+      double P, Q;
+      finalize_fwd_channel(F, c, n, mean, M2, true, P, Q);
     }
   }
 };
@@ -286,6 +400,8 @@ struct BwdOp {
   const float* __restrict__ gamma;
   const float* __restrict__ beta;
   double mean, P, Q;
+  int mode;    // kPartial or kLocalFinal
+  BwdFinal F;  // kLocalFinal
   struct Regs { float g[VEC]; float x[VEC]; };
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
     mean = saved[c];
@@ -307,8 +423,12 @@ struct BwdOp {
   }
   __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
                                          double* __restrict__ out) const {
-    out[c] = S1;
-    out[g.C + c] = S2;
+    if (mode == kPartial) {
+      out[c] = S1;
+      out[g.C + c] = S2;
+    } else {
+      finalize_bwd_channel(F, c, S1, S2, true);
+    }
   }
 };
 
@@ -418,253 +538,169 @@ k_reduce_team(Geom g, Op op, double* __restrict__ out) {
 }
 
 // ----------------------------------------------------------------------------------
-// Elementwise per-channel affine y = P[c]*x + Q[c] (fp64 coefficients and arithmetic,
-// one rounding to fp32 at the end), with the per-channel coefficient prologue chosen
-// by MODE.
+// Finalize kernels (one thread per channel): group partials -> coefficient tables.
 
-enum AffineMode { kTrain = 0, kEval = 1, kAffine = 2, kXhat = 3 };
+__global__ void k_finalize_fwd(Parts parts, FwdFinal F) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= F.C) return;
+  double n, mean, M2, P, Q;
+  merge_fwd_partials(parts, c, F.C, n, mean, M2);
+  finalize_fwd_channel(F, c, n, mean, M2, true, P, Q);
+}
 
-struct AffineArgs {
-  const float* x;
-  float* y;
-  Parts parts;
-  const float* gamma;
-  const float* beta;
-  const float* rmean_in;
-  const float* rvar_in;
-  float* rmean;
-  float* rvar;
-  double* saved;
-  const double* scale;
-  const double* shift;
-  double eps, momentum;
-  unsigned* status;
-};
-
-// `first`: the caller is the unique writer of channel c's saved statistics and
-// running-stat update.
-template <int MODE>
-__device__ __forceinline__ void affine_prologue(const Geom& g, const AffineArgs& A, uint32_t c,
-                                                bool first, double& P, double& Q) {
-  if constexpr (MODE == kTrain) {
-    double n, mean, M2;
-    merge_fwd_partials(A.parts, c, g.C, n, mean, M2);
-    const double var = fmax(M2 / n, 0.0);
-    const double inv_std = 1.0 / sqrt(var + A.eps);
-    affine_coeffs(mean, inv_std, (double)A.gamma[c], (double)A.beta[c], P, Q);
-    if (first) {
-      const uint32_t C = g.C;
-      A.saved[c] = mean;
-      A.saved[C + c] = var;
-      A.saved[2 * C + c] = inv_std;
-      if (c == 0) A.saved[3 * C] = n;
-      unsigned bad = 0;
-      if (!isfinite(mean) || !isfinite(var)) bad |= CGBN_STATUS_NONFINITE;
-      if (n < 2.0) bad |= CGBN_STATUS_SMALL_COUNT;
-      if (bad) {
-        if (A.status) atomicOr(A.status, bad);
-      } else if (A.rmean) {
-        // bn_update_running (batchnorm.py:239-252): unbiased m/(m-1) on the variance.
-        const double rho = A.momentum;
-        const double unbiased = var * (n / (n - 1.0));
-        A.rmean[c] = (float)((1.0 - rho) * (double)A.rmean[c] + rho * mean);
-        A.rvar[c] = (float)((1.0 - rho) * (double)A.rvar[c] + rho * unbiased);
-      }
-    }
-  } else if constexpr (MODE == kEval) {
-    const double inv_std = 1.0 / sqrt((double)A.rvar_in[c] + A.eps);
-    affine_coeffs((double)A.rmean_in[c], inv_std, (double)A.gamma[c], (double)A.beta[c], P, Q);
-  } else if constexpr (MODE == kAffine) {
-    P = A.scale[c];
-    Q = A.shift[c];
-  } else {  // kXhat
-    affine_coeffs(A.saved[c], A.saved[2 * g.C + c], 1.0, 0.0, P, Q);
+__global__ void k_finalize_bwd(Parts parts, BwdFinal F) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= F.C) return;
+  const uint32_t C = F.C;
+  double sdy = parts.p[0][c], sdyx = parts.p[0][C + c];
+  for (int r = 1; r < parts.G; ++r) {  // ascending rank fold (collectives.py:293-295)
+    sdy += parts.p[r][c];
+    sdyx += parts.p[r][C + c];
   }
+  finalize_bwd_channel(F, c, sdy, sdyx, true);
 }
 
-template <int VEC>
-struct LoadX {
-  static constexpr int kVec = VEC;
-  const float* __restrict__ x;
-  struct Regs { float v[VEC]; };
-  __device__ __forceinline__ void load(size_t off, Regs& r) const { ldv<VEC>(x + off * VEC, r.v); }
-};
-
-template <int VEC, bool RELU>
-__device__ __forceinline__ void affine_range(const Geom& g, const AffineArgs& A, uint32_t c,
-                                             uint32_t start, uint32_t end, uint32_t stride,
-                                             double P, double Q) {
-  constexpr int U = unroll_for<VEC, 2>();  // keeps data for the store: budget as 2 streams
-  LoadX<VEC> op{A.x};
-  float* __restrict__ y = A.y;
-  strided_rounds<U>(g, c, start, end, stride, op,
-                    [&](int, uint32_t j, const typename LoadX<VEC>::Regs& r) {
-                      float v[VEC];
-#pragma unroll
-                      for (int k = 0; k < VEC; ++k) {
-                        double t = bn_out(P, Q, r.v[k]);
-                        if (RELU) t = t > 0.0 ? t : 0.0;
-                        v[k] = (float)t;
-                      }
-                      stv<VEC>(y + voff(g, c, j) * VEC, v);
-                    });
+// Eval (batchnorm.py:158-166) and x_hat coefficient tables.
+__global__ void k_coef_eval(const float* gamma, const float* beta, const float* rmean,
+                            const float* rvar, double eps, double* P, double* Q, uint32_t C) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double inv_std = 1.0 / sqrt((double)rvar[c] + eps);
+  affine_coeffs((double)rmean[c], inv_std, (double)gamma[c], (double)beta[c], P[c], Q[c]);
 }
 
-template <int VEC, int MODE, bool RELU>
-__global__ void __launch_bounds__(kThreads, 3) k_affine_flat(Geom g, AffineArgs A) {
-  __shared__ double sP, sQ;
-  for_each_segment(g, [&](const Seg& sg) {
-    if (threadIdx.x == 0) {
-      double P, Q;
-      affine_prologue<MODE>(g, A, sg.c, sg.j0 == 0, P, Q);
-      sP = P;
-      sQ = Q;
-    }
-    __syncthreads();
-    affine_range<VEC, RELU>(g, A, sg.c, sg.j0 + threadIdx.x, sg.j1, kThreads, sP, sQ);
-    __syncthreads();  // sP/sQ are rewritten by the next segment's prologue
-  });
-}
-
-template <int VEC, int MODE, bool RELU>
-__global__ void __launch_bounds__(kThreads, 3) k_affine_team(Geom g, AffineArgs A) {
-  const uint32_t tpc = 1u << g.tpc_log2;
-  const uint32_t cpt = kThreads >> g.tpc_log2;
-  const uint32_t q = threadIdx.x & (tpc - 1);
-  const uint32_t team = threadIdx.x >> g.tpc_log2;
-  const uint32_t l = threadIdx.x & 31;
-  const uint32_t tiles = (g.C + cpt - 1) / cpt;
-  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const uint32_t c = tile * cpt + team;
-    if (c >= g.C) continue;  // whole warps (tpc >= 32) skip together
-    double P = 0.0, Q = 0.0;
-    if (l == 0) affine_prologue<MODE>(g, A, c, q == 0, P, Q);  // per warp; writer: q == 0
-    P = __shfl_sync(0xffffffffu, P, 0);
-    Q = __shfl_sync(0xffffffffu, Q, 0);
-    affine_range<VEC, RELU>(g, A, c, q, g.Lv, tpc, P, Q);
-  }
+__global__ void k_coef_xhat(const double* saved, double* P, double* Q, uint32_t C) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  affine_coeffs(saved[c], saved[2 * C + c], 1.0, 0.0, P[c], Q[c]);
 }
 
 // ----------------------------------------------------------------------------------
-// Backward dx: prologue folds the G backward partials (ascending rank order), then
-// dx = A*g + B*x + Cc with A = gamma/sqrt(var+eps), B = -A*inv_std*dgamma/m,
-// Cc = -A*dbeta/m - B*mean  (== gamma/sqrt(var+eps)*(g - dbeta/m - x_hat*dgamma/m)).
+// Memory-order elementwise kernels: grid-stride over the whole tensor in float4 units.
+// Channel of element e: NCHW (e / HW) % C, NHWC and 2-D e % C. CM (channel mode):
+// 0 = NCHW with HW % 4 == 0 (one channel per float4), 1 = NCHW per element,
+// 2 = NHWC / 2-D per element.
 
-struct DxArgs {
-  const float* dy;
-  const float* x;
-  float* dx;
-  Parts parts;
-  const double* saved;
-  const float* gamma;
-  const float* beta;
-  float* dgamma;
-  float* dbeta;
-  unsigned* status;
-  double eps;
+struct EwGeom {
+  uint32_t C, HW;
+  uint32_t n4;    // E / 4
+  uint32_t tail;  // E % 4
+  FastDiv dhw, dc;
 };
 
-struct DxCoef {
-  double A, B, Cc, P, Q;
-};
-
-template <bool RELU>
-__device__ __forceinline__ DxCoef dx_prologue(const Geom& g, const DxArgs& D, uint32_t c,
-                                              bool first) {
-  const uint32_t C = g.C;
-  double sdy = D.parts.p[0][c], sdyx = D.parts.p[0][C + c];
-  for (int r = 1; r < D.parts.G; ++r) {
-    sdy += D.parts.p[r][c];
-    sdyx += D.parts.p[r][C + c];
-  }
-  const double mean = D.saved[c];
-  const double inv_std = D.saved[2 * C + c];
-  const double m = D.saved[3 * C];
-  const double dbeta = sdy;
-  const double dgamma = sdyx * inv_std;
-  const double gam = (double)D.gamma[c];
-  DxCoef k;
-  // batchnorm.py:205: gamma / sqrt(var + eps) with the backward state's eps (x_hat
-  // itself keeps the forward's inv_std, as the reference's cached x_hat does).
-  k.A = gam / sqrt(D.saved[C + c] + D.eps);
-  k.B = -k.A * inv_std * (dgamma / m);
-  k.Cc = -k.A * (dbeta / m) - k.B * mean;
-  k.P = k.Q = 0.0;
-  if (RELU) affine_coeffs(mean, inv_std, gam, (double)D.beta[c], k.P, k.Q);
-  if (first) {
-    if (D.dgamma) D.dgamma[c] = (float)dgamma;
-    if (D.dbeta) D.dbeta[c] = (float)dbeta;
-    if (D.status && (!isfinite(dbeta) || !isfinite(dgamma)))
-      atomicOr(D.status, CGBN_STATUS_NONFINITE);
-  }
-  return k;
+template <int CM>
+__device__ __forceinline__ uint32_t chan_of(const EwGeom& g, uint32_t e) {
+  if (CM == 2) return e - g.dc.div(e) * g.C;
+  const uint32_t p = g.dhw.div(e);
+  return p - g.dc.div(p) * g.C;
 }
 
-template <int VEC>
-struct LoadGX {
-  static constexpr int kVec = VEC;
-  const float* __restrict__ dy;
-  const float* __restrict__ x;
-  struct Regs { float g[VEC]; float x[VEC]; };
-  __device__ __forceinline__ void load(size_t off, Regs& r) const {
-    ldv<VEC>(dy + off * VEC, r.g);
-    ldv<VEC>(x + off * VEC, r.x);
-  }
-};
-
-template <int VEC, bool RELU>
-__device__ __forceinline__ void dx_range(const Geom& g, const DxArgs& D, uint32_t c,
-                                         uint32_t start, uint32_t end, uint32_t stride,
-                                         const DxCoef& k) {
-  constexpr int U = unroll_for<VEC, 2>();
-  LoadGX<VEC> op{D.dy, D.x};
-  float* __restrict__ dx = D.dx;
-  strided_rounds<U>(g, c, start, end, stride, op,
-                    [&](int, uint32_t j, const typename LoadGX<VEC>::Regs& r) {
-                      float v[VEC];
+template <int CM>
+__device__ __forceinline__ void chan4(const EwGeom& g, uint32_t e, uint32_t (&c)[4]) {
+  if (CM == 0) {
+    c[0] = c[1] = c[2] = c[3] = chan_of<0>(g, e);
+  } else {
 #pragma unroll
-                      for (int e = 0; e < VEC; ++e) {
-                        double gk = (double)r.g[e];
-                        if (RELU && !(bn_out(k.P, k.Q, r.x[e]) > 0.0)) gk = 0.0;
-                        v[e] = (float)__fma_rn(k.A, gk, __fma_rn(k.B, (double)r.x[e], k.Cc));
-                      }
-                      stv<VEC>(dx + voff(g, c, j) * VEC, v);
-                    });
+    for (int k = 0; k < 4; ++k) c[k] = chan_of<CM>(g, e + k);
+  }
 }
 
-template <int VEC, bool RELU>
-__global__ void __launch_bounds__(kThreads, 3) k_dx_flat(Geom g, DxArgs D) {
-  __shared__ DxCoef sk;
-  for_each_segment(g, [&](const Seg& sg) {
-    if (threadIdx.x == 0) sk = dx_prologue<RELU>(g, D, sg.c, sg.j0 == 0);
-    __syncthreads();
-    const DxCoef k = sk;
-    dx_range<VEC, RELU>(g, D, sg.c, sg.j0 + threadIdx.x, sg.j1, kThreads, k);
-    __syncthreads();  // sk is rewritten by the next segment's prologue
-  });
-}
+constexpr int kEwU = 4;
 
-template <int VEC, bool RELU>
-__global__ void __launch_bounds__(kThreads, 3) k_dx_team(Geom g, DxArgs D) {
-  const uint32_t tpc = 1u << g.tpc_log2;
-  const uint32_t cpt = kThreads >> g.tpc_log2;
-  const uint32_t q = threadIdx.x & (tpc - 1);
-  const uint32_t team = threadIdx.x >> g.tpc_log2;
-  const uint32_t l = threadIdx.x & 31;
-  const uint32_t tiles = (g.C + cpt - 1) / cpt;
-  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const uint32_t c = tile * cpt + team;
-    if (c >= g.C) continue;
-    DxCoef k{0.0, 0.0, 0.0, 0.0, 0.0};
-    if (l == 0) k = dx_prologue<RELU>(g, D, c, q == 0);
-    k.A = __shfl_sync(0xffffffffu, k.A, 0);
-    k.B = __shfl_sync(0xffffffffu, k.B, 0);
-    k.Cc = __shfl_sync(0xffffffffu, k.Cc, 0);
-    if (RELU) {
-      k.P = __shfl_sync(0xffffffffu, k.P, 0);
-      k.Q = __shfl_sync(0xffffffffu, k.Q, 0);
+template <bool RELU, int CM>
+__global__ void __launch_bounds__(kThreads)
+k_ew_affine(EwGeom g, const float* __restrict__ x, float* __restrict__ y,
+            const double* __restrict__ P, const double* __restrict__ Q) {
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4* y4 = reinterpret_cast<float4*>(y);
+  const uint32_t stride = gridDim.x * kThreads;
+  for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < g.n4; i += kEwU * stride) {
+    float4 v[kEwU];
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u)
+      if (i + u * stride < g.n4) v[u] = __ldg(&x4[i + u * stride]);
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u) {
+      const uint32_t j = i + u * stride;
+      if (j >= g.n4) continue;
+      uint32_t c[4];
+      chan4<CM>(g, 4 * j, c);
+      float o[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      double p = 0.0, q = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (CM != 0 || k == 0) {  // CM 0: one coefficient pair serves the whole float4
+          p = __ldg(&P[c[k]]);
+          q = __ldg(&Q[c[k]]);
+        }
+        double t = __fma_rn(p, (double)o[k], q);
+        if (RELU) t = t > 0.0 ? t : 0.0;
+        o[k] = (float)t;
+      }
+      y4[j] = make_float4(o[0], o[1], o[2], o[3]);
     }
-    dx_range<VEC, RELU>(g, D, c, q, g.Lv, tpc, k);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < g.tail) {
+    const uint32_t e = 4 * g.n4 + threadIdx.x;
+    const uint32_t c = CM == 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
+    double t = __fma_rn(P[c], (double)x[e], Q[c]);
+    if (RELU) t = t > 0.0 ? t : 0.0;
+    y[e] = (float)t;
+  }
+}
+
+template <bool RELU, int CM>
+__global__ void __launch_bounds__(kThreads)
+k_ew_dx(EwGeom g, const float* __restrict__ dy, const float* __restrict__ x,
+        float* __restrict__ dx, const double* __restrict__ A, const double* __restrict__ B,
+        const double* __restrict__ Cc, const double* __restrict__ P,
+        const double* __restrict__ Q) {
+  const float4* g4 = reinterpret_cast<const float4*>(dy);
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4* d4 = reinterpret_cast<float4*>(dx);
+  const uint32_t stride = gridDim.x * kThreads;
+  for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < g.n4; i += kEwU * stride) {
+    float4 gv[kEwU], xv[kEwU];
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u)
+      if (i + u * stride < g.n4) {
+        gv[u] = __ldg(&g4[i + u * stride]);
+        xv[u] = __ldg(&x4[i + u * stride]);
+      }
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u) {
+      const uint32_t j = i + u * stride;
+      if (j >= g.n4) continue;
+      uint32_t c[4];
+      chan4<CM>(g, 4 * j, c);
+      const float gi[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+      const float xi[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+      float o[4];
+      double a = 0.0, b = 0.0, cc = 0.0, p = 0.0, q = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (CM != 0 || k == 0) {
+          a = __ldg(&A[c[k]]);
+          b = __ldg(&B[c[k]]);
+          cc = __ldg(&Cc[c[k]]);
+          if (RELU) {
+            p = __ldg(&P[c[k]]);
+            q = __ldg(&Q[c[k]]);
+          }
+        }
+        double gk = (double)gi[k];
+        if (RELU && !(bn_out(p, q, xi[k]) > 0.0)) gk = 0.0;
+        o[k] = (float)__fma_rn(a, gk, __fma_rn(b, (double)xi[k], cc));
+      }
+      d4[j] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < g.tail) {
+    const uint32_t e = 4 * g.n4 + threadIdx.x;
+    const uint32_t c = CM == 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
+    double gk = (double)dy[e];
+    if (RELU && !(bn_out(P[c], Q[c], x[e]) > 0.0)) gk = 0.0;
+    dx[e] = (float)__fma_rn(A[c], gk, __fma_rn(B[c], (double)x[e], Cc[c]));
   }
 }
 
@@ -684,6 +720,7 @@ __global__ void k_fold_sum(Parts P, int64_t n, T* __restrict__ out) {
 }  // namespace
 
 #include "cgbn_tma.cuh"
+#include "cgbn_fused.cuh"
 
 namespace {
 
@@ -705,9 +742,43 @@ int num_sms_cached() {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Workspace: fixed-size ticket array (max C), then (C + max grid) double2 slots.
+// Workspace: tickets + barrier words | (C + max grid) double2 slots | coefficient table
+// (5 x C doubles: P, Q, A, B, Cc).
+size_t slots_bytes(int64_t C, int sms) {
+  return ((size_t)C + (size_t)sms * kMaxCtasPerSm) * sizeof(double2);
+}
 size_t ws_bytes_for(int64_t C, int sms) {
-  return kTicketBytes + ((size_t)C + (size_t)sms * kMaxCtasPerSm) * sizeof(double2);
+  return kTicketBytes + slots_bytes(C, sms) + 5 * (size_t)C * sizeof(double);
+}
+
+struct WsView {
+  unsigned* tickets;
+  unsigned* bar;
+  double2* slots;
+  double* P;
+  double* Q;
+  double* A;
+  double* B;
+  double* Cc;
+};
+
+int ws_view(void* ws, size_t ws_bytes, int64_t C, WsView* v) {
+  const int sms = num_sms_cached();
+  const size_t need = ws_bytes_for(C, sms);
+  if (!ws || ws_bytes < need)
+    return set_error(CGBN_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need,
+                     ws_bytes);
+  char* b = reinterpret_cast<char*>(ws);
+  v->tickets = reinterpret_cast<unsigned*>(b);
+  v->bar = v->tickets + kTicketWords;
+  v->slots = reinterpret_cast<double2*>(b + kTicketBytes);
+  double* coef = reinterpret_cast<double*>(b + kTicketBytes + slots_bytes(C, sms));
+  v->P = coef;
+  v->Q = coef + C;
+  v->A = coef + 2 * C;
+  v->B = coef + 3 * C;
+  v->Cc = coef + 4 * C;
+  return CGBN_OK;
 }
 
 // Per-(kernel, device) caches. Keyed by the kernel's address: kernels of one signature
@@ -716,7 +787,6 @@ std::mutex g_cache_mu;
 std::map<std::pair<const void*, int>, int> g_occ_cache;
 std::map<std::pair<const void*, int>, bool> g_smem_done;
 
-// Resident CTAs of `kernel` on the whole device.
 template <class K>
 int64_t resident_ctas(K kernel) {
   int dev = 0;
@@ -739,17 +809,19 @@ int64_t resident_ctas(K kernel) {
   return (int64_t)num_sms_cached() * occ;
 }
 
-struct Plan {
-  int vec;
-  bool team;
-  bool tma;  // NCHW, HW % 4 == 0, 16-byte aligned: TMA bulk-copy kernels
-  Geom g;
-  tma::TGeom tg;
-  int64_t elems;
-};
+template <class K>
+void smem_optin(K kernel, size_t smem_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_smem_done.count(key)) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+  g_smem_done[key] = true;
+}
 
-// CGBN_PATH=tma selects the TMA streaming kernels for eligible shapes (A/B measurement);
-// the register kernels are the default (measured faster on every ResNet-50 shape).
+// CGBN_PATH=tma selects the TMA streaming statistics reductions (A/B measurement);
+// CGBN_PATH=reg disables every TMA / cp.async variant.
 int path_override() {
   static int v = -1;
   if (v < 0) {
@@ -769,11 +841,23 @@ int validate_shape(int64_t N, int64_t C, int64_t HW, int layout) {
   if (N * HW >= (1ll << 31))
     return set_error(CGBN_ERR_INVALID, "per-channel count N*HW=%lld must be < 2^31",
                      (long long)(N * HW));
+  if (N * C * HW >= (1ll << 32))
+    return set_error(CGBN_ERR_INVALID, "tensor of %lld elements exceeds 2^32",
+                     (long long)(N * C * HW));
   return CGBN_OK;
 }
 
-// `ptrs` are every activation pointer the kernel touches; the vector width is the
-// widest one that divides the plane length and the alignment of all of them.
+struct Plan {
+  int vec;
+  bool team;
+  bool tma;  // NCHW, HW % 4 == 0, 16-byte aligned, CGBN_PATH=tma
+  Geom g;
+  tma::TGeom tg;
+  int64_t elems;
+};
+
+// Reduction plan. `ptrs` are every activation pointer the kernel touches; the vector
+// width is the widest one that divides the plane length and the alignment of all.
 int make_plan(int64_t N, int64_t C, int64_t HW, int layout, const void* const* ptrs, int nptr,
               Plan* out) {
   int rc = validate_shape(N, C, HW, layout);
@@ -830,7 +914,6 @@ int fill_parts(Parts* P, const double* const* partials, int G) {
   return CGBN_OK;
 }
 
-// flat grid: resident CTAs, but no more than one CTA per kMinElemsPerCta elements.
 template <class K>
 unsigned flat_grid(K kernel, const Plan& pl) {
   int64_t grid = resident_ctas(kernel);
@@ -839,7 +922,6 @@ unsigned flat_grid(K kernel, const Plan& pl) {
   return (unsigned)(grid < 1 ? 1 : grid);
 }
 
-// team grid: one CTA per channel tile, capped at the resident CTAs.
 template <class K>
 unsigned team_grid(K kernel, const Plan& pl) {
   const int64_t cpt = kThreads >> pl.g.tpc_log2;
@@ -849,69 +931,37 @@ unsigned team_grid(K kernel, const Plan& pl) {
   return (unsigned)(grid < 1 ? 1 : grid);
 }
 
-// One-time opt-in to the large dynamic shared memory of a TMA kernel (per device).
-template <class K>
-void tma_prepare(K kernel, size_t smem_bytes = tma::kSmemBytes) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
-  std::lock_guard<std::mutex> lk(g_cache_mu);
-  if (g_smem_done.count(key)) return;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
-  g_smem_done[key] = true;
-}
-
-int ws_parts(const Plan& pl, void* ws, size_t ws_bytes, unsigned** tickets, double2** slots) {
-  const size_t need = ws_bytes_for(pl.g.C, num_sms_cached());
-  if (!ws || ws_bytes < need)
-    return set_error(CGBN_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need,
-                     ws_bytes);
-  *tickets = reinterpret_cast<unsigned*>(ws);
-  *slots = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + kTicketBytes);
-  return CGBN_OK;
-}
-
-template <class TOp>
-int launch_tma_reduce(const Plan& pl, const TOp& op, double* out, void* ws, size_t ws_bytes,
-                      cudaStream_t st) {
-  unsigned* tickets;
-  double2* slots;
-  int rc = ws_parts(pl, ws, ws_bytes, &tickets, &slots);
-  if (rc) return rc;
-  tma_prepare(tma::k_tma_reduce<TOp>);
-  tma::k_tma_reduce<TOp><<<pl.tg.grid, tma::kThreadsTma, tma::kSmemBytes, st>>>(
-      pl.tg, op, out, slots, tickets);
-  return CGBN_OK;
-}
-
 template <class Op>
-int launch_reduce(const Plan& pl, const Op& op, double* out, void* ws, size_t ws_bytes,
-                  cudaStream_t st) {
+int launch_reduce(const Plan& pl, const Op& op, double* out, const WsView& w, cudaStream_t st) {
   Geom g = pl.g;
   if (pl.team) {
     g.grid = team_grid(k_reduce_team<Op>, pl);
     k_reduce_team<Op><<<g.grid, kThreads, 0, st>>>(g, op, out);
-    return CGBN_OK;
+  } else {
+    g.grid = flat_grid(k_reduce_flat<Op>, pl);
+    k_reduce_flat<Op><<<g.grid, kThreads, 0, st>>>(g, op, out, w.slots, w.tickets);
   }
-  const size_t need = ws_bytes_for(pl.g.C, num_sms_cached());
-  if (!ws || ws_bytes < need)
-    return set_error(CGBN_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need,
-                     ws_bytes);
-  unsigned* tickets = reinterpret_cast<unsigned*>(ws);
-  double2* slots = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + kTicketBytes);
-  g.grid = flat_grid(k_reduce_flat<Op>, pl);
-  k_reduce_flat<Op><<<g.grid, kThreads, 0, st>>>(g, op, out, slots, tickets);
   return CGBN_OK;
 }
 
+template <class TOp>
+int launch_tma_reduce(const Plan& pl, const TOp& op, double* out, const WsView& w,
+                      cudaStream_t st) {
+  smem_optin(tma::k_tma_reduce<TOp>, tma::kSmemBytes);
+  tma::k_tma_reduce<TOp><<<pl.tg.grid, tma::kThreadsTma, tma::kSmemBytes, st>>>(
+      pl.tg, op, out, w.slots, w.tickets);
+  return CGBN_OK;
+}
+
+// Forward statistics in mode kPartial / kRawSums / kLocalFinal.
 template <int VEC>
 int run_stats(const Plan& pl, const float* x, bool shift, int mode, double* out, double* out2,
-              void* ws, size_t wsb, cudaStream_t st) {
-  if (VEC == 4 && pl.tma && shift && mode == 0) {
+              const FwdFinal* F, const WsView& w, cudaStream_t st) {
+  if (VEC == 4 && pl.tma && shift && mode == kPartial) {
     tma::TmaStats op;
     op.x = x;
     op.K = 0.0;
-    return launch_tma_reduce(pl, op, out, ws, wsb, st);
+    return launch_tma_reduce(pl, op, out, w, st);
   }
   StatsOp<VEC> op;
   op.x = x;
@@ -919,14 +969,15 @@ int run_stats(const Plan& pl, const float* x, bool shift, int mode, double* out,
   op.shift = shift;
   op.mode = mode;
   op.out2 = out2;
-  return launch_reduce(pl, op, out, ws, wsb, st);
+  if (F) op.F = *F;
+  return launch_reduce(pl, op, out, w, st);
 }
 
 template <int VEC, bool RELU>
 int run_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double* saved,
-                   const float* gamma, const float* beta, double* out, void* ws, size_t wsb,
-                   cudaStream_t st) {
-  if (VEC == 4 && pl.tma) {
+                   const float* gamma, const float* beta, int mode, double* out,
+                   const BwdFinal* F, const WsView& w, cudaStream_t st) {
+  if (VEC == 4 && pl.tma && mode == kPartial) {
     tma::TmaBwd<RELU> op;
     op.dy = dy;
     op.x = x;
@@ -934,7 +985,7 @@ int run_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double
     op.gamma = gamma;
     op.beta = beta;
     op.mean = op.P = op.Q = 0.0;
-    return launch_tma_reduce(pl, op, out, ws, wsb, st);
+    return launch_tma_reduce(pl, op, out, w, st);
   }
   BwdOp<VEC, RELU> op;
   op.dy = dy;
@@ -943,76 +994,223 @@ int run_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double
   op.gamma = gamma;
   op.beta = beta;
   op.mean = op.P = op.Q = 0.0;
-  return launch_reduce(pl, op, out, ws, wsb, st);
+  op.mode = mode;
+  if (F) op.F = *F;
+  return launch_reduce(pl, op, out, w, st);
 }
 
-template <int VEC, int MODE, bool RELU>
-void launch_affine_v(const Plan& pl, const AffineArgs& A, cudaStream_t st) {
-  Geom g = pl.g;
-  if (VEC == 4 && pl.tma) {
-    tma_prepare(tma::k_tma_affine<MODE, RELU>);
-    tma::k_tma_affine<MODE, RELU><<<pl.tg.grid, tma::kThreadsTma, tma::kSmemBytes, st>>>(pl.tg, A);
-    return;
-  }
-  if (pl.team) {
-    g.grid = team_grid(k_affine_team<VEC, MODE, RELU>, pl);
-    k_affine_team<VEC, MODE, RELU><<<g.grid, kThreads, 0, st>>>(g, A);
-  } else {
-    g.grid = flat_grid(k_affine_flat<VEC, MODE, RELU>, pl);
-    k_affine_flat<VEC, MODE, RELU><<<g.grid, kThreads, 0, st>>>(g, A);
+int dispatch_stats(const Plan& pl, const float* x, bool shift, int mode, double* out,
+                   double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st) {
+  switch (pl.vec) {
+    case 4: return run_stats<4>(pl, x, shift, mode, out, out2, F, w, st);
+    case 2: return run_stats<2>(pl, x, shift, mode, out, out2, F, w, st);
+    default: return run_stats<1>(pl, x, shift, mode, out, out2, F, w, st);
   }
 }
 
-template <int MODE>
-void launch_affine(const Plan& pl, const AffineArgs& A, bool relu, cudaStream_t st) {
+int dispatch_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double* saved,
+                        const float* gamma, const float* beta, bool relu, int mode, double* out,
+                        const BwdFinal* F, const WsView& w, cudaStream_t st) {
   if (relu) {
     switch (pl.vec) {
-      case 4: launch_affine_v<4, MODE, true>(pl, A, st); break;
-      case 2: launch_affine_v<2, MODE, true>(pl, A, st); break;
-      default: launch_affine_v<1, MODE, true>(pl, A, st); break;
+      case 4: return run_bwd_reduce<4, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      case 2: return run_bwd_reduce<2, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      default: return run_bwd_reduce<1, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
     }
-  } else {
-    switch (pl.vec) {
-      case 4: launch_affine_v<4, MODE, false>(pl, A, st); break;
-      case 2: launch_affine_v<2, MODE, false>(pl, A, st); break;
-      default: launch_affine_v<1, MODE, false>(pl, A, st); break;
-    }
+  }
+  switch (pl.vec) {
+    case 4: return run_bwd_reduce<4, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+    case 2: return run_bwd_reduce<2, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+    default: return run_bwd_reduce<1, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
   }
 }
 
-template <int VEC, bool RELU>
-void launch_dx_v(const Plan& pl, const DxArgs& D, cudaStream_t st) {
-  Geom g = pl.g;
-  if (VEC == 4 && pl.tma) {
-    tma_prepare(tma::k_tma_dx<RELU>);
-    tma::k_tma_dx<RELU><<<pl.tg.grid, tma::kThreadsTma, tma::kSmemBytes, st>>>(pl.tg, D);
-    return;
-  }
-  if (pl.team) {
-    g.grid = team_grid(k_dx_team<VEC, RELU>, pl);
-    k_dx_team<VEC, RELU><<<g.grid, kThreads, 0, st>>>(g, D);
+// ---- elementwise
+
+struct EwPlan {
+  EwGeom g;
+  int cm;
+};
+
+int make_ew(int64_t N, int64_t C, int64_t HW, int layout, const void* const* ptrs, int nptr,
+            EwPlan* out) {
+  int rc = validate_shape(N, C, HW, layout);
+  if (rc) return rc;
+  uintptr_t align = 0;
+  for (int k = 0; k < nptr; ++k) align |= (uintptr_t)ptrs[k];
+  if (align % 16)
+    return set_error(CGBN_ERR_INVALID, "activation pointers must be 16-byte aligned");
+  const uint64_t E = (uint64_t)N * C * HW;
+  EwGeom& g = out->g;
+  g.C = (uint32_t)C;
+  g.HW = (uint32_t)HW;
+  g.n4 = (uint32_t)(E / 4);
+  g.tail = (uint32_t)(E % 4);
+  g.dhw.init((uint32_t)HW);
+  g.dc.init((uint32_t)C);
+  if (layout == CGBN_LAYOUT_NHWC || HW == 1) out->cm = 2;
+  else out->cm = (HW % 4 == 0) ? 0 : 1;
+  return CGBN_OK;
+}
+
+template <class K>
+unsigned ew_grid(K kernel, const EwPlan& ep) {
+  int64_t grid = resident_ctas(kernel);
+  const int64_t want = ceil_div((int64_t)ep.g.n4 + 1, kThreads * kEwU);
+  if (want < grid) grid = want;
+  return (unsigned)(grid < 1 ? 1 : grid);
+}
+
+template <bool RELU, int CM>
+void launch_ew_affine_t(const EwPlan& ep, const float* x, float* y, const double* P,
+                        const double* Q, cudaStream_t st) {
+  k_ew_affine<RELU, CM><<<ew_grid(k_ew_affine<RELU, CM>, ep), kThreads, 0, st>>>(ep.g, x, y, P,
+                                                                                 Q);
+}
+
+void launch_ew_affine(const EwPlan& ep, bool relu, const float* x, float* y, const double* P,
+                      const double* Q, cudaStream_t st) {
+  if (relu) {
+    if (ep.cm == 0) launch_ew_affine_t<true, 0>(ep, x, y, P, Q, st);
+    else if (ep.cm == 1) launch_ew_affine_t<true, 1>(ep, x, y, P, Q, st);
+    else launch_ew_affine_t<true, 2>(ep, x, y, P, Q, st);
   } else {
-    g.grid = flat_grid(k_dx_flat<VEC, RELU>, pl);
-    k_dx_flat<VEC, RELU><<<g.grid, kThreads, 0, st>>>(g, D);
+    if (ep.cm == 0) launch_ew_affine_t<false, 0>(ep, x, y, P, Q, st);
+    else if (ep.cm == 1) launch_ew_affine_t<false, 1>(ep, x, y, P, Q, st);
+    else launch_ew_affine_t<false, 2>(ep, x, y, P, Q, st);
   }
 }
 
-AffineArgs empty_affine_args() {
-  AffineArgs A;
-  A.x = nullptr; A.y = nullptr;
-  A.parts.G = 0;
-  for (int r = 0; r < CGBN_MAX_GROUP; ++r) A.parts.p[r] = nullptr;
-  A.gamma = A.beta = A.rmean_in = A.rvar_in = nullptr;
-  A.rmean = A.rvar = nullptr;
-  A.saved = nullptr;
-  A.scale = A.shift = nullptr;
-  A.eps = 0.0; A.momentum = 0.0;
-  A.status = nullptr;
-  return A;
+template <bool RELU, int CM>
+void launch_ew_dx_t(const EwPlan& ep, const float* dy, const float* x, float* dx,
+                    const WsView& w, cudaStream_t st) {
+  k_ew_dx<RELU, CM><<<ew_grid(k_ew_dx<RELU, CM>, ep), kThreads, 0, st>>>(
+      ep.g, dy, x, dx, w.A, w.B, w.Cc, w.P, w.Q);
+}
+
+void launch_ew_dx(const EwPlan& ep, bool relu, const float* dy, const float* x, float* dx,
+                  const WsView& w, cudaStream_t st) {
+  if (relu) {
+    if (ep.cm == 0) launch_ew_dx_t<true, 0>(ep, dy, x, dx, w, st);
+    else if (ep.cm == 1) launch_ew_dx_t<true, 1>(ep, dy, x, dx, w, st);
+    else launch_ew_dx_t<true, 2>(ep, dy, x, dx, w, st);
+  } else {
+    if (ep.cm == 0) launch_ew_dx_t<false, 0>(ep, dy, x, dx, w, st);
+    else if (ep.cm == 1) launch_ew_dx_t<false, 1>(ep, dy, x, dx, w, st);
+    else launch_ew_dx_t<false, 2>(ep, dy, x, dx, w, st);
+  }
+}
+
+unsigned chan_blocks(int64_t C) { return (unsigned)ceil_div(C, 256); }
+
+FwdFinal make_fwd_final(int64_t C, const float* gamma, const float* beta, double eps,
+                        double momentum, float* rm, float* rv, double* saved, unsigned* status,
+                        const WsView& w) {
+  FwdFinal F;
+  F.gamma = gamma; F.beta = beta;
+  F.eps = eps; F.momentum = momentum;
+  F.rmean = rm; F.rvar = rv;
+  F.saved = saved;
+  F.P = w.P; F.Q = w.Q;
+  F.status = status;
+  F.C = (uint32_t)C;
+  return F;
+}
+
+BwdFinal make_bwd_final(int64_t C, const double* saved, const float* gamma, const float* beta,
+                        double eps, bool relu, float* dgamma, float* dbeta, unsigned* status,
+                        const WsView& w) {
+  BwdFinal F;
+  F.saved = saved; F.gamma = gamma; F.beta = beta;
+  F.eps = eps;
+  F.relu = relu ? 1 : 0;
+  F.A = w.A; F.B = w.B; F.Cc = w.Cc; F.P = w.P; F.Q = w.Q;
+  F.dgamma = dgamma; F.dbeta = dbeta;
+  F.status = status;
+  F.C = (uint32_t)C;
+  return F;
+}
+
+// ---- fused cooperative kernels (cgbn_fused.cuh)
+
+bool fused_plan(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align, int nin,
+                fused::FGeom* fg) {
+  if (path_override() == 2 || getenv("CGBN_NO_FUSED")) return false;
+  if (layout != CGBN_LAYOUT_NCHW || HW % 4 != 0 || (align % 16) != 0) return false;
+  if (validate_shape(N, C, HW, layout) != CGBN_OK) return false;
+  const int64_t L = N * HW;
+  const int64_t T4 = C * L / 4;
+  int64_t grid = ceil_div(T4, 64);
+  if (grid > num_sms_cached()) grid = num_sms_cached();
+  if (grid < 1) grid = 1;
+  const int64_t max_slice = ceil_div(T4, grid) * 4;
+  const int64_t cap = (int64_t)(fused::kDataBytes / (4 * nin));
+  if (max_slice > cap) return false;
+  if (max_slice / L + 2 > fused::kMaxSeg) return false;
+  fg->C = (uint32_t)C;
+  fg->HW = (uint32_t)HW;
+  fg->L = (uint32_t)L;
+  fg->grid = (uint32_t)grid;
+  fg->T4 = (uint64_t)T4;
+  fg->dhw.init((uint32_t)HW);
+  fg->count = (double)L;
+  return true;
+}
+
+// Cooperative grids must never interleave on one device (their grid barriers could
+// deadlock): launches from different streams of one process are chained through a
+// per-device event. Skipped under stream capture, where a graph replays in order.
+std::mutex g_coop_mu;
+cudaEvent_t g_coop_last[64] = {nullptr};
+
+template <class K, class... Args>
+int launch_cooperative(K kernel, unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  const bool chain = cap == cudaStreamCaptureStatusNone && dev >= 0 && dev < 64;
+  std::unique_lock<std::mutex> lk(g_coop_mu, std::defer_lock);
+  if (chain) {
+    lk.lock();
+    if (!g_coop_last[dev]) cudaEventCreateWithFlags(&g_coop_last[dev], cudaEventDisableTiming);
+    cudaStreamWaitEvent(st, g_coop_last[dev], 0);
+  }
+  smem_optin(kernel, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(fused::kThreadsF);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (chain) cudaEventRecord(g_coop_last[dev], st);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cooperative launch failed: %s", cudaGetErrorString(e));
+  return CGBN_OK;
 }
 
 #define CGBN_REQUIRE(cond, ...) \
   do { if (!(cond)) return set_error(CGBN_ERR_INVALID, __VA_ARGS__); } while (0)
+
+#define CGBN_TRY(expr) \
+  do { int rc_ = (expr); if (rc_) return rc_; } while (0)
+
+int check_fwd_args(const float* x, const float* y, const float* gamma, const float* beta,
+                   const double* saved, double eps, double momentum, const float* running_mean,
+                   const float* running_var) {
+  CGBN_REQUIRE(x && y && gamma && beta && saved, "forward: NULL pointer");
+  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
+  CGBN_REQUIRE(momentum >= 0.0 && momentum <= 1.0, "momentum must lie in [0, 1], got %g",
+               momentum);
+  CGBN_REQUIRE((running_mean == nullptr) == (running_var == nullptr),
+               "running_mean and running_var must both be set or both be NULL");
+  return CGBN_OK;
+}
 
 }  // namespace
 
@@ -1027,7 +1225,7 @@ int cgbn_abi_version(void) { return CGBN_ABI_VERSION; }
 #define CGBN_STR(x) CGBN_STR2(x)
 const char* cgbn_build_info(void) {
   return "cgbn sm_100a; nvcc " CGBN_STR(__CUDACC_VER_MAJOR__) "." CGBN_STR(__CUDACC_VER_MINOR__)
-         "; kThreads=256; flat+team kernels";
+         "; reduce flat/team + memory-order elementwise; fused cooperative (opt-in)";
 }
 
 const char* cgbn_last_error(void) { return g_last_error.c_str(); }
@@ -1044,15 +1242,11 @@ int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   CGBN_REQUIRE(x && partial, "cgbn_fwd_stats: NULL pointer");
   const void* ptrs[] = {x};
   Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 1, &pl);
-  if (rc) return rc;
+  CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  switch (pl.vec) {
-    case 4: rc = run_stats<4>(pl, x, true, 0, partial, nullptr, ws, ws_bytes, st); break;
-    case 2: rc = run_stats<2>(pl, x, true, 0, partial, nullptr, ws, ws_bytes, st); break;
-    default: rc = run_stats<1>(pl, x, true, 0, partial, nullptr, ws, ws_bytes, st); break;
-  }
-  if (rc) return rc;
+  CGBN_TRY(dispatch_stats(pl, x, true, kPartial, partial, nullptr, nullptr, w, st));
   return check_launch("cgbn_fwd_stats");
 }
 
@@ -1061,15 +1255,12 @@ int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layou
   CGBN_REQUIRE(x && sum, "cgbn_channel_sum: NULL pointer");
   const void* ptrs[] = {x};
   Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 1, &pl);
-  if (rc) return rc;
+  CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  switch (pl.vec) {
-    case 4: rc = run_stats<4>(pl, x, false, 1, sum, sum_sq, ws, ws_bytes, st); break;
-    case 2: rc = run_stats<2>(pl, x, false, 1, sum, sum_sq, ws, ws_bytes, st); break;
-    default: rc = run_stats<1>(pl, x, false, 1, sum, sum_sq, ws, ws_bytes, st); break;
-  }
-  if (rc) return rc;
+  pl.tma = false;
+  CGBN_TRY(dispatch_stats(pl, x, false, kRawSums, sum, sum_sq, nullptr, w, st));
   return check_launch("cgbn_channel_sum");
 }
 
@@ -1077,60 +1268,75 @@ int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int lay
                        const double* const* partials, int G, const float* gamma,
                        const float* beta, double eps, double momentum, float* running_mean,
                        float* running_var, double* saved, int relu, float* y, unsigned* status,
-                       void* stream) {
-  CGBN_REQUIRE(x && y && gamma && beta && saved, "cgbn_fwd_normalize: NULL pointer");
-  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
-  CGBN_REQUIRE(momentum >= 0.0 && momentum <= 1.0, "momentum must lie in [0, 1], got %g",
-               momentum);
-  CGBN_REQUIRE((running_mean == nullptr) == (running_var == nullptr),
-               "running_mean and running_var must both be set or both be NULL");
+                       void* ws, size_t ws_bytes, void* stream) {
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
   const void* ptrs[] = {x, y};
-  Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 2, &pl);
-  if (rc) return rc;
-  AffineArgs A = empty_affine_args();
-  rc = fill_parts(&A.parts, partials, G);
-  if (rc) return rc;
-  A.x = x; A.y = y;
-  A.gamma = gamma; A.beta = beta;
-  A.rmean = running_mean; A.rvar = running_var;
-  A.saved = saved;
-  A.eps = eps; A.momentum = momentum;
-  A.status = status;
-  launch_affine<kTrain>(pl, A, relu != 0, reinterpret_cast<cudaStream_t>(stream));
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
+  Parts parts;
+  CGBN_TRY(fill_parts(&parts, partials, G));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  k_finalize_fwd<<<chan_blocks(C), 256, 0, st>>>(parts, F);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
   return check_launch("cgbn_fwd_normalize");
+}
+
+int cgbn_fwd_train_local(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                         const float* gamma, const float* beta, double eps, double momentum,
+                         float* running_mean, float* running_var, double* saved, int relu,
+                         float* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  const void* ptrs[] = {x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
+  const void* eptrs[] = {x, y};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, eptrs, 2, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  pl.tma = false;  // the TMA reductions only emit partials
+  CGBN_TRY(dispatch_stats(pl, x, true, kLocalFinal, nullptr, nullptr, &F, w, st));
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  return check_launch("cgbn_fwd_train_local");
 }
 
 int cgbn_fwd_eval(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                   const float* gamma, const float* beta, const float* running_mean,
-                  const float* running_var, double eps, int relu, float* y, void* stream) {
+                  const float* running_var, double eps, int relu, float* y, void* ws,
+                  size_t ws_bytes, void* stream) {
   CGBN_REQUIRE(x && y && gamma && beta && running_mean && running_var,
                "cgbn_fwd_eval: NULL pointer");
   CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
   const void* ptrs[] = {x, y};
-  Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 2, &pl);
-  if (rc) return rc;
-  AffineArgs A = empty_affine_args();
-  A.x = x; A.y = y;
-  A.gamma = gamma; A.beta = beta;
-  A.rmean_in = running_mean; A.rvar_in = running_var;
-  A.eps = eps;
-  launch_affine<kEval>(pl, A, relu != 0, reinterpret_cast<cudaStream_t>(stream));
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_coef_eval<<<chan_blocks(C), 256, 0, st>>>(gamma, beta, running_mean, running_var, eps, w.P,
+                                              w.Q, (uint32_t)C);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
   return check_launch("cgbn_fwd_eval");
 }
 
 int cgbn_xhat(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
-              const double* saved, float* xhat, void* stream) {
+              const double* saved, float* xhat, void* ws, size_t ws_bytes, void* stream) {
   CGBN_REQUIRE(x && saved && xhat, "cgbn_xhat: NULL pointer");
   const void* ptrs[] = {x, xhat};
-  Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 2, &pl);
-  if (rc) return rc;
-  AffineArgs A = empty_affine_args();
-  A.x = x; A.y = xhat;
-  A.saved = const_cast<double*>(saved);
-  launch_affine<kXhat>(pl, A, false, reinterpret_cast<cudaStream_t>(stream));
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_coef_xhat<<<chan_blocks(C), 256, 0, st>>>(saved, w.P, w.Q, (uint32_t)C);
+  launch_ew_affine(ep, false, x, xhat, w.P, w.Q, st);
   return check_launch("cgbn_xhat");
 }
 
@@ -1138,13 +1344,9 @@ int cgbn_channel_affine(const float* x, int64_t N, int64_t C, int64_t HW, int la
                         const double* scale, const double* shift, float* out, void* stream) {
   CGBN_REQUIRE(x && scale && shift && out, "cgbn_channel_affine: NULL pointer");
   const void* ptrs[] = {x, out};
-  Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 2, &pl);
-  if (rc) return rc;
-  AffineArgs A = empty_affine_args();
-  A.x = x; A.y = out;
-  A.scale = scale; A.shift = shift;
-  launch_affine<kAffine>(pl, A, false, reinterpret_cast<cudaStream_t>(stream));
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
+  launch_ew_affine(ep, false, x, out, scale, shift, reinterpret_cast<cudaStream_t>(stream));
   return check_launch("cgbn_channel_affine");
 }
 
@@ -1155,59 +1357,110 @@ int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64
   CGBN_REQUIRE(!relu || (gamma && beta), "cgbn_bwd_reduce: relu needs gamma and beta");
   const void* ptrs[] = {dy, x};
   Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 2, &pl);
-  if (rc) return rc;
+  CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 2, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (relu) {
-    switch (pl.vec) {
-      case 4: rc = run_bwd_reduce<4, true>(pl, dy, x, saved, gamma, beta, partial, ws, ws_bytes, st); break;
-      case 2: rc = run_bwd_reduce<2, true>(pl, dy, x, saved, gamma, beta, partial, ws, ws_bytes, st); break;
-      default: rc = run_bwd_reduce<1, true>(pl, dy, x, saved, gamma, beta, partial, ws, ws_bytes, st); break;
-    }
-  } else {
-    switch (pl.vec) {
-      case 4: rc = run_bwd_reduce<4, false>(pl, dy, x, saved, gamma, beta, partial, ws, ws_bytes, st); break;
-      case 2: rc = run_bwd_reduce<2, false>(pl, dy, x, saved, gamma, beta, partial, ws, ws_bytes, st); break;
-      default: rc = run_bwd_reduce<1, false>(pl, dy, x, saved, gamma, beta, partial, ws, ws_bytes, st); break;
-    }
-  }
-  if (rc) return rc;
+  CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, partial,
+                               nullptr, w, st));
   return check_launch("cgbn_bwd_reduce");
 }
 
 int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                 const double* const* partials, int G, const double* saved, const float* gamma,
                 const float* beta, double eps, int relu, float* dx, float* dgamma,
-                float* dbeta, unsigned* status, void* stream) {
+                float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
   CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_dx: NULL pointer");
   CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
   CGBN_REQUIRE(!relu || beta, "cgbn_bwd_dx: relu needs beta");
   const void* ptrs[] = {dy, x, dx};
-  Plan pl;
-  int rc = make_plan(N, C, HW, layout, ptrs, 3, &pl);
-  if (rc) return rc;
-  DxArgs D;
-  rc = fill_parts(&D.parts, partials, G);
-  if (rc) return rc;
-  D.dy = dy; D.x = x; D.dx = dx;
-  D.saved = saved; D.gamma = gamma; D.beta = beta;
-  D.dgamma = dgamma; D.dbeta = dbeta; D.status = status;
-  D.eps = eps;
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 3, &ep));
+  Parts parts;
+  CGBN_TRY(fill_parts(&parts, partials, G));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (relu) {
-    switch (pl.vec) {
-      case 4: launch_dx_v<4, true>(pl, D, st); break;
-      case 2: launch_dx_v<2, true>(pl, D, st); break;
-      default: launch_dx_v<1, true>(pl, D, st); break;
-    }
-  } else {
-    switch (pl.vec) {
-      case 4: launch_dx_v<4, false>(pl, D, st); break;
-      case 2: launch_dx_v<2, false>(pl, D, st); break;
-      default: launch_dx_v<1, false>(pl, D, st); break;
-    }
-  }
+  const BwdFinal F =
+      make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
+  k_finalize_bwd<<<chan_blocks(C), 256, 0, st>>>(parts, F);
+  launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
   return check_launch("cgbn_bwd_dx");
+}
+
+int cgbn_bwd_local(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW,
+                   int layout, const double* saved, const float* gamma, const float* beta,
+                   double eps, int relu, float* dx, float* dgamma, float* dbeta,
+                   unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_local: NULL pointer");
+  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
+  CGBN_REQUIRE(!relu || beta, "cgbn_bwd_local: relu needs beta");
+  const void* ptrs[] = {dy, x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 2, &pl));
+  const void* eptrs[] = {dy, x, dx};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, eptrs, 3, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const BwdFinal F =
+      make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
+  pl.tma = false;
+  CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kLocalFinal, nullptr,
+                               &F, w, st));
+  launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
+  return check_launch("cgbn_bwd_local");
+}
+
+int cgbn_fused_supported(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
+  fused::FGeom fg;
+  return fused_plan(N, C, HW, layout, 0, backward ? 2 : 1, &fg) ? 1 : 0;
+}
+
+int cgbn_fwd_fused(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                   const float* gamma, const float* beta, double eps, double momentum,
+                   float* running_mean, float* running_var, double* saved, int relu, float* y,
+                   unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  CGBN_TRY(validate_shape(N, C, HW, layout));
+  fused::FGeom fg;
+  if (!fused_plan(N, C, HW, layout, (uintptr_t)x | (uintptr_t)y, 1, &fg))
+    return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_fwd_fused: shape/layout not eligible");
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  F.P = F.Q = nullptr;  // the fused kernel keeps its coefficients in shared memory
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CGBN_TRY(relu ? launch_cooperative(fused::k_fused_fwd<true>, fg.grid, fused::kSmemBytes, st, fg,
+                                     x, y, F, w.slots, w.bar)
+                : launch_cooperative(fused::k_fused_fwd<false>, fg.grid, fused::kSmemBytes, st,
+                                     fg, x, y, F, w.slots, w.bar));
+  return check_launch("cgbn_fwd_fused");
+}
+
+int cgbn_bwd_fused(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                   const double* saved, const float* gamma, const float* beta, double eps,
+                   int relu, float* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
+                   size_t ws_bytes, void* stream) {
+  CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_fused: NULL pointer");
+  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
+  CGBN_REQUIRE(!relu || beta, "cgbn_bwd_fused: relu needs beta");
+  CGBN_TRY(validate_shape(N, C, HW, layout));
+  fused::FGeom fg;
+  if (!fused_plan(N, C, HW, layout, (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, 2, &fg))
+    return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_bwd_fused: shape/layout not eligible");
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  BwdFinal F = make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
+  F.A = F.B = F.Cc = F.P = F.Q = nullptr;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CGBN_TRY(relu ? launch_cooperative(fused::k_fused_bwd<true>, fg.grid, fused::kSmemBytes, st, fg,
+                                     dy, x, dx, F, w.slots, w.bar)
+                : launch_cooperative(fused::k_fused_bwd<false>, fg.grid, fused::kSmemBytes, st,
+                                     fg, dy, x, dx, F, w.slots, w.bar));
+  return check_launch("cgbn_bwd_fused");
 }
 
 int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void* out,
@@ -1216,8 +1469,7 @@ int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void*
   CGBN_REQUIRE(n >= 1, "cgbn_fold_sum: n must be >= 1");
   CGBN_REQUIRE(dtype == CGBN_DTYPE_F32 || dtype == CGBN_DTYPE_F64, "unknown dtype %d", dtype);
   Parts P;
-  int rc = fill_parts(&P, reinterpret_cast<const double* const*>(vectors), G);
-  if (rc) return rc;
+  CGBN_TRY(fill_parts(&P, reinterpret_cast<const double* const*>(vectors), G));
   const int threads = 256;
   int64_t blocks = ceil_div(n, threads);
   if (blocks > (int64_t)num_sms_cached() * 8) blocks = (int64_t)num_sms_cached() * 8;

@@ -1,8 +1,11 @@
 // cgbn_tma.cuh — TMA bulk-copy streaming kernels for the CGBN hot path (sm_100a).
 //
-// Used for NCHW activations whose plane length HW is a multiple of 4 floats (every
-// plane piece is then 16-byte aligned, as cp.async.bulk requires). One persistent CTA
-// per SM: warp kConsumerWarps is the producer — one elected lane walks the CTA's slice
+// Opt-in (CGBN_PATH=tma) statistics reductions for NCHW activations whose plane length
+// HW is a multiple of 4 floats (every plane piece is then 16-byte aligned, as
+// cp.async.bulk requires). Measured against the register kernels on every ResNet-50 /
+// FPN shape they were 5-10% slower on large planes and up to 2.5x slower on 14x14
+// planes (one producer lane issuing hundreds of 784-byte bulk copies), so the register
+// kernels are the default; kept for A/B measurement. One persistent CTA per SM: warp kConsumerWarps is the producer — one elected lane walks the CTA's slice
 // of the channel-major float stream and issues 1-D bulk copies
 //   cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes
 // of plane pieces into a kStages-deep shared-memory ring (full/empty mbarrier pairs);
@@ -325,109 +328,5 @@ struct TmaBwd {
     out[C + c] = S2;
   }
 };
-
-// ---------------------------------------------------------------------------------
-// Elementwise kernels over the ring: y = P*x + Q (forward) and dx (backward); outputs
-// are written straight from registers with coalesced float4 stores.
-
-template <int MODE, bool RELU>
-__global__ void __launch_bounds__(kThreadsTma, 1) k_tma_affine(TGeom g, AffineArgs A) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double sP, sQ;
-  const Ring<1> R = ring_setup<1>(smem);
-  if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) produce<1>(g, R, A.x, A.x);
-    return;
-  }
-  // the Geom view the shared prologue expects (only C is read)
-  Geom gg;
-  gg.C = g.C;
-  ChunkWalk walk{tslice_begin(g, blockIdx.x), tslice_begin(g, blockIdx.x + 1), R.cap};
-  Chunk ch;
-  uint32_t k = 0, cur = 0xffffffffu;
-  double P = 0.0, Q = 0.0;
-  float* __restrict__ y = A.y;
-  while (walk.next(g, ch)) {
-    if (ch.c != cur) {
-      consumer_sync();  // everyone is done with the previous coefficients
-      if (threadIdx.x == 0) {
-        double p, q;
-        affine_prologue<MODE>(gg, A, ch.c, ch.w == 0, p, q);
-        sP = p;
-        sQ = q;
-      }
-      consumer_sync();
-      P = sP;
-      Q = sQ;
-      cur = ch.c;
-    }
-    const int s = (int)(k % kStages);
-    mbar_wait(&R.full[s], (k / kStages) & 1);
-    const float4* p0 = reinterpret_cast<const float4*>(R.stage(s, 0));
-    const uint32_t n4 = ch.nf >> 2;
-    for (uint32_t q = threadIdx.x; q < n4; q += kConsumers) {
-      const float4 v = p0[q];
-      float o[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        double t = bn_out(P, Q, o[e]);
-        if (RELU) t = t > 0.0 ? t : 0.0;
-        o[e] = (float)t;
-      }
-      *reinterpret_cast<float4*>(y + toff(g, cur, ch.w + 4 * q)) = make_float4(o[0], o[1], o[2], o[3]);
-    }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&R.empty[s]);
-    ++k;
-  }
-}
-
-template <bool RELU>
-__global__ void __launch_bounds__(kThreadsTma, 1) k_tma_dx(TGeom g, DxArgs D) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ DxCoef sk;
-  const Ring<2> R = ring_setup<2>(smem);
-  if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) produce<2>(g, R, D.dy, D.x);
-    return;
-  }
-  Geom gg;
-  gg.C = g.C;
-  ChunkWalk walk{tslice_begin(g, blockIdx.x), tslice_begin(g, blockIdx.x + 1), R.cap};
-  Chunk ch;
-  uint32_t k = 0, cur = 0xffffffffu;
-  DxCoef kc{0.0, 0.0, 0.0, 0.0, 0.0};
-  float* __restrict__ dx = D.dx;
-  while (walk.next(g, ch)) {
-    if (ch.c != cur) {
-      consumer_sync();
-      if (threadIdx.x == 0) sk = dx_prologue<RELU>(gg, D, ch.c, ch.w == 0);
-      consumer_sync();
-      kc = sk;
-      cur = ch.c;
-    }
-    const int s = (int)(k % kStages);
-    mbar_wait(&R.full[s], (k / kStages) & 1);
-    const float4* pg = reinterpret_cast<const float4*>(R.stage(s, 0));
-    const float4* px = reinterpret_cast<const float4*>(R.stage(s, 1));
-    const uint32_t n4 = ch.nf >> 2;
-    for (uint32_t q = threadIdx.x; q < n4; q += kConsumers) {
-      const float4 gv = pg[q], xv = px[q];
-      const float gi[4] = {gv.x, gv.y, gv.z, gv.w};
-      const float xi[4] = {xv.x, xv.y, xv.z, xv.w};
-      float o[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        double gk = (double)gi[e];
-        if (RELU && !(bn_out(kc.P, kc.Q, xi[e]) > 0.0)) gk = 0.0;
-        o[e] = (float)__fma_rn(kc.A, gk, __fma_rn(kc.B, (double)xi[e], kc.Cc));
-      }
-      *reinterpret_cast<float4*>(dx + toff(g, cur, ch.w + 4 * q)) = make_float4(o[0], o[1], o[2], o[3]);
-    }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&R.empty[s]);
-    ++k;
-  }
-}
 
 }  // namespace tma

@@ -270,3 +270,63 @@ def test_channel_primitives():
     out = cg.channel_affine(torch.from_numpy(x).to(dev), [2.0, -1.0], [0.5, 0.25])
     want = O.channel_affine(x.astype(np.float64), [2.0, -1.0], [0.5, 0.25])
     assert O.rel_err(out.cpu().numpy(), want) <= 1e-7
+
+
+def _local_run(x, dy, gamma, beta, relu=False):
+    dev = _dev()
+    st = cg.BNLayerState(gamma=gamma, beta=beta)
+    y, cache = cg.bn_forward_local(torch.from_numpy(x).to(dev), st, relu=relu)
+    dx, dgamma, dbeta = cg.bn_backward_local(torch.from_numpy(dy).to(dev), cache, st)
+    return dict(y=y.cpu().numpy(), mu=cache.mu.cpu().numpy(), var=cache.var.cpu().numpy(),
+                running_mean=st.running_mean.cpu().numpy(),
+                running_var=st.running_var.cpu().numpy(), dx=dx.cpu().numpy(),
+                dgamma=dgamma.cpu().numpy(), dbeta=dbeta.cpu().numpy())
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("shape,loc,relu", [
+    ((8, 64, 28, 28), 0.0, False),
+    ((4, 256, 14, 14), 2.0, True),
+    ((32, 128, 28, 28), 0.0, False),   # 3.2M elements: fused forward and backward
+    ((32, 64, 56, 56), -5.0, False),   # 6.4M: fused forward only (backward split)
+    ((3, 5, 4, 8), 0.0, True),         # tiny, one CTA
+])
+def test_single_rank_fused_and_split(shape, loc, relu, fused):
+    prev = cg.set_fused(fused)
+    try:
+        xs, dys, gamma, beta, _, ref = _oracle_case([shape], seed=sum(shape), loc=loc, relu=relu)
+        out = _local_run(xs[0], dys[0], gamma, beta, relu=relu)
+    finally:
+        cg.set_fused(prev)
+    for key in ("y", "mu", "var", "running_mean", "running_var"):
+        assert O.rel_err(out[key], ref[0][key]) <= TOL_FWD, key
+    for key in ("dx", "dgamma", "dbeta"):
+        assert O.rel_err(out[key], ref[0][key]) <= TOL_BWD, key
+
+
+def test_fused_eligibility():
+    from paper_1711_07240_b200 import _lib
+    _dev()
+    lib = _lib.load()
+    assert lib.cgbn_fused_supported(32, 128, 784, 0, 0) == 1
+    assert lib.cgbn_fused_supported(32, 128, 784, 0, 1) == 1
+    assert lib.cgbn_fused_supported(32, 64, 3136, 0, 0) == 1
+    assert lib.cgbn_fused_supported(32, 64, 3136, 0, 1) == 0      # 6.4M: backward too big
+    assert lib.cgbn_fused_supported(32, 256, 3136, 0, 0) == 0     # 25.7M: neither
+    assert lib.cgbn_fused_supported(32, 2048, 49, 0, 0) == 0      # HW % 4 != 0
+    assert lib.cgbn_fused_supported(32, 128, 784, 1, 0) == 0      # NHWC
+
+
+def test_fused_run_to_run_bitwise_and_matches_split_closely():
+    xs, dys, gamma, beta, _, _ = _oracle_case([(16, 96, 28, 28)], seed=77)
+    a = _local_run(xs[0], dys[0], gamma, beta)
+    b = _local_run(xs[0], dys[0], gamma, beta)
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    prev = cg.set_fused(False)
+    try:
+        s = _local_run(xs[0], dys[0], gamma, beta)
+    finally:
+        cg.set_fused(prev)
+    assert O.rel_err(a["mu"], s["mu"]) <= 1e-9
+    assert O.rel_err(a["y"], s["y"]) <= 1e-6

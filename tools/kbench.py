@@ -65,7 +65,8 @@ def run_shape(shape, iters, layout, relu):
         return lib.cgbn_fwd_normalize(b[0].data_ptr(), n, c, hw, layout, pa, 1,
                                       gamma.data_ptr(), beta.data_ptr(), 1e-5, 0.1,
                                       rm.data_ptr(), rv.data_ptr(), saved.data_ptr(), int(relu),
-                                      b[2].data_ptr(), status.data_ptr(), st)
+                                      b[2].data_ptr(), status.data_ptr(), ws.data_ptr(),
+                                      ws.numel(), st)
 
     def k_bred(b):
         return lib.cgbn_bwd_reduce(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout,
@@ -76,11 +77,41 @@ def run_shape(shape, iters, layout, relu):
         return lib.cgbn_bwd_dx(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout, pb, 1,
                                saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5,
                                int(relu), b[3].data_ptr(), dg.data_ptr(), db.data_ptr(),
-                               status.data_ptr(), st)
+                               status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+
+    def k_lfwd(b):
+        return lib.cgbn_fwd_train_local(b[0].data_ptr(), n, c, hw, layout, gamma.data_ptr(),
+                                        beta.data_ptr(), 1e-5, 0.1, rm.data_ptr(), rv.data_ptr(),
+                                        saved.data_ptr(), int(relu), b[2].data_ptr(),
+                                        status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+
+    def k_lbwd(b):
+        return lib.cgbn_bwd_local(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout,
+                                  saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5,
+                                  int(relu), b[3].data_ptr(), dg.data_ptr(), db.data_ptr(),
+                                  status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+
+    def k_ffwd(b):
+        return lib.cgbn_fwd_fused(b[0].data_ptr(), n, c, hw, layout, gamma.data_ptr(),
+                                  beta.data_ptr(), 1e-5, 0.1, rm.data_ptr(), rv.data_ptr(),
+                                  saved.data_ptr(), int(relu), b[2].data_ptr(), status.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), st)
+
+    def k_fbwd(b):
+        return lib.cgbn_bwd_fused(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout,
+                                  saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5,
+                                  int(relu), b[3].data_ptr(), dg.data_ptr(), db.data_ptr(),
+                                  status.data_ptr(), ws.data_ptr(), ws.numel(), st)
 
     out = {"shape": list(shape), "elements": e, "rotating_sets": sets}
-    for name, fn, bpe in (("fwd_stats", k_stats, 4), ("fwd_normalize", k_norm, 8),
-                          ("bwd_reduce", k_bred, 8), ("bwd_dx", k_dx, 12)):
+    kernels = [("fwd_stats", k_stats, 4), ("fwd_normalize", k_norm, 8),
+               ("bwd_reduce", k_bred, 8), ("bwd_dx", k_dx, 12),
+               ("fwd_local", k_lfwd, 12), ("bwd_local", k_lbwd, 20)]
+    if lib.cgbn_fused_supported(n, c, hw, layout, 0):
+        kernels.append(("fwd_fused", k_ffwd, 12))
+    if lib.cgbn_fused_supported(n, c, hw, layout, 1):
+        kernels.append(("bwd_fused", k_fbwd, 20))
+    for name, fn, bpe in kernels:
         for i in range(3):
             _lib.check(fn(bufs[i % sets]), name)
         torch.cuda.synchronize()
