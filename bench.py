@@ -284,6 +284,7 @@ def run_gpu_arm(args):
     else:
         handle = cg.SoloHandle(dev)
     cg.set_strict(False)
+    cg.set_fused(args.fused)
 
     shapes = resnet50_bn_shapes(32)
     elems = [numel(s) for s in shapes]
@@ -532,6 +533,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="single-launch cooperative kernels for layers that fit on chip")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

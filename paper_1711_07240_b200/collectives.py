@@ -22,7 +22,7 @@ Two transports:
   numbers, kind/length mismatch -> CollectiveProtocolError naming ranks, timeouts ->
   CollectiveTimeoutError naming the missing ranks, and abort fan-out when a worker dies.
 
-``DistGroup`` (torch.distributed, one process per GPU, NCCL over NVLink/NVSwitch):
+``DistHandle`` (torch.distributed, one process per GPU, NCCL over NVLink/NVSwitch):
   the transport is an all-gather of the fixed-size partial vector on the BN sub-group's
   communicator (contiguous rank blocks of ``bn_group_size``, collectives.py:98-126).
 """
@@ -400,11 +400,7 @@ class DistHandle(_HandleBase):
             self._validate(pg, ranks, scope_key, seq, kind, vec)
         if g == 1:
             return [vec], None
-        out = torch.empty((g, vec.numel()), dtype=vec.dtype, device=vec.device)
-        if vec.is_cuda:
-            dist.all_gather_into_tensor(out, vec.contiguous(), group=pg)
-        else:  # gloo (CPU tests of the transport)
-            dist.all_gather(list(out.unbind(0)), vec.contiguous(), group=pg)
+        out = _all_gather_rows(vec, g, pg)
         return [out[i] for i in range(g)], None
 
     def _validate(self, pg, ranks, scope_key, seq, kind, vec):
@@ -416,9 +412,7 @@ class DistHandle(_HandleBase):
         dt_id = {torch.float32: 0, torch.float64: 1}.get(vec.dtype, 2)
         meta = torch.tensor([seq, kind_id, vec.numel(), dt_id], dtype=torch.int64,
                             device=vec.device)
-        allm = torch.empty((len(ranks), 4), dtype=torch.int64, device=vec.device)
-        dist.all_gather_into_tensor(allm, meta, group=pg)
-        allm = allm.cpu().tolist()
+        allm = _all_gather_rows(meta, len(ranks), pg).cpu().tolist()
         if any(m[:2] != allm[0][:2] for m in allm):
             raise CollectiveProtocolError(
                 f"collective mismatch in {scope_key}#{seq}: per-rank (seq, kind) = "
@@ -427,6 +421,19 @@ class DistHandle(_HandleBase):
             raise CollectiveProtocolError(
                 f"{kind}[{scope_key}#{seq}]: payload mismatch across ranks ("
                 + ", ".join(f"rank {r}: len {m[2]}" for r, m in zip(ranks, allm)) + ")")
+
+
+def _all_gather_rows(vec: torch.Tensor, g: int, pg) -> torch.Tensor:
+    """(g, n) tensor whose row r is rank r's 1-D ``vec`` (NCHW: one NCCL all-gather into
+    a contiguous buffer; gloo on CPU for the transport tests)."""
+    import torch.distributed as dist
+    vec = vec.contiguous()
+    out = torch.empty((g, vec.numel()), dtype=vec.dtype, device=vec.device)
+    if vec.is_cuda:
+        dist.all_gather_into_tensor(out.view(-1), vec, group=pg)
+    else:
+        dist.all_gather(list(out.unbind(0)), vec, group=pg)
+    return out
 
 
 # ------------------------------------------------------------------------------------

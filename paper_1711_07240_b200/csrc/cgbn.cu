@@ -254,12 +254,26 @@ struct FwdFinal {
   uint32_t C;
 };
 
+// Per-channel inputs of the forward finisher (prefetchable).
+struct FwdChan {
+  float gamma, beta, rmean, rvar;
+};
+
+__device__ __forceinline__ FwdChan load_fwd_chan(const FwdFinal& F, uint32_t c) {
+  FwdChan v;
+  v.gamma = F.gamma[c];
+  v.beta = F.beta[c];
+  v.rmean = F.rmean ? F.rmean[c] : 0.f;
+  v.rvar = F.rvar ? F.rvar[c] : 0.f;
+  return v;
+}
+
 __device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
                                                      double mean, double M2, bool write,
-                                                     double& P, double& Q) {
+                                                     const FwdChan& v, double& P, double& Q) {
   const double var = fmax(M2 / n, 0.0);
   const double inv_std = 1.0 / sqrt(var + F.eps);
-  affine_coeffs(mean, inv_std, (double)F.gamma[c], (double)F.beta[c], P, Q);
+  affine_coeffs(mean, inv_std, (double)v.gamma, (double)v.beta, P, Q);
   if (F.P) { F.P[c] = P; F.Q[c] = Q; }
   if (!write) return;
   const uint32_t C = F.C;
@@ -275,9 +289,15 @@ __device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t
   } else if (F.rmean) {
     const double rho = F.momentum;
     const double unbiased = var * (n / (n - 1.0));
-    F.rmean[c] = (float)((1.0 - rho) * (double)F.rmean[c] + rho * mean);
-    F.rvar[c] = (float)((1.0 - rho) * (double)F.rvar[c] + rho * unbiased);
+    F.rmean[c] = (float)((1.0 - rho) * (double)v.rmean + rho * mean);
+    F.rvar[c] = (float)((1.0 - rho) * (double)v.rvar + rho * unbiased);
   }
+}
+
+__device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
+                                                     double mean, double M2, bool write,
+                                                     double& P, double& Q) {
+  finalize_fwd_channel(F, c, n, mean, M2, write, load_fwd_chan(F, c), P, Q);
 }
 
 // Backward: group sums [sum g, sum g*(x-mean)] of one channel -> dbeta, dgamma
@@ -306,21 +326,39 @@ struct DxCoef {
   double A, B, Cc, P, Q;
 };
 
-__device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32_t c, double sdy,
-                                                       double sdyx, bool write) {
+// Per-channel inputs of the backward finisher (prefetchable).
+struct BwdChan {
+  double mean, var, inv_std, m;
+  float gamma, beta;
+};
+
+__device__ __forceinline__ BwdChan load_bwd_chan(const BwdFinal& F, uint32_t c) {
   const uint32_t C = F.C;
-  const double mean = F.saved[c];
-  const double inv_std = F.saved[2 * C + c];
-  const double m = F.saved[3 * C];
+  BwdChan v;
+  v.mean = F.saved[c];
+  v.var = F.saved[C + c];
+  v.inv_std = F.saved[2 * C + c];
+  v.m = F.saved[3 * C];
+  v.gamma = F.gamma[c];
+  v.beta = F.relu ? F.beta[c] : 0.f;
+  return v;
+}
+
+__device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32_t c, double sdy,
+                                                       double sdyx, bool write,
+                                                       const BwdChan& v) {
+  const double mean = v.mean;
+  const double inv_std = v.inv_std;
+  const double m = v.m;
   const double dbeta = sdy;
   const double dgamma = sdyx * inv_std;
-  const double gam = (double)F.gamma[c];
+  const double gam = (double)v.gamma;
   DxCoef k;
-  k.A = gam / sqrt(F.saved[C + c] + F.eps);
+  k.A = gam / sqrt(v.var + F.eps);
   k.B = -k.A * inv_std * (dgamma / m);
   k.Cc = -k.A * (dbeta / m) - k.B * mean;
   k.P = k.Q = 0.0;
-  if (F.relu) affine_coeffs(mean, inv_std, gam, (double)F.beta[c], k.P, k.Q);
+  if (F.relu) affine_coeffs(mean, inv_std, gam, (double)v.beta, k.P, k.Q);
   if (F.A) {
     F.A[c] = k.A;
     F.B[c] = k.B;
@@ -335,6 +373,11 @@ __device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32
       atomicOr(F.status, CGBN_STATUS_NONFINITE);
   }
   return k;
+}
+
+__device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32_t c, double sdy,
+                                                       double sdyx, bool write) {
+  return finalize_bwd_channel(F, c, sdy, sdyx, write, load_bwd_chan(F, c));
 }
 
 // ----------------------------------------------------------------------------------
@@ -355,9 +398,12 @@ struct StatsOp {
   double* __restrict__ out2;  // kRawSums: sum_sq destination (may be null)
   FwdFinal F;                 // kLocalFinal
   struct Regs { float v[VEC]; };
+  struct Init { double K; };
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
     K = shift ? (double)__ldg(x + (size_t)c * g.HWv * VEC) : 0.0;
   }
+  __device__ __forceinline__ Init get_init() const { return Init{K}; }
+  __device__ __forceinline__ void set_init(const Init& i) { K = i.K; }
   __device__ __forceinline__ void load(size_t off, Regs& r) const { ldv<VEC>(x + off * VEC, r.v); }
   __device__ __forceinline__ void acc(const Regs& r, double& a, double& b) const {
 #pragma unroll
@@ -403,11 +449,14 @@ struct BwdOp {
   int mode;    // kPartial or kLocalFinal
   BwdFinal F;  // kLocalFinal
   struct Regs { float g[VEC]; float x[VEC]; };
+  struct Init { double mean; };  // finish() needs no per-channel state
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
     mean = saved[c];
     const double inv_std = saved[2 * g.C + c];
     if (RELU) affine_coeffs(mean, inv_std, (double)gamma[c], (double)beta[c], P, Q);
   }
+  __device__ __forceinline__ Init get_init() const { return Init{mean}; }
+  __device__ __forceinline__ void set_init(const Init& i) { mean = i.mean; }
   __device__ __forceinline__ void load(size_t off, Regs& r) const {
     ldv<VEC>(dy + off * VEC, r.g);
     ldv<VEC>(x + off * VEC, r.x);
@@ -447,59 +496,97 @@ __device__ __forceinline__ void reduce_range(const Geom& g, uint32_t c, uint32_t
   S2 = b[0] + b[1];
 }
 
-// flat reduction (see header): one CTA partial per segment (warp shuffle, then thread 0
-// folds the kWarps values in order), cross-CTA fold by the last CTA to arrive.
+// flat reduction (see header). A CTA's slice covers consecutive channels c0, c0+1, ...
+// (segments). Segments are processed in batches of up to kMaxSegF: first every
+// segment's data is reduced to one CTA partial (warp shuffle, thread 0 folds the
+// kWarps values in order), then the tails of all segments of the batch run in
+// parallel — thread k publishes segment k's partial in slot (b + c) and takes the
+// channel's arrival ticket (or finishes the channel directly when this CTA covers it
+// alone), and warp k (mod kWarps) of the last CTA to arrive folds the slots b0+c..b1+c
+// in index order and finishes the channel. Running the tails in parallel keeps the
+// L2 round trips of one segment from delaying the loads of the next.
+constexpr int kMaxSegF = 16;
+
 template <class Op>
 __global__ void __launch_bounds__(kThreads, 3)
 k_reduce_flat(Geom g, Op op, double* __restrict__ out, double2* __restrict__ ws,
               unsigned* __restrict__ tickets) {
   __shared__ double sa[kWarps], sb[kWarps];
-  __shared__ int s_last;
+  __shared__ double s_S1[kMaxSegF], s_S2[kMaxSegF];
+  __shared__ typename Op::Init s_init[kMaxSegF];
+  __shared__ int s_last[kMaxSegF];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  for_each_segment(g, [&](const Seg& sg) {
-    const uint32_t c = sg.c;
-    op.init(g, c);
-    double S1, S2;
-    reduce_range(g, c, sg.j0 + threadIdx.x, sg.j1, kThreads, op, S1, S2);
-    S1 = warp_sum(S1);
-    S2 = warp_sum(S2);
-    if (l == 0) { sa[w] = S1; sb[w] = S2; }
-    __syncthreads();
-    const uint64_t cbase = (uint64_t)c * g.Lv;
-    const uint32_t b0 = cta_of(g, cbase), b1 = cta_of(g, cbase + g.Lv - 1);
-    if (threadIdx.x == 0) {
-      S1 = sa[0]; S2 = sb[0];
+  const uint64_t u_beg = cta_begin(g, blockIdx.x), u_end = cta_begin(g, blockIdx.x + 1);
+  if (u_beg >= u_end) return;
+  const uint32_t c_first = (uint32_t)(u_beg / g.Lv), c_last = (uint32_t)((u_end - 1) / g.Lv);
+  for (uint32_t cb = c_first; cb <= c_last; cb += kMaxSegF) {
+    const int nseg = (int)min((uint32_t)kMaxSegF, c_last - cb + 1);
+    for (int k = 0; k < nseg; ++k) {
+      const uint32_t c = cb + k;
+      const uint64_t cbase = (uint64_t)c * g.Lv;
+      const uint32_t j0 = (uint32_t)(max(u_beg, cbase) - cbase);
+      const uint32_t j1 = (uint32_t)(min(u_end, cbase + g.Lv) - cbase);
+      op.init(g, c);
+      double S1, S2;
+      reduce_range(g, c, j0 + threadIdx.x, j1, kThreads, op, S1, S2);
+      S1 = warp_sum(S1);
+      S2 = warp_sum(S2);
+      if (l == 0) { sa[w] = S1; sb[w] = S2; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        S1 = sa[0]; S2 = sb[0];
 #pragma unroll
-      for (int i = 1; i < kWarps; ++i) { S1 += sa[i]; S2 += sb[i]; }
+        for (int i = 1; i < kWarps; ++i) { S1 += sa[i]; S2 += sb[i]; }
+        s_S1[k] = S1;
+        s_S2[k] = S2;
+        s_init[k] = op.get_init();
+      }
+      __syncthreads();
+    }
+    // tails of the batch, one thread per segment
+    if (threadIdx.x < nseg) {
+      const int k = threadIdx.x;
+      const uint32_t c = cb + k;
+      const uint64_t cbase = (uint64_t)c * g.Lv;
+      const uint32_t b0 = cta_of(g, cbase), b1 = cta_of(g, cbase + g.Lv - 1);
       int last = 0;
       if (b0 == b1) {
-        op.finish(g, c, S1, S2, out);
+        Op o = op;
+        o.set_init(s_init[k]);
+        o.finish(g, c, s_S1[k], s_S2[k], out);
       } else {
-        ws[(size_t)blockIdx.x + c] = make_double2(S1, S2);
+        ws[(size_t)blockIdx.x + c] = make_double2(s_S1[k], s_S2[k]);
         __threadfence();
         last = atomicAdd(&tickets[c], 1u) == b1 - b0;
       }
-      s_last = last;
+      s_last[k] = last;
     }
     __syncthreads();
-    if (s_last && w == 0) {
+    // folds: warp w takes segments w, w + kWarps, ... completed by this CTA
+    for (int k = w; k < nseg; k += kWarps) {
+      if (!s_last[k]) continue;
+      const uint32_t c = cb + k;
+      const uint64_t cbase = (uint64_t)c * g.Lv;
+      const uint32_t b0 = cta_of(g, cbase), b1 = cta_of(g, cbase + g.Lv - 1);
       __threadfence();
       const uint32_t cnt = b1 - b0 + 1;
       double x1 = 0.0, x2 = 0.0;
-      for (uint32_t k = l; k < cnt; k += 32) {
-        const double2 t = __ldcg(&ws[(size_t)b0 + c + k]);
+      for (uint32_t i = l; i < cnt; i += 32) {
+        const double2 t = __ldcg(&ws[(size_t)b0 + c + i]);
         x1 += t.x;
         x2 += t.y;
       }
       x1 = warp_sum(x1);
       x2 = warp_sum(x2);
       if (l == 0) {
-        op.finish(g, c, x1, x2, out);
+        Op o = op;
+        o.set_init(s_init[k]);
+        o.finish(g, c, x1, x2, out);
         tickets[c] = 0u;  // leave the workspace reusable
       }
     }
-    __syncthreads();  // sa/sb/s_last are reused by the next segment
-  });
+    __syncthreads();  // smem is reused by the next batch
+  }
 }
 
 // team reduction: 2^tpc_log2 threads per channel, 256/tpc channels per tile.

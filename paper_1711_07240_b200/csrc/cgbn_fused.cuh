@@ -208,14 +208,23 @@ k_fused_fwd(FGeom g, const float* __restrict__ x, float* __restrict__ y, FwdFina
   __shared__ SegInfo segs[kMaxSeg];
   __shared__ double sa[kWarpsF], sb[kWarpsF];
   __shared__ double segK[kMaxSeg], segP[kMaxSeg], segQ[kMaxSeg];
+  __shared__ FwdChan segV[kMaxSeg];
   __shared__ int s_ns;
   const uint32_t cap = (uint32_t)(kDataBytes / 4);
   const SliceCtx<1> sc = load_slice<1>(g, segs, qb, qbar, &s_ns, smem, cap, x, x);
+  // prefetch every per-channel input the statistics and the finisher need while the
+  // slice is in flight
+  if (threadIdx.x < sc.ns) {
+    const uint32_t c = segs[threadIdx.x].c;
+    segK[threadIdx.x] = (double)__ldg(x + (size_t)c * g.HW);
+    segV[threadIdx.x] = load_fwd_chan(F, c);
+  }
+  __syncthreads();
 
   // 2. per-segment statistics (shift K = first element of the channel on this rank)
   for (int si = 0; si < sc.ns; ++si) {
     const SegInfo sg = segs[si];
-    const double K = (double)__ldg(x + (size_t)sg.c * g.HW);
+    const double K = segK[si];
     const uint32_t len = sg.w1 - sg.w0;
     wait_range(qb, qbar, sg.s0, sg.s0 + len, sc.total);
     const float4* p = reinterpret_cast<const float4*>(smem + sg.s0);
@@ -242,10 +251,7 @@ k_fused_fwd(FGeom g, const float* __restrict__ x, float* __restrict__ y, FwdFina
     }
     double S1 = a0 + a1, S2 = b0 + b1;
     block_sum2_f(S1, S2, sa, sb);
-    if (threadIdx.x == 0) {
-      slots[(size_t)blockIdx.x + sg.c] = make_double2(S1, S2);
-      segK[si] = K;
-    }
+    if (threadIdx.x == 0) slots[(size_t)blockIdx.x + sg.c] = make_double2(S1, S2);
   }
 
   // 3. all partials of all CTAs are published
@@ -268,7 +274,7 @@ k_fused_fwd(FGeom g, const float* __restrict__ x, float* __restrict__ y, FwdFina
     const double mean = K + S1 / n;
     const double M2 = fmax(S2 - S1 * (S1 / n), 0.0);
     double P, Q;
-    finalize_fwd_channel(F, sg.c, n, mean, M2, b0 == blockIdx.x, P, Q);
+    finalize_fwd_channel(F, sg.c, n, mean, M2, b0 == blockIdx.x, segV[si], P, Q);
     segP[si] = P;
     segQ[si] = Q;
   }
@@ -306,19 +312,28 @@ k_fused_bwd(FGeom g, const float* __restrict__ dy, const float* __restrict__ x,
   __shared__ SegInfo segs[kMaxSeg];
   __shared__ double sa[kWarpsF], sb[kWarpsF];
   __shared__ double segA[kMaxSeg], segB[kMaxSeg], segC[kMaxSeg], segP[kMaxSeg], segQ[kMaxSeg];
+  __shared__ BwdChan segV[kMaxSeg];
   __shared__ int s_ns;
   const uint32_t cap = (uint32_t)(kDataBytes / 8);
   const SliceCtx<2> sc = load_slice<2>(g, segs, qb, qbar, &s_ns, smem, cap, dy, x);
+  if (threadIdx.x < sc.ns) {
+    const uint32_t c = segs[threadIdx.x].c;
+    const BwdChan v = load_bwd_chan(F, c);
+    segV[threadIdx.x] = v;
+    double P = 0.0, Q = 0.0;
+    if (RELU) affine_coeffs(v.mean, v.inv_std, (double)v.gamma, (double)v.beta, P, Q);
+    segP[threadIdx.x] = P;
+    segQ[threadIdx.x] = Q;
+  }
+  __syncthreads();
   const uint32_t C = g.C;
   const float* gs = smem;        // dy
   const float* xs = smem + cap;  // x
 
   for (int si = 0; si < sc.ns; ++si) {
     const SegInfo sg = segs[si];
-    const double mean = F.saved[sg.c];
-    const double inv_std = F.saved[2 * C + sg.c];
-    double P = 0.0, Q = 0.0;
-    if (RELU) affine_coeffs(mean, inv_std, (double)F.gamma[sg.c], (double)F.beta[sg.c], P, Q);
+    const double mean = segV[si].mean;
+    const double P = segP[si], Q = segQ[si];
     const uint32_t len = sg.w1 - sg.w0;
     wait_range(qb, qbar, sg.s0, sg.s0 + len, sc.total);
     const float4* pg = reinterpret_cast<const float4*>(gs + sg.s0);
@@ -361,7 +376,7 @@ k_fused_bwd(FGeom g, const float* __restrict__ dy, const float* __restrict__ x,
       sdy += t.x;
       sdyx += t.y;
     }
-    const DxCoef k = finalize_bwd_channel(F, c, sdy, sdyx, b0 == blockIdx.x);
+    const DxCoef k = finalize_bwd_channel(F, c, sdy, sdyx, b0 == blockIdx.x, segV[si]);
     segA[si] = k.A;
     segB[si] = k.B;
     segC[si] = k.Cc;

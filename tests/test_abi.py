@@ -1,0 +1,74 @@
+"""The C-ABI library loads and exports every symbol include/cgbn.h declares (no GPU
+needed: nothing here launches a kernel)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1711_07240_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cgbn.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int|size_t|const char\*)\s+(cgbn_\w+)\(", text, re.M)))
+
+
+def test_header_declares_the_hot_path():
+    syms = declared_symbols()
+    for name in ("cgbn_fwd_stats", "cgbn_fwd_normalize", "cgbn_fwd_train_local",
+                 "cgbn_bwd_reduce", "cgbn_bwd_dx", "cgbn_bwd_local", "cgbn_fwd_eval",
+                 "cgbn_fold_sum", "cgbn_workspace_bytes", "cgbn_last_error"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_binding_table_matches_header():
+    assert sorted(_lib.SIGNATURES) == declared_symbols()
+
+
+def test_constants_match_header():
+    text = open(HEADER).read()
+
+    def define(name):
+        return int(re.search(rf"#define {name}\s+(\d+)", text).group(1))
+
+    assert define("CGBN_LAYOUT_NCHW") == _lib.LAYOUT_NCHW
+    assert define("CGBN_LAYOUT_NHWC") == _lib.LAYOUT_NHWC
+    assert define("CGBN_MAX_GROUP") == _lib.MAX_GROUP
+    assert define("CGBN_ERR_INVALID") == _lib.ERR_INVALID
+    assert define("CGBN_ERR_UNSUPPORTED") == _lib.ERR_UNSUPPORTED
+    assert define("CGBN_STATUS_NONFINITE") == _lib.STATUS_NONFINITE
+    assert define("CGBN_STATUS_SMALL_COUNT") == _lib.STATUS_SMALL_COUNT
+
+
+def test_abi_version_and_argument_validation_without_gpu():
+    lib = _lib.load()
+    assert lib.cgbn_abi_version() == 2
+    assert b"sm_100a" in lib.cgbn_build_info()
+    # invalid shapes are rejected on the host before any CUDA call
+    rc = lib.cgbn_fwd_stats(None, 2, 3, 4, 0, None, None, 0, None)
+    assert rc == _lib.ERR_INVALID
+    assert b"NULL" in lib.cgbn_last_error()
+    rc = lib.cgbn_fwd_stats(1, 0, 3, 4, 0, 1, None, 0, None)
+    assert rc == _lib.ERR_INVALID
+    assert b"positive" in lib.cgbn_last_error()
+    rc = lib.cgbn_fwd_stats(1, 2, 70000, 4, 0, 1, None, 0, None)
+    assert rc == _lib.ERR_INVALID
+    assert b"65535" in lib.cgbn_last_error()
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(_lib.CGBNLibraryError, match="no CPU fallback"):
+        _lib.load()

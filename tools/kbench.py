@@ -24,10 +24,12 @@ from paper_1711_07240_b200 import _lib  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 
 
-def run_shape(shape, iters, layout, relu):
+def run_shape(shape, iters, layout, relu, graph=False):
     lib = _lib.load()
     dev = torch.device("cuda", 0)
-    st = torch.cuda.current_stream().cuda_stream
+    st0 = torch.cuda.current_stream().cuda_stream
+    nonlocal_st = [st0]
+    st = st0
     n, c, h, w = shape
     hw = h * w
     e = n * c * hw
@@ -59,49 +61,49 @@ def run_shape(shape, iters, layout, relu):
 
     def k_stats(b):
         return lib.cgbn_fwd_stats(b[0].data_ptr(), n, c, hw, layout, part.data_ptr(),
-                                  ws.data_ptr(), ws.numel(), st)
+                                  ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     def k_norm(b):
         return lib.cgbn_fwd_normalize(b[0].data_ptr(), n, c, hw, layout, pa, 1,
                                       gamma.data_ptr(), beta.data_ptr(), 1e-5, 0.1,
                                       rm.data_ptr(), rv.data_ptr(), saved.data_ptr(), int(relu),
                                       b[2].data_ptr(), status.data_ptr(), ws.data_ptr(),
-                                      ws.numel(), st)
+                                      ws.numel(), nonlocal_st[0])
 
     def k_bred(b):
         return lib.cgbn_bwd_reduce(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout,
                                    saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), int(relu),
-                                   bpart.data_ptr(), ws.data_ptr(), ws.numel(), st)
+                                   bpart.data_ptr(), ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     def k_dx(b):
         return lib.cgbn_bwd_dx(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout, pb, 1,
                                saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5,
                                int(relu), b[3].data_ptr(), dg.data_ptr(), db.data_ptr(),
-                               status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+                               status.data_ptr(), ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     def k_lfwd(b):
         return lib.cgbn_fwd_train_local(b[0].data_ptr(), n, c, hw, layout, gamma.data_ptr(),
                                         beta.data_ptr(), 1e-5, 0.1, rm.data_ptr(), rv.data_ptr(),
                                         saved.data_ptr(), int(relu), b[2].data_ptr(),
-                                        status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+                                        status.data_ptr(), ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     def k_lbwd(b):
         return lib.cgbn_bwd_local(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout,
                                   saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5,
                                   int(relu), b[3].data_ptr(), dg.data_ptr(), db.data_ptr(),
-                                  status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+                                  status.data_ptr(), ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     def k_ffwd(b):
         return lib.cgbn_fwd_fused(b[0].data_ptr(), n, c, hw, layout, gamma.data_ptr(),
                                   beta.data_ptr(), 1e-5, 0.1, rm.data_ptr(), rv.data_ptr(),
                                   saved.data_ptr(), int(relu), b[2].data_ptr(), status.data_ptr(),
-                                  ws.data_ptr(), ws.numel(), st)
+                                  ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     def k_fbwd(b):
         return lib.cgbn_bwd_fused(b[1].data_ptr(), b[0].data_ptr(), n, c, hw, layout,
                                   saved.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5,
                                   int(relu), b[3].data_ptr(), dg.data_ptr(), db.data_ptr(),
-                                  status.data_ptr(), ws.data_ptr(), ws.numel(), st)
+                                  status.data_ptr(), ws.data_ptr(), ws.numel(), nonlocal_st[0])
 
     out = {"shape": list(shape), "elements": e, "rotating_sets": sets}
     kernels = [("fwd_stats", k_stats, 4), ("fwd_normalize", k_norm, 8),
@@ -117,10 +119,28 @@ def run_shape(shape, iters, layout, relu):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(iters):
-            fn(bufs[i % sets])
-        e1.record()
+        if graph:
+            gr = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                gst = side.cuda_stream
+                nonlocal_st[0] = gst
+                with torch.cuda.graph(gr, stream=side):
+                    for i in range(iters):
+                        fn(bufs[i % sets])
+                nonlocal_st[0] = st
+            torch.cuda.current_stream().wait_stream(side)
+            gr.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            gr.replay()
+            e1.record()
+        else:
+            e0.record()
+            for i in range(iters):
+                fn(bufs[i % sets])
+            e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / iters
         out[name] = {"us": round(us, 2), "alg_gbs": round(bpe * e / (us * 1e-6) / 1e9, 1)}
@@ -133,6 +153,7 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--nhwc", action="store_true")
     ap.add_argument("--relu", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="time inside a CUDA graph")
     args = ap.parse_args()
     shapes = [tuple(int(v) for v in s.split(",")) for s in args.shape] or [
         (32, 64, 112, 112), (32, 256, 56, 56), (32, 64, 56, 56), (32, 512, 28, 28),
@@ -140,7 +161,7 @@ def main():
         (32, 512, 7, 7), (2, 256, 200, 334), (2, 64, 400, 667), (1, 2048, 7, 7)]
     layout = _lib.LAYOUT_NHWC if args.nhwc else _lib.LAYOUT_NCHW
     for s in shapes:
-        print(json.dumps(run_shape(s, args.iters, layout, args.relu)), flush=True)
+        print(json.dumps(run_shape(s, args.iters, layout, args.relu, args.graph)), flush=True)
 
 
 if __name__ == "__main__":
