@@ -108,20 +108,47 @@ struct FastDiv {
 // Reduction-kernel geometry. Element offset of vector unit j of channel c:
 // (c*HWv + j + (j / HWv) * gap) * VEC with gap = (C-1)*HWv. NCHW: HWv = HW/VEC.
 // NHWC and 2-D (N, C): HWv = 1, VEC = 1.
+// VM (vector mode) 1, 2, 4: exact vectors of VM floats (HW % VM == 0); VM 5 = "masked
+// float4": planes whose length is not a multiple of 4 (ResNet 7x7, FPN 25x42 / 13x21) are
+// read as the aligned float4 cover of each plane (ceil(HW/4) + 1 units per plane) with a
+// per-element mask, so odd planes also stream with 128-bit loads.
 struct Geom {
   uint32_t C;
-  uint32_t Lv;        // vector units per channel stream (N*HW/VEC)
+  uint32_t Lv;        // vector units per channel stream (N*HWv)
   uint32_t HWv;       // vector units per plane
   uint32_t grid;      // CTAs of this launch
   uint32_t tpc_log2;  // team kernels: log2(threads per channel)
+  uint32_t HW;        // floats per plane (1 for NHWC / 2-D)
   uint64_t T;         // C * Lv
   uint64_t gap;       // (C-1)*HWv
-  FastDiv dhw;
+  FastDiv dhw;        // division by HWv
   double count;       // elements per channel on this rank (N*HW)
 };
 
+constexpr int vec_of(int vm) { return vm == 5 ? 4 : vm; }
+
 __device__ __forceinline__ size_t voff(const Geom& g, uint32_t c, uint32_t j) {
   return (size_t)c * g.HWv + j + (size_t)g.dhw.div(j) * g.gap;
+}
+
+// Address (in floats) and element mask of unit j of channel c.
+template <int VM>
+__device__ __forceinline__ size_t unit_addr(const Geom& g, uint32_t c, uint32_t j,
+                                            uint32_t& mask) {
+  if constexpr (VM != 5) {
+    mask = 0xFu;
+    return voff(g, c, j) * VM;
+  } else {
+    const uint32_t n = g.dhw.div(j);
+    const uint32_t k = j - n * g.HWv;
+    const size_t ps = ((size_t)n * g.C + c) * g.HW;  // plane start
+    const size_t base = (ps & ~(size_t)3) + 4 * (size_t)k;
+    mask = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      mask |= (base + e >= ps && base + e < ps + g.HW) ? (1u << e) : 0u;
+    return base;
+  }
 }
 
 // flat: CTA b owns stream units [cta_begin(b), cta_begin(b+1)).
@@ -172,8 +199,8 @@ __device__ __forceinline__ void ldv(const float* __restrict__ p, float (&v)[VEC]
 
 // Loads in flight per thread per round: ~128 B for one input stream, ~128 B total for
 // two (NIN = number of input streams).
-template <int VEC, int NIN = 1>
-constexpr int unroll_for() { return (NIN == 1 || VEC == 1) ? 8 : 4; }
+template <int VM, int NIN = 1>
+constexpr int unroll_for() { return (NIN == 1 || VM == 1) ? 8 : 4; }
 
 // Visit units j = start, start+stride, ... < end of channel c in rounds of U: the U
 // (predicated) loads of a round are issued before any of them is used.
@@ -186,7 +213,7 @@ __device__ __forceinline__ void strided_rounds(const Geom& g, uint32_t c, uint32
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t j = i + u * stride;
-      if (j < end) op.load(voff(g, c, j), r[u]);
+      if (j < end) op.load(g, c, j, r[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -387,9 +414,10 @@ enum FinishMode { kPartial = 0, kRawSums = 1, kLocalFinal = 2 };
 
 // Forward statistics: sums of d = x - K (K = first element of the channel on this rank,
 // the same for every CTA of the channel; d is exact in fp64) -> (mean, M2, count).
-template <int VEC>
+template <int VM>
 struct StatsOp {
-  static constexpr int kVec = VEC;
+  static constexpr int kVec = VM;
+  static constexpr int VEC = vec_of(VM);
   static constexpr int kIn = 1;
   const float* __restrict__ x;
   double K;
@@ -397,17 +425,26 @@ struct StatsOp {
   int mode;                   // FinishMode
   double* __restrict__ out2;  // kRawSums: sum_sq destination (may be null)
   FwdFinal F;                 // kLocalFinal
-  struct Regs { float v[VEC]; };
+  struct Regs { float v[VEC]; uint32_t m; };
   struct Init { double K; };
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
-    K = shift ? (double)__ldg(x + (size_t)c * g.HWv * VEC) : 0.0;
+    K = shift ? (double)__ldg(x + (size_t)c * g.HW) : 0.0;
   }
   __device__ __forceinline__ Init get_init() const { return Init{K}; }
   __device__ __forceinline__ void set_init(const Init& i) { K = i.K; }
-  __device__ __forceinline__ void load(size_t off, Regs& r) const { ldv<VEC>(x + off * VEC, r.v); }
+  // per-channel finisher inputs, loaded early to overlap the data stream
+  using Pre = FwdChan;
+  __device__ __forceinline__ Pre prefetch(uint32_t c) const {
+    return mode == kLocalFinal ? load_fwd_chan(F, c) : FwdChan{0.f, 0.f, 0.f, 0.f};
+  }
+  __device__ __forceinline__ void load(const Geom& g, uint32_t c, uint32_t j, Regs& r) const {
+    const size_t off = unit_addr<VM>(g, c, j, r.m);
+    if (VM != 5 || r.m) ldv<VEC>(x + off, r.v);
+  }
   __device__ __forceinline__ void acc(const Regs& r, double& a, double& b) const {
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
+      if (VM == 5 && !((r.m >> k) & 1u)) continue;
       const double d = (double)r.v[k] - K;
       a += d;
       b = __fma_rn(d, d, b);
@@ -415,6 +452,10 @@ struct StatsOp {
   }
   __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
                                          double* __restrict__ out) const {
+    finish(g, c, S1, S2, out, prefetch(c));
+  }
+  __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
+                                         double* __restrict__ out, const Pre& pre) const {
     const double n = g.count;
     if (mode == kRawSums) {
       out[c] = S1;
@@ -429,16 +470,17 @@ struct StatsOp {
       if (c == 0) out[2 * g.C] = n;
     } else {
       double P, Q;
-      finalize_fwd_channel(F, c, n, mean, M2, true, P, Q);
+      finalize_fwd_channel(F, c, n, mean, M2, true, pre, P, Q);
     }
   }
 };
 
 // Backward: g = dy (ReLU-masked when the forward fused a ReLU); fp64 sums of g and
 // g*(x - mean).
-template <int VEC, bool RELU>
+template <int VM, bool RELU>
 struct BwdOp {
-  static constexpr int kVec = VEC;
+  static constexpr int kVec = VM;
+  static constexpr int VEC = vec_of(VM);
   static constexpr int kIn = 2;
   const float* __restrict__ dy;
   const float* __restrict__ x;
@@ -448,7 +490,7 @@ struct BwdOp {
   double mean, P, Q;
   int mode;    // kPartial or kLocalFinal
   BwdFinal F;  // kLocalFinal
-  struct Regs { float g[VEC]; float x[VEC]; };
+  struct Regs { float g[VEC]; float x[VEC]; uint32_t m; };
   struct Init { double mean; };  // finish() needs no per-channel state
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
     mean = saved[c];
@@ -457,13 +499,25 @@ struct BwdOp {
   }
   __device__ __forceinline__ Init get_init() const { return Init{mean}; }
   __device__ __forceinline__ void set_init(const Init& i) { mean = i.mean; }
-  __device__ __forceinline__ void load(size_t off, Regs& r) const {
-    ldv<VEC>(dy + off * VEC, r.g);
-    ldv<VEC>(x + off * VEC, r.x);
+  using Pre = BwdChan;
+  __device__ __forceinline__ Pre prefetch(uint32_t c) const {
+    if (mode == kLocalFinal) return load_bwd_chan(F, c);
+    BwdChan v;
+    v.mean = v.var = v.inv_std = v.m = 0.0;
+    v.gamma = v.beta = 0.f;
+    return v;
+  }
+  __device__ __forceinline__ void load(const Geom& g, uint32_t c, uint32_t j, Regs& r) const {
+    const size_t off = unit_addr<VM>(g, c, j, r.m);
+    if (VM != 5 || r.m) {
+      ldv<VEC>(dy + off, r.g);
+      ldv<VEC>(x + off, r.x);
+    }
   }
   __device__ __forceinline__ void acc(const Regs& r, double& a, double& b) const {
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
+      if (VM == 5 && !((r.m >> k) & 1u)) continue;
       double gk = (double)r.g[k];
       if (RELU && !(bn_out(P, Q, r.x[k]) > 0.0)) gk = 0.0;
       a += gk;
@@ -472,11 +526,15 @@ struct BwdOp {
   }
   __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
                                          double* __restrict__ out) const {
+    finish(g, c, S1, S2, out, prefetch(c));
+  }
+  __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
+                                         double* __restrict__ out, const Pre& pre) const {
     if (mode == kPartial) {
       out[c] = S1;
       out[g.C + c] = S2;
     } else {
-      finalize_bwd_channel(F, c, S1, S2, true);
+      finalize_bwd_channel(F, c, S1, S2, true, pre);
     }
   }
 };
@@ -553,7 +611,7 @@ k_reduce_flat(Geom g, Op op, double* __restrict__ out, double2* __restrict__ ws,
       if (b0 == b1) {
         Op o = op;
         o.set_init(s_init[k]);
-        o.finish(g, c, s_S1[k], s_S2[k], out);
+        o.finish(g, c, s_S1[k], s_S2[k], out, o.prefetch(c));
       } else {
         ws[(size_t)blockIdx.x + c] = make_double2(s_S1[k], s_S2[k]);
         __threadfence();
@@ -603,6 +661,8 @@ k_reduce_team(Geom g, Op op, double* __restrict__ out) {
   for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint32_t c = tile * cpt + team;
     double S1 = 0.0, S2 = 0.0;
+    typename Op::Pre pre;
+    if (q == 0 && c < g.C) pre = op.prefetch(c);  // overlaps the data loads below
     if (c < g.C) {
       op.init(g, c);
       reduce_range(g, c, q, g.Lv, tpc, op, S1, S2);
@@ -610,14 +670,14 @@ k_reduce_team(Geom g, Op op, double* __restrict__ out) {
     S1 = warp_sum(S1);
     S2 = warp_sum(S2);
     if (tpc == 32) {
-      if (l == 0 && c < g.C) op.finish(g, c, S1, S2, out);
+      if (l == 0 && c < g.C) op.finish(g, c, S1, S2, out, pre);
     } else {
       if (l == 0) { sa[w] = S1; sb[w] = S2; }
       __syncthreads();
       if (q == 0 && c < g.C) {
         const int wpt = (int)(tpc >> 5);
         for (int i = 1; i < wpt; ++i) { S1 += sa[w + i]; S2 += sb[w + i]; }
-        op.finish(g, c, S1, S2, out);
+        op.finish(g, c, S1, S2, out, pre);
       }
       __syncthreads();
     }
@@ -955,10 +1015,14 @@ int make_plan(int64_t N, int64_t C, int64_t HW, int layout, const void* const* p
   for (int k = 0; k < nptr; ++k) align |= (uintptr_t)ptrs[k];
   int vec = 1;
   if (planeHW % 4 == 0 && (align % 16) == 0) vec = 4;
+  else if (layout == CGBN_LAYOUT_NCHW && HW >= 16 && (align % 16) == 0 && (N * C * HW) % 4 == 0 &&
+           !getenv("CGBN_NO_MASKED"))
+    vec = 5;  // masked float4 cover of odd planes (the cover never leaves the tensor)
   else if (planeHW % 2 == 0 && (align % 8) == 0) vec = 2;
   Geom g;
   g.C = (uint32_t)C;
-  g.HWv = (uint32_t)(planeHW / vec);
+  g.HW = (uint32_t)planeHW;
+  g.HWv = (uint32_t)(vec == 5 ? (planeHW + 3) / 4 + 1 : planeHW / vec);
   g.Lv = (uint32_t)(planeN * g.HWv);
   g.gap = (uint64_t)(C - 1) * g.HWv;
   g.dhw.init(g.HWv);
@@ -1089,6 +1153,7 @@ int run_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double
 int dispatch_stats(const Plan& pl, const float* x, bool shift, int mode, double* out,
                    double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st) {
   switch (pl.vec) {
+    case 5: return run_stats<5>(pl, x, shift, mode, out, out2, F, w, st);
     case 4: return run_stats<4>(pl, x, shift, mode, out, out2, F, w, st);
     case 2: return run_stats<2>(pl, x, shift, mode, out, out2, F, w, st);
     default: return run_stats<1>(pl, x, shift, mode, out, out2, F, w, st);
@@ -1100,12 +1165,14 @@ int dispatch_bwd_reduce(const Plan& pl, const float* dy, const float* x, const d
                         const BwdFinal* F, const WsView& w, cudaStream_t st) {
   if (relu) {
     switch (pl.vec) {
+      case 5: return run_bwd_reduce<5, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
       case 4: return run_bwd_reduce<4, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
       case 2: return run_bwd_reduce<2, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
       default: return run_bwd_reduce<1, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
     }
   }
   switch (pl.vec) {
+    case 5: return run_bwd_reduce<5, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
     case 4: return run_bwd_reduce<4, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
     case 2: return run_bwd_reduce<2, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
     default: return run_bwd_reduce<1, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
