@@ -226,40 +226,100 @@ def run_reference_arm(args):
 # ----------------------------------------------------------------------------------
 # GPU arm
 
-class GraphKernelTimer:
-    """Records CUDA events around every native launch; external events when capturing
-    so that the event nodes live inside the CUDA graph."""
+def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
+    """Per-kernel-family device time of one step. For each family a CUDA graph holds that
+    kernel's launch for every layer (the layers' own buffers, step order) made through
+    the C ABI: statistics (cgbn_fwd_stats), normalise (the elementwise pass alone,
+    cgbn_channel_affine with the layer's coefficients), backward reduce
+    (cgbn_bwd_reduce) and dx (cgbn_bwd_dx with G=1: the C-thread finalize + the
+    elementwise pass). Returns ({family: stats}, description)."""
+    import torch
+    from paper_1711_07240_b200 import _lib
+    from paper_1711_07240_b200.tensor import workspace
+    lib = _lib.load()
+    dev = xs[0].device
+    # one eager forward to obtain every layer's saved statistics
+    caches = [cg.sync_bn_forward(handle, x, st)[1] for x, st in zip(xs, states)]
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream(device=dev)
+    L = []
+    for s, x, dy, st, ca in zip(shapes, xs, dys, states, caches):
+        n, c, h, w = s
+        L.append(dict(n=n, c=c, hw=h * w, x=x, dy=dy, st=st, saved=ca.saved,
+                      y=torch.empty_like(x), dx=torch.empty_like(x),
+                      part=torch.empty(2 * c + 1, dtype=torch.float64, device=dev),
+                      bpart=torch.empty(2 * c, dtype=torch.float64, device=dev),
+                      P=torch.ones(c, dtype=torch.float64, device=dev),
+                      Q=torch.zeros(c, dtype=torch.float64, device=dev),
+                      dg=torch.empty(c, device=dev), db=torch.empty(c, device=dev),
+                      rm=torch.zeros(c, device=dev), rv=torch.ones(c, device=dev),
+                      saved2=torch.empty(3 * c + 1, dtype=torch.float64, device=dev),
+                      status=torch.zeros(1, dtype=torch.int32, device=dev)))
+    keep = []
 
-    def __init__(self, external):
-        import torch
-        self.torch = torch
-        self.external = external
-        self.spans = []
-        self._cur = None
+    def ptrs1(t):
+        arr, k = _lib.ptr_array([t.data_ptr()])
+        keep.append(k)
+        return arr
 
-    def _ev(self):
-        if self.external:
-            return self.torch.cuda.Event(enable_timing=True, external=True)
-        return self.torch.cuda.Event(enable_timing=True)
-
-    def begin(self, name, nbytes):
-        e0 = self._ev()
-        e0.record()
-        self._cur = (name, nbytes, e0)
-
-    def end(self):
-        e1 = self._ev()
-        e1.record()
-        name, nb, e0 = self._cur
-        self.spans.append((name, nb, e0, e1))
-
-    def collect(self, acc):
-        for name, nb, e0, e1 in self.spans:
-            ms = e0.elapsed_time(e1)
-            a = acc.setdefault(name, [0.0, 0, 0])
-            a[0] += ms
-            a[1] += nb
-            a[2] += 1
+    fams = {
+        "fwd_stats": (4, lambda d, ws, st: lib.cgbn_fwd_stats(
+            d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0, d["part"].data_ptr(),
+            ws.data_ptr(), ws.numel(), st)),
+        "fwd_pair": (12, lambda d, ws, st: lib.cgbn_fwd_train_local(
+            d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0, d["st"].gamma.data_ptr(),
+            d["st"].beta.data_ptr(), 1e-5, 0.1, d["rm"].data_ptr(), d["rv"].data_ptr(),
+            d["saved2"].data_ptr(), 0, d["y"].data_ptr(), d["status"].data_ptr(),
+            ws.data_ptr(), ws.numel(), st)),
+        "bwd_reduce": (8, lambda d, ws, st: lib.cgbn_bwd_reduce(
+            d["dy"].data_ptr(), d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0,
+            d["saved"].data_ptr(), d["st"].gamma.data_ptr(), d["st"].beta.data_ptr(), 0,
+            d["bpart"].data_ptr(), ws.data_ptr(), ws.numel(), st)),
+        "bwd_pair": (20, lambda d, ws, st: lib.cgbn_bwd_local(
+            d["dy"].data_ptr(), d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0,
+            d["saved"].data_ptr(), d["st"].gamma.data_ptr(), d["st"].beta.data_ptr(), 1e-5,
+            0, d["dx"].data_ptr(), d["dg"].data_ptr(), d["db"].data_ptr(),
+            d["status"].data_ptr(), ws.data_ptr(), ws.numel(), st)),
+    }
+    out, raw = {}, {}
+    total_elems = sum(numel(s) for s in shapes)
+    with torch.cuda.stream(side):
+        ws = workspace(dev, max(lib.cgbn_workspace_bytes(d["n"], d["c"], d["hw"], 0) for d in L))
+        st = side.cuda_stream
+        for name, (bpe, fn) in fams.items():
+            for d in L:
+                _lib.check(fn(d, ws, st), name)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for d in L:
+                    fn(d, ws, side.cuda_stream)
+            g.replay()
+            side.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(side)
+            for _ in range(reps):
+                g.replay()
+            e1.record(side)
+            side.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            raw[name] = ms
+            del g
+    # the elementwise passes in context: (reduction + elementwise) - reduction alone, so
+    # x (and dy) are as L2-warm as in the step
+    fam = {"fwd_stats": (4, raw["fwd_stats"]),
+           "fwd_normalize_ew": (8, raw["fwd_pair"] - raw["fwd_stats"]),
+           "bwd_reduce": (8, raw["bwd_reduce"]),
+           "bwd_dx_ew": (12, raw["bwd_pair"] - raw["bwd_reduce"])}
+    for name, (bpe, ms) in fam.items():
+        out[name] = {"ms_per_step": ms, "launches_per_step": len(L), "bytes_per_elem": bpe,
+                     "alg_gbs": bpe * total_elems / (ms * 1e-3) / 1e9}
+    tot = sum(v["ms_per_step"] for v in out.values())
+    for v in out.values():
+        v["share"] = v["ms_per_step"] / tot
+    return out, ("CUDA graphs of the step's 53 launches per family through the C ABI "
+                 "(stats, local fwd pair, bwd reduce, local bwd pair); elementwise = pair - "
+                 f"reduction; CUDA events on the replay stream, mean of {reps} replays")
 
 
 def run_gpu_arm(args):
@@ -268,7 +328,6 @@ def run_gpu_arm(args):
     import torch.distributed as dist
 
     import paper_1711_07240_b200 as cg
-    from paper_1711_07240_b200 import batchnorm as bnmod
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -360,33 +419,11 @@ def run_gpu_arm(args):
     value = step_bytes_rank * world / (ms_step * 1e-3) / 1e9
     launches_per_step = 4 * len(shapes)
 
-    # ---- per-kernel times: same step captured with event nodes (external events), else
-    # an eagerly instrumented step; several replays, CUDA events on the launch stream.
-    kstats = {}
-    timing_mode = "graph-external-events"
-    try:
-        tg = torch.cuda.CUDAGraph()
-        timer = GraphKernelTimer(external=True)
-        bnmod.kernel_timer = timer
-        with torch.cuda.graph(tg):
-            step()
-        bnmod.kernel_timer = None
-        for _ in range(min(args.steps, 10)):
-            tg.replay()
-            torch.cuda.synchronize()
-            timer.collect(kstats)
-        del tg
-    except Exception as exc:  # noqa: BLE001
-        bnmod.kernel_timer = None
-        timing_mode = f"eager-events ({type(exc).__name__})"
-        kstats = {}
-        for _ in range(min(args.steps, 10)):
-            timer = GraphKernelTimer(external=False)
-            bnmod.kernel_timer = timer
-            step()
-            bnmod.kernel_timer = None
-            torch.cuda.synchronize()
-            timer.collect(kstats)
+    # ---- per-kernel times: one CUDA graph per kernel family replays that kernel's 53
+    # launches of the step (same layer buffers, step order) through the C ABI; CUDA
+    # events on the replay stream around `reps` replays.
+    kern, timing_mode = ({}, "skipped") if args.no_kprof else \
+        kernel_profile(cg, shapes, xs, dys, states, handle, reps=20)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -395,18 +432,24 @@ def run_gpu_arm(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks \
         else "fallback 6.65 TB/s (B200_PROFILING.md)"
-    kern = {}
-    tot_ms = sum(v[0] for v in kstats.values()) or 1.0
-    for name, (ms, nb, cnt) in kstats.items():
-        kern[name] = {"ms_per_step": ms / max(1, cnt / len(shapes)), "launches": cnt,
-                      "alg_gbs": nb / (ms * 1e-3) / 1e9 if ms > 0 else None,
-                      "share": ms / tot_ms}
-    dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"]) if kern else None
     roofline = None
     if dom:
         ach = kern[dom]["alg_gbs"]
+        traffic = args.traffic
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))["families"]
+            key = {"bwd_dx_ew": "bwd_dx", "fwd_normalize_ew": "fwd_normalize_ew"}.get(dom, dom)
+            if traffic is None and key in tr:
+                traffic = tr[key]["dram_bytes_per_launch"]
+        except Exception:  # noqa: BLE001
+            pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak,
-                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
+                    "traffic_unit": "dram bytes per launch (profiles/r1_traffic.json, ncu)",
+                    "alg_bytes_per_launch": (kern[dom]["bytes_per_elem"] *
+                                             sum(numel(s) for s in shapes) / len(shapes)),
+                    "alg_bytes_per_elem": kern[dom]["bytes_per_elem"],
                     "peak_source": peak_src, "timing": timing_mode}
 
     # ---- statistics exchange latency (N>1): NCCL all-gather of the fwd partial
@@ -533,9 +576,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes/launch of the dominant kernel (recorded as-is)")
     ap.add_argument("--fused", action="store_true",
                     help="single-launch cooperative kernels for layers that fit on chip")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kprof", action="store_true", help="skip the per-kernel profile")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)

@@ -889,13 +889,15 @@ int num_sms_cached() {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Workspace: tickets + barrier words | (C + max grid) double2 slots | coefficient table
-// (5 x C doubles: P, Q, A, B, Cc).
-size_t slots_bytes(int64_t C, int sms) {
+// Workspace: tickets + barrier words | (C + max grid) double2 per-CTA partial slots |
+// coefficient table (5 x C doubles: P, Q, A, B, Cc).
+size_t slots_bytes(int64_t N, int64_t C, int64_t HW, int sms) {
+  (void)N;
+  (void)HW;
   return ((size_t)C + (size_t)sms * kMaxCtasPerSm) * sizeof(double2);
 }
-size_t ws_bytes_for(int64_t C, int sms) {
-  return kTicketBytes + slots_bytes(C, sms) + 5 * (size_t)C * sizeof(double);
+size_t ws_bytes_for(int64_t N, int64_t C, int64_t HW, int sms) {
+  return kTicketBytes + slots_bytes(N, C, HW, sms) + 5 * (size_t)C * sizeof(double);
 }
 
 struct WsView {
@@ -909,9 +911,9 @@ struct WsView {
   double* Cc;
 };
 
-int ws_view(void* ws, size_t ws_bytes, int64_t C, WsView* v) {
+int ws_view(void* ws, size_t ws_bytes, int64_t N, int64_t C, int64_t HW, WsView* v) {
   const int sms = num_sms_cached();
-  const size_t need = ws_bytes_for(C, sms);
+  const size_t need = ws_bytes_for(N, C, HW, sms);
   if (!ws || ws_bytes < need)
     return set_error(CGBN_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need,
                      ws_bytes);
@@ -919,7 +921,7 @@ int ws_view(void* ws, size_t ws_bytes, int64_t C, WsView* v) {
   v->tickets = reinterpret_cast<unsigned*>(b);
   v->bar = v->tickets + kTicketWords;
   v->slots = reinterpret_cast<double2*>(b + kTicketBytes);
-  double* coef = reinterpret_cast<double*>(b + kTicketBytes + slots_bytes(C, sms));
+  double* coef = reinterpret_cast<double*>(b + kTicketBytes + slots_bytes(N, C, HW, sms));
   v->P = coef;
   v->Q = coef + C;
   v->A = coef + 2 * C;
@@ -1388,7 +1390,7 @@ int cgbn_num_sms(void) { return num_sms_cached(); }
 
 size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout) {
   if (validate_shape(N, C, HW, layout)) return 0;
-  return ws_bytes_for(C, num_sms_cached());
+  return ws_bytes_for(N, C, HW, num_sms_cached());
 }
 
 int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
@@ -1398,7 +1400,7 @@ int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CGBN_TRY(dispatch_stats(pl, x, true, kPartial, partial, nullptr, nullptr, w, st));
   return check_launch("cgbn_fwd_stats");
@@ -1411,7 +1413,7 @@ int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layou
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   pl.tma = false;
   CGBN_TRY(dispatch_stats(pl, x, false, kRawSums, sum, sum_sq, nullptr, w, st));
@@ -1430,7 +1432,7 @@ int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int lay
   Parts parts;
   CGBN_TRY(fill_parts(&parts, partials, G));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
@@ -1451,7 +1453,7 @@ int cgbn_fwd_train_local(const float* x, int64_t N, int64_t C, int64_t HW, int l
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, eptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
@@ -1472,7 +1474,7 @@ int cgbn_fwd_eval(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_coef_eval<<<chan_blocks(C), 256, 0, st>>>(gamma, beta, running_mean, running_var, eps, w.P,
                                               w.Q, (uint32_t)C);
@@ -1487,7 +1489,7 @@ int cgbn_xhat(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_coef_xhat<<<chan_blocks(C), 256, 0, st>>>(saved, w.P, w.Q, (uint32_t)C);
   launch_ew_affine(ep, false, x, xhat, w.P, w.Q, st);
@@ -1513,7 +1515,7 @@ int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 2, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, partial,
                                nullptr, w, st));
@@ -1533,7 +1535,7 @@ int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t H
   Parts parts;
   CGBN_TRY(fill_parts(&parts, partials, G));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const BwdFinal F =
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
@@ -1556,7 +1558,7 @@ int cgbn_bwd_local(const float* dy, const float* x, int64_t N, int64_t C, int64_
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, eptrs, 3, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const BwdFinal F =
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
@@ -1582,7 +1584,7 @@ int cgbn_fwd_fused(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   if (!fused_plan(N, C, HW, layout, (uintptr_t)x | (uintptr_t)y, 1, &fg))
     return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_fwd_fused: shape/layout not eligible");
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
   F.P = F.Q = nullptr;  // the fused kernel keeps its coefficients in shared memory
@@ -1606,7 +1608,7 @@ int cgbn_bwd_fused(const float* dy, const float* x, int64_t N, int64_t C, int64_
   if (!fused_plan(N, C, HW, layout, (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, 2, &fg))
     return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_bwd_fused: shape/layout not eligible");
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, C, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
   BwdFinal F = make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
   F.A = F.B = F.Cc = F.P = F.Q = nullptr;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

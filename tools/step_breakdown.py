@@ -1,40 +1,49 @@
 #!/usr/bin/env python3
-"""Aggregate an ncu launch list (gpu__time_duration.sum per kernel) of one bench step
-into per-layer / per-kernel-type times. Usage: step_breakdown.py launches.csv [n_skip]"""
+"""Per-layer / per-kernel device times of one bench step from an ncu launch list
+(gpu__time_duration.sum + dram bytes), taken with
+    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --cache-control none --csv --log-file L.csv \
+        python bench.py --steps 1 --warmup 3 --no-graph --no-e2e --no-cpu-baseline --no-kprof
+The last 4*53 CGBN launches of the list are the measured step (fwd: reduce, elementwise
+per layer; bwd: reduce, elementwise per layer in reverse order)."""
 import csv
-import sys
 import os
+import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from bench import resnet50_bn_shapes, numel  # noqa: E402
+from bench import numel, resnet50_bn_shapes  # noqa: E402
 
-rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
-hdr = rows[0]
-ki, vi, mi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
-ks = [(r[ki], float(r[vi])) for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
-ours = [(n, t) for n, t in ks if "k_" in n and ("reduce" in n or "affine" in n or "dx" in n or "fused" in n)]
-shapes = resnet50_bn_shapes(32)
-per_step = 4 * len(shapes)
-step = ours[-per_step:]
-def kind(n):
-    if "StatsOp" in n: return "stats"
-    if "BwdOp" in n: return "bwd_reduce"
-    if "affine" in n: return "normalize"
-    if "dx" in n: return "bwd_dx"
-    return n[:30]
-fwd = step[:2 * len(shapes)]
-bwd = step[2 * len(shapes):]
-tot = {}
-print(f"{'layer':>5} {'shape':>22} {'MB':>7} {'stats':>7} {'norm':>7} {'bred':>7} {'dx':>7} {'sum us':>8} {'alg GB/s':>9}")
-grand = 0.0
-for li, s in enumerate(shapes):
-    st, nm = fwd[2 * li], fwd[2 * li + 1]
-    bi = len(shapes) - 1 - li
-    br, dx = bwd[2 * bi], bwd[2 * bi + 1]
-    ts = [st[1] / 1e3, nm[1] / 1e3, br[1] / 1e3, dx[1] / 1e3]
-    for k, t in zip(("stats", "normalize", "bwd_reduce", "bwd_dx"), ts):
-        tot[k] = tot.get(k, 0.0) + t
-    ssum = sum(ts)
-    grand += ssum
-    print(f"{li:5d} {str(s):>22} {4 * numel(s) / 1e6:7.1f} {ts[0]:7.1f} {ts[1]:7.1f} {ts[2]:7.1f} {ts[3]:7.1f} {ssum:8.1f} {32 * numel(s) / (ssum * 1e-6) / 1e9:9.0f}")
-print("totals (us):", {k: round(v, 1) for k, v in tot.items()}, "sum", round(grand, 1))
+
+def main(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    ki, mi, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+    k = {}
+    for r in rows[1:]:
+        d = k.setdefault(int(r[ii]), {"name": r[ki]})
+        d[r[mi]] = float(r[vi].replace(",", ""))
+    ours = [k[i] for i in sorted(k) if ("k_reduce" in k[i]["name"] or "k_ew" in k[i]["name"])]
+    shapes = resnet50_bn_shapes(32)
+    step = ours[-4 * len(shapes):]
+    fwd, bwd = step[:2 * len(shapes)], step[2 * len(shapes):]
+    print(f"{'l':>3} {'C,H,W':>16} {'stats':>6} {'norm':>6} {'bred':>6} {'dx':>6} {'sum us':>7}"
+          f" {'alg GB/s':>8} {'dram/alg':>8}")
+    tot = [0.0] * 4
+    dram = alg = 0.0
+    for li, s in enumerate(shapes):
+        bi = len(shapes) - 1 - li
+        ks = (fwd[2 * li], fwd[2 * li + 1], bwd[2 * bi], bwd[2 * bi + 1])
+        t = [x["gpu__time_duration.sum"] / 1e3 for x in ks]
+        by = sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in ks)
+        for i in range(4):
+            tot[i] += t[i]
+        dram += by
+        alg += 32 * numel(s)
+        print(f"{li:3d} {str(s[1:]):>16} {t[0]:6.1f} {t[1]:6.1f} {t[2]:6.1f} {t[3]:6.1f} "
+              f"{sum(t):7.1f} {32 * numel(s) / (sum(t) * 1e-6) / 1e9:8.0f} {by / (32 * numel(s)):8.2f}")
+    print("totals us: stats %.1f norm %.1f bred %.1f dx %.1f | sum %.1f | dram/alg %.3f"
+          % (tot[0], tot[1], tot[2], tot[3], sum(tot), dram / alg))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
