@@ -37,6 +37,7 @@
 //                                          k_finalize_* / merge_fwd_partials)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
@@ -46,6 +47,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <utility>
 
 #include "cgbn.h"
@@ -261,6 +263,22 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Asynchronous global -> shared copies (no register staging): the finisher's per-channel
+// inputs are fetched while the data streams and waited for only at the end.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // ----------------------------------------------------------------------------------
 // Channel finishers: the group statistics of one channel -> everything downstream.
 
@@ -293,6 +311,17 @@ __device__ __forceinline__ FwdChan load_fwd_chan(const FwdFinal& F, uint32_t c) 
   v.rmean = F.rmean ? F.rmean[c] : 0.f;
   v.rvar = F.rvar ? F.rvar[c] : 0.f;
   return v;
+}
+
+__device__ __forceinline__ void load_fwd_chan_async(const FwdFinal& F, uint32_t c, FwdChan* d) {
+  cp_async4(&d->gamma, F.gamma + c);
+  cp_async4(&d->beta, F.beta + c);
+  if (F.rmean) {
+    cp_async4(&d->rmean, F.rmean + c);
+    cp_async4(&d->rvar, F.rvar + c);
+  } else {
+    d->rmean = d->rvar = 0.f;
+  }
 }
 
 __device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
@@ -371,6 +400,17 @@ __device__ __forceinline__ BwdChan load_bwd_chan(const BwdFinal& F, uint32_t c) 
   return v;
 }
 
+__device__ __forceinline__ void load_bwd_chan_async(const BwdFinal& F, uint32_t c, BwdChan* d) {
+  const uint32_t C = F.C;
+  cp_async8(&d->mean, F.saved + c);
+  cp_async8(&d->var, F.saved + C + c);
+  cp_async8(&d->inv_std, F.saved + 2 * C + c);
+  cp_async8(&d->m, F.saved + 3 * C);
+  cp_async4(&d->gamma, F.gamma + c);
+  if (F.relu) cp_async4(&d->beta, F.beta + c);
+  else d->beta = 0.f;
+}
+
 __device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32_t c, double sdy,
                                                        double sdyx, bool write,
                                                        const BwdChan& v) {
@@ -437,6 +477,9 @@ struct StatsOp {
   __device__ __forceinline__ Pre prefetch(uint32_t c) const {
     return mode == kLocalFinal ? load_fwd_chan(F, c) : FwdChan{0.f, 0.f, 0.f, 0.f};
   }
+  __device__ __forceinline__ void prefetch_async(uint32_t c, Pre* d) const {
+    if (mode == kLocalFinal) load_fwd_chan_async(F, c, d);
+  }
   __device__ __forceinline__ void load(const Geom& g, uint32_t c, uint32_t j, Regs& r) const {
     const size_t off = unit_addr<VM>(g, c, j, r.m);
     if (VM != 5 || r.m) ldv<VEC>(x + off, r.v);
@@ -500,6 +543,9 @@ struct BwdOp {
   __device__ __forceinline__ Init get_init() const { return Init{mean}; }
   __device__ __forceinline__ void set_init(const Init& i) { mean = i.mean; }
   using Pre = BwdChan;
+  __device__ __forceinline__ void prefetch_async(uint32_t c, Pre* d) const {
+    if (mode == kLocalFinal) load_bwd_chan_async(F, c, d);
+  }
   __device__ __forceinline__ Pre prefetch(uint32_t c) const {
     if (mode == kLocalFinal) return load_bwd_chan(F, c);
     BwdChan v;
@@ -545,10 +591,11 @@ __device__ __forceinline__ void reduce_range(const Geom& g, uint32_t c, uint32_t
                                              uint32_t end, uint32_t stride, const Op& op,
                                              double& S1, double& S2) {
   constexpr int U = unroll_for<Op::kVec, Op::kIn>();
+  constexpr int NA = Op::kIn == 1 ? 2 : 1;  // accumulator pairs (registers vs. DADD chains)
   double a[2] = {0.0, 0.0}, b[2] = {0.0, 0.0};
   strided_rounds<U>(g, c, start, end, stride, op,
                     [&](int u, uint32_t, const typename Op::Regs& r) {
-                      op.acc(r, a[u & 1], b[u & 1]);
+                      op.acc(r, a[u % NA], b[u % NA]);
                     });
   S1 = a[0] + a[1];
   S2 = b[0] + b[1];
@@ -681,6 +728,94 @@ k_reduce_team(Geom g, Op op, double* __restrict__ out) {
       }
       __syncthreads();
     }
+  }
+}
+
+// cluster-team reduction (NCHW default). Cluster q of KC CTAs (runtime cluster size,
+// 1..8) owns channels q*nch .. q*nch+nch-1 with nch = 256 >> TL. In every CTA of the
+// cluster, team i (2^TL threads) streams CTA rank r's share [r*Lv/KC, (r+1)*Lv/KC) of
+// channel q*nch+i with no block barrier: warp partials go to shared memory, one
+// __syncthreads folds each team's warps in ascending order, one cluster barrier, then
+// rank (i % KC) folds the KC CTA partials of channel i over DSMEM in rank order and
+// finishes the channel. Compared with k_reduce_flat this removes the slot/ticket round
+// trips through L2 (tools/flatlab.cu: 3-4 us per launch at ResNet mid shapes) and the
+// per-segment block barriers. Clusters loop over q when C needs more CTAs than fit.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ double2 ld_dsmem(const double2* p, uint32_t rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(ra) : "memory");
+  return v;
+}
+
+template <class Op, int TL>
+__global__ void __launch_bounds__(kThreads, 4)
+k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
+  constexpr uint32_t tpc = 1u << TL;
+  constexpr uint32_t nch = kThreads >> TL;
+  constexpr uint32_t wpt = tpc / 32;
+  __shared__ double2 wpart[kWarps];
+  __shared__ double2 cpart[nch];
+  __shared__ typename Op::Pre spre[nch];
+  const uint32_t KC = cluster_size(), r = cluster_rank();
+  const uint32_t team = threadIdx.x >> TL, tq = threadIdx.x & (tpc - 1);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // rank r's share of every channel stream: a balanced split in 32-bit arithmetic
+  const uint32_t base = g.Lv / KC, rem = g.Lv - base * KC;
+  const uint32_t j0 = r * base + min(r, rem);
+  const uint32_t j1 = j0 + base + (r < rem ? 1u : 0u);
+  const uint32_t nq = (g.C + nch - 1) / nch;
+  for (uint32_t q = blockIdx.x / KC; q < nq; q += gridDim.x / KC) {
+    const uint32_t c = q * nch + team;
+    const bool live = c < g.C;
+    const bool fin = live && tq == 0 && team % KC == r;
+    Op o = op;
+    if (fin) o.prefetch_async(c, &spre[team]);  // lands while the data streams
+    double S1 = 0.0, S2 = 0.0;
+    if (live) {
+      o.init(g, c);
+      reduce_range(g, c, j0 + tq, j1, tpc, o, S1, S2);
+    }
+    S1 = warp_sum(S1);
+    S2 = warp_sum(S2);
+    if (l == 0) wpart[w] = make_double2(S1, S2);
+    if (fin) cp_async_wait_all();
+    __syncthreads();
+    if (tq == 0) {
+      double2 t = wpart[team * wpt];
+#pragma unroll
+      for (uint32_t k = 1; k < wpt; ++k) {
+        t.x += wpart[team * wpt + k].x;
+        t.y += wpart[team * wpt + k].y;
+      }
+      cpart[team] = t;
+    }
+    if (KC > 1) cluster_barrier(); else __syncthreads();
+    if (fin) {
+      double a = 0.0, b = 0.0;
+      for (uint32_t k = 0; k < KC; ++k) {
+        const double2 t = ld_dsmem(&cpart[team], k);
+        a += t.x;
+        b += t.y;
+      }
+      o.finish(g, c, a, b, out, spre[team]);
+    }
+    // wpart/cpart are reused by the next q; peers may still be reading cpart over DSMEM
+    if (KC > 1) cluster_barrier(); else __syncthreads();
   }
 }
 
@@ -999,6 +1134,7 @@ int validate_shape(int64_t N, int64_t C, int64_t HW, int layout) {
 struct Plan {
   int vec;
   bool team;
+  bool ct;   // NCHW: cluster-team reduction (k_reduce_ct) when it fills the GPU
   bool tma;  // NCHW, HW % 4 == 0, 16-byte aligned, CGBN_PATH=tma
   Geom g;
   tma::TGeom tg;
@@ -1037,6 +1173,7 @@ int make_plan(int64_t N, int64_t C, int64_t HW, int layout, const void* const* p
   g.tpc_log2 = tl;
   out->vec = vec;
   out->team = g.Lv <= kTeamMaxLv;
+  out->ct = layout == CGBN_LAYOUT_NCHW && !getenv("CGBN_NO_CT");
   out->g = g;
   out->elems = N * C * HW;
   out->tma = layout == CGBN_LAYOUT_NCHW && HW % 4 == 0 && (align % 16) == 0 &&
@@ -1084,9 +1221,151 @@ unsigned team_grid(K kernel, const Plan& pl) {
   return (unsigned)(grid < 1 ? 1 : grid);
 }
 
+// Clusters of `kc` CTAs of `kernel` that can be co-resident (cached; 0 if unsupported).
+std::map<std::tuple<const void*, int, int>, int> g_cluster_cache;
+
+template <class K>
+int64_t cluster_capacity(K kernel, uint32_t kc) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, (int)kc);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cluster_cache.find(key);
+    if (it != g_cluster_cache.end()) return (int64_t)it->second * kc;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kc * 64);
+  cfg.blockDim = dim3(kThreads);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cluster_cache[key] = n;
+  return (int64_t)n * kc;
+}
+
+struct CtCfg {
+  int tl;
+  uint32_t kc, grid;
+};
+
+// Cluster-team configuration, from the lab sweep (tools/flatlab.cu "sweep", B200,
+// ResNet-50 shapes). Cluster sizes are powers of two; U = vector loads of each input a
+// thread keeps in flight per round.
+//  - latency-bound (the whole stream fits in one round of the resident slots): the
+//    fewest CTAs whose threads need a single round, unclustered first (a cluster costs
+//    ~1 us of barrier + DSMEM at these sizes);
+//  - bandwidth-bound: the largest grid that fits in one wave (bytes in flight), then the
+//    smaller cluster, then the larger team.
+// Returns false when nothing fills a quarter of the slots (tiny C: the flat kernel
+// spreads one channel over more CTAs than a cluster holds).
+template <class Op>
+int64_t ct_cluster_cap(int tl, uint32_t kc) {
+  switch (tl) {
+    case 8: return cluster_capacity(k_reduce_ct<Op, 8>, kc);
+    case 7: return cluster_capacity(k_reduce_ct<Op, 7>, kc);
+    case 6: return cluster_capacity(k_reduce_ct<Op, 6>, kc);
+    default: return cluster_capacity(k_reduce_ct<Op, 5>, kc);
+  }
+}
+
+template <class Op>
+bool choose_ct(const Plan& pl, CtCfg* cfg) {
+  constexpr int64_t U = unroll_for<Op::kVec, Op::kIn>();
+  const int64_t slots = resident_ctas(k_reduce_ct<Op, 8>);
+  const int64_t C = pl.g.C, Lv = pl.g.Lv;
+  bool latency_bound = C * Lv <= slots * kThreads * U;
+  int64_t best_n = 0;
+  double best = 1e30;
+again:
+  for (uint32_t kc = 1; kc <= 8; kc *= 2) {
+    for (int tl = 8; tl >= 5; --tl) {
+      const int64_t tpc = 1 << tl;
+      if (kc > 1 && Lv / kc < tpc) continue;  // every thread keeps >= 1 unit
+      const int64_t n = ceil_div(C, (int64_t)kThreads >> tl) * kc;
+      if (n > slots) continue;
+      const int64_t units = ceil_div(Lv, (int64_t)kc * tpc);
+      double score;
+      if (latency_bound) {
+        if (units > U) continue;
+        score = (kc > 1 ? 1e6 : 0.0) + (double)n;  // unclustered, then fewest CTAs
+      } else {
+        score = -(double)n * 16.0 + kc;  // most CTAs, then smallest cluster
+      }
+      if (score >= best) continue;
+      if (kc > 1 && n > ct_cluster_cap<Op>(tl, kc)) continue;
+      best = score;
+      best_n = n;
+      cfg->tl = tl;
+      cfg->kc = kc;
+      cfg->grid = (uint32_t)n;
+    }
+  }
+  if (latency_bound && best_n == 0) {
+    latency_bound = false;  // no single-round configuration: rank by fill instead
+    goto again;
+  }
+  if (getenv("CGBN_DEBUG_PLAN"))
+    fprintf(stderr, "[cgbn] ct C=%lld Lv=%lld in=%d slots=%lld %s -> tl=%d kc=%u grid=%lld\n",
+            (long long)C, (long long)Lv, Op::kIn, (long long)slots,
+            latency_bound ? "latency" : "bandwidth", best_n ? cfg->tl : -1, best_n ? cfg->kc : 0,
+            (long long)best_n);
+  if (best_n == 0 && ceil_div(C, kThreads >> 5) > slots) {
+    // very wide layers: 8 channels per CTA, CTAs loop over channel groups
+    cfg->tl = 5;
+    cfg->kc = 1;
+    cfg->grid = (uint32_t)slots;
+    return true;
+  }
+  return best_n * 4 >= slots;
+}
+
+template <class Op, int TL>
+int launch_ct(Geom g, const Op& op, double* out, uint32_t kc, cudaStream_t st) {
+  if (kc == 1) {
+    k_reduce_ct<Op, TL><<<g.grid, kThreads, 0, st>>>(g, op, out);
+    return CGBN_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce_ct<Op, TL>, g, op, out);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cluster reduction launch failed: %s", cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
 template <class Op>
 int launch_reduce(const Plan& pl, const Op& op, double* out, const WsView& w, cudaStream_t st) {
   Geom g = pl.g;
+  CtCfg cc;
+  if (pl.ct && choose_ct<Op>(pl, &cc)) {
+    g.grid = cc.grid;
+    switch (cc.tl) {
+      case 8: return launch_ct<Op, 8>(g, op, out, cc.kc, st);
+      case 7: return launch_ct<Op, 7>(g, op, out, cc.kc, st);
+      case 6: return launch_ct<Op, 6>(g, op, out, cc.kc, st);
+      default: return launch_ct<Op, 5>(g, op, out, cc.kc, st);
+    }
+  }
   if (pl.team) {
     g.grid = team_grid(k_reduce_team<Op>, pl);
     k_reduce_team<Op><<<g.grid, kThreads, 0, st>>>(g, op, out);
