@@ -291,6 +291,14 @@ __device__ __forceinline__ double bn_out(double P, double Q, float x) {
   return __fma_rn(P, (double)x, Q);
 }
 
+// Programmatic dependent launch. The reductions and finalize kernels let the following
+// elementwise kernel launch early; it prefetches its first round of x / dy (complete
+// before the reduction started) and waits for the coefficients with griddepcontrol.wait.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -650,6 +658,7 @@ template <class Op>
 __global__ void __launch_bounds__(kThreads, 3)
 k_reduce_flat(Geom g, Op op, double* __restrict__ out, double2* __restrict__ ws,
               unsigned* __restrict__ tickets) {
+  pdl_trigger();
   __shared__ double sa[kWarps], sb[kWarps];
   __shared__ double s_S1[kMaxSegF], s_S2[kMaxSegF];
   __shared__ typename Op::Init s_init[kMaxSegF];
@@ -732,6 +741,7 @@ k_reduce_flat(Geom g, Op op, double* __restrict__ out, double2* __restrict__ ws,
 template <class Op>
 __global__ void __launch_bounds__(kThreads, 3)
 k_reduce_team(Geom g, Op op, double* __restrict__ out) {
+  pdl_trigger();
   __shared__ double sa[kWarps], sb[kWarps];
   const uint32_t tpc = 1u << g.tpc_log2;
   const uint32_t cpt = kThreads >> g.tpc_log2;
@@ -799,6 +809,7 @@ __device__ __forceinline__ double2 ld_dsmem(const double2* p, uint32_t rank) {
 template <class Op, int TL>
 __global__ void __launch_bounds__(kThreads, 4)
 k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
+  pdl_trigger();
   constexpr uint32_t tpc = 1u << TL;
   constexpr uint32_t nch = kThreads >> TL;
   constexpr uint32_t wpt = tpc / 32;
@@ -857,6 +868,7 @@ k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
 // Finalize kernels (one thread per channel): group partials -> coefficient tables.
 
 __global__ void k_finalize_fwd(Parts parts, FwdFinal F) {
+  pdl_trigger();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= F.C) return;
   double n, mean, M2, P, Q;
@@ -865,6 +877,7 @@ __global__ void k_finalize_fwd(Parts parts, FwdFinal F) {
 }
 
 __global__ void k_finalize_bwd(Parts parts, BwdFinal F) {
+  pdl_trigger();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= F.C) return;
   const uint32_t C = F.C;
@@ -930,11 +943,16 @@ k_ew_affine(EwGeom g, const float* __restrict__ x, float* __restrict__ y,
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* y4 = reinterpret_cast<float4*>(y);
   const uint32_t stride = gridDim.x * kThreads;
-  for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < g.n4; i += kEwU * stride) {
-    float4 v[kEwU];
+  uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  float4 v[kEwU];
+  auto load = [&](uint32_t i0) {
 #pragma unroll
     for (int u = 0; u < kEwU; ++u)
-      if (i + u * stride < g.n4) v[u] = __ldg(&x4[i + u * stride]);
+      if (i0 + u * stride < g.n4) v[u] = __ldg(&x4[i0 + u * stride]);
+  };
+  load(i);    // x is not written by the kernel we may overlap with
+  pdl_wait();  // the coefficient table is
+  for (; i < g.n4; i += kEwU * stride) {
 #pragma unroll
     for (int u = 0; u < kEwU; ++u) {
       const uint32_t j = i + u * stride;
@@ -955,6 +973,7 @@ k_ew_affine(EwGeom g, const float* __restrict__ x, float* __restrict__ y,
       }
       y4[j] = make_float4(o[0], o[1], o[2], o[3]);
     }
+    load(i + kEwU * stride);
   }
   if (blockIdx.x == 0 && threadIdx.x < g.tail) {
     const uint32_t e = 4 * g.n4 + threadIdx.x;
@@ -975,14 +994,19 @@ k_ew_dx(EwGeom g, const float* __restrict__ dy, const float* __restrict__ x,
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* d4 = reinterpret_cast<float4*>(dx);
   const uint32_t stride = gridDim.x * kThreads;
-  for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < g.n4; i += kEwU * stride) {
-    float4 gv[kEwU], xv[kEwU];
+  uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  float4 gv[kEwU], xv[kEwU];
+  auto load = [&](uint32_t i0) {
 #pragma unroll
     for (int u = 0; u < kEwU; ++u)
-      if (i + u * stride < g.n4) {
-        gv[u] = __ldg(&g4[i + u * stride]);
-        xv[u] = __ldg(&x4[i + u * stride]);
+      if (i0 + u * stride < g.n4) {
+        gv[u] = __ldg(&g4[i0 + u * stride]);
+        xv[u] = __ldg(&x4[i0 + u * stride]);
       }
+  };
+  load(i);    // dy and x are not written by the kernel we may overlap with
+  pdl_wait();  // the coefficient tables are
+  for (; i < g.n4; i += kEwU * stride) {
 #pragma unroll
     for (int u = 0; u < kEwU; ++u) {
       const uint32_t j = i + u * stride;
@@ -1010,6 +1034,7 @@ k_ew_dx(EwGeom g, const float* __restrict__ dy, const float* __restrict__ x,
       }
       d4[j] = make_float4(o[0], o[1], o[2], o[3]);
     }
+    load(i + kEwU * stride);
   }
   if (blockIdx.x == 0 && threadIdx.x < g.tail) {
     const uint32_t e = 4 * g.n4 + threadIdx.x;
@@ -1530,31 +1555,60 @@ unsigned ew_grid(K kernel, const EwPlan& ep) {
   return (unsigned)(grid < 1 ? 1 : grid);
 }
 
+// Elementwise launches allow programmatic dependent launch (CGBN_NO_PDL=1 disables it).
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("CGBN_NO_PDL") ? 0 : 1;
+  return v == 1;
+}
+
+template <class K, class... Args>
+void launch_pdl(K kernel, unsigned grid, bool pdl, cudaStream_t st, Args... args) {
+  if (!pdl || !pdl_enabled()) {
+    kernel<<<grid, kThreads, 0, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// pdl: the kernel before this launch on `st` is one of ours that does not write x
+// (a reduction, finalize or coefficient kernel), so x may be prefetched before the
+// dependency wait.
 template <bool RELU, int CM>
 void launch_ew_affine_t(const EwPlan& ep, const float* x, float* y, const double* P,
-                        const double* Q, cudaStream_t st) {
-  k_ew_affine<RELU, CM><<<ew_grid(k_ew_affine<RELU, CM>, ep), kThreads, 0, st>>>(ep.g, x, y, P,
-                                                                                 Q);
+                        const double* Q, bool pdl, cudaStream_t st) {
+  launch_pdl(k_ew_affine<RELU, CM>, ew_grid(k_ew_affine<RELU, CM>, ep), pdl, st, ep.g, x, y, P,
+             Q);
 }
 
 void launch_ew_affine(const EwPlan& ep, bool relu, const float* x, float* y, const double* P,
-                      const double* Q, cudaStream_t st) {
+                      const double* Q, cudaStream_t st, bool pdl = true) {
   if (relu) {
-    if (ep.cm == 0) launch_ew_affine_t<true, 0>(ep, x, y, P, Q, st);
-    else if (ep.cm == 1) launch_ew_affine_t<true, 1>(ep, x, y, P, Q, st);
-    else launch_ew_affine_t<true, 2>(ep, x, y, P, Q, st);
+    if (ep.cm == 0) launch_ew_affine_t<true, 0>(ep, x, y, P, Q, pdl, st);
+    else if (ep.cm == 1) launch_ew_affine_t<true, 1>(ep, x, y, P, Q, pdl, st);
+    else launch_ew_affine_t<true, 2>(ep, x, y, P, Q, pdl, st);
   } else {
-    if (ep.cm == 0) launch_ew_affine_t<false, 0>(ep, x, y, P, Q, st);
-    else if (ep.cm == 1) launch_ew_affine_t<false, 1>(ep, x, y, P, Q, st);
-    else launch_ew_affine_t<false, 2>(ep, x, y, P, Q, st);
+    if (ep.cm == 0) launch_ew_affine_t<false, 0>(ep, x, y, P, Q, pdl, st);
+    else if (ep.cm == 1) launch_ew_affine_t<false, 1>(ep, x, y, P, Q, pdl, st);
+    else launch_ew_affine_t<false, 2>(ep, x, y, P, Q, pdl, st);
   }
 }
 
 template <bool RELU, int CM>
 void launch_ew_dx_t(const EwPlan& ep, const float* dy, const float* x, float* dx,
                     const WsView& w, cudaStream_t st) {
-  k_ew_dx<RELU, CM><<<ew_grid(k_ew_dx<RELU, CM>, ep), kThreads, 0, st>>>(
-      ep.g, dy, x, dx, w.A, w.B, w.Cc, w.P, w.Q);
+  launch_pdl(k_ew_dx<RELU, CM>, ew_grid(k_ew_dx<RELU, CM>, ep), true, st, ep.g, dy, x, dx,
+             (const double*)w.A, (const double*)w.B, (const double*)w.Cc, (const double*)w.P,
+             (const double*)w.Q);
 }
 
 void launch_ew_dx(const EwPlan& ep, bool relu, const float* dy, const float* x, float* dx,
@@ -1815,7 +1869,8 @@ int cgbn_channel_affine(const float* x, int64_t N, int64_t C, int64_t HW, int la
   const void* ptrs[] = {x, out};
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
-  launch_ew_affine(ep, false, x, out, scale, shift, reinterpret_cast<cudaStream_t>(stream));
+  // no PDL: the previous kernel on the stream may be the caller's producer of x
+  launch_ew_affine(ep, false, x, out, scale, shift, reinterpret_cast<cudaStream_t>(stream), false);
   return check_launch("cgbn_channel_affine");
 }
 
