@@ -291,9 +291,11 @@ __device__ __forceinline__ double bn_out(double P, double Q, float x) {
   return __fma_rn(P, (double)x, Q);
 }
 
-// Programmatic dependent launch. The reductions and finalize kernels let the following
-// elementwise kernel launch early; it prefetches its first round of x / dy (complete
-// before the reduction started) and waits for the coefficients with griddepcontrol.wait.
+// Programmatic dependent launch (CGBN_NO_PDL=1 disables it). Every kernel waits
+// (griddepcontrol.wait) before reading what the previous kernel may have produced and
+// then lets the next one launch. The elementwise kernels prefetch their first round of
+// x / dy before waiting: they always follow one of our reduction / finalize kernels,
+// which passed its own wait, so x / dy are complete; only the coefficients are not.
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -658,6 +660,7 @@ template <class Op>
 __global__ void __launch_bounds__(kThreads, 3)
 k_reduce_flat(Geom g, Op op, double* __restrict__ out, double2* __restrict__ ws,
               unsigned* __restrict__ tickets) {
+  pdl_wait();  // inputs may come from the previous kernel (PDL launch)
   pdl_trigger();
   __shared__ double sa[kWarps], sb[kWarps];
   __shared__ double s_S1[kMaxSegF], s_S2[kMaxSegF];
@@ -741,6 +744,7 @@ k_reduce_flat(Geom g, Op op, double* __restrict__ out, double2* __restrict__ ws,
 template <class Op>
 __global__ void __launch_bounds__(kThreads, 3)
 k_reduce_team(Geom g, Op op, double* __restrict__ out) {
+  pdl_wait();  // inputs may come from the previous kernel (PDL launch)
   pdl_trigger();
   __shared__ double sa[kWarps], sb[kWarps];
   const uint32_t tpc = 1u << g.tpc_log2;
@@ -809,6 +813,7 @@ __device__ __forceinline__ double2 ld_dsmem(const double2* p, uint32_t rank) {
 template <class Op, int TL>
 __global__ void __launch_bounds__(kThreads, 4)
 k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
+  pdl_wait();  // inputs may come from the previous kernel (PDL launch)
   pdl_trigger();
   constexpr uint32_t tpc = 1u << TL;
   constexpr uint32_t nch = kThreads >> TL;
@@ -868,6 +873,7 @@ k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
 // Finalize kernels (one thread per channel): group partials -> coefficient tables.
 
 __global__ void k_finalize_fwd(Parts parts, FwdFinal F) {
+  pdl_wait();  // inputs may come from the previous kernel (PDL launch)
   pdl_trigger();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= F.C) return;
@@ -877,6 +883,7 @@ __global__ void k_finalize_fwd(Parts parts, FwdFinal F) {
 }
 
 __global__ void k_finalize_bwd(Parts parts, BwdFinal F) {
+  pdl_wait();  // inputs may come from the previous kernel (PDL launch)
   pdl_trigger();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= F.C) return;
@@ -940,6 +947,7 @@ template <bool RELU, int CM>
 __global__ void __launch_bounds__(kThreads)
 k_ew_affine(EwGeom g, const float* __restrict__ x, float* __restrict__ y,
             const double* __restrict__ P, const double* __restrict__ Q) {
+  pdl_trigger();  // the next reduction may launch and wait
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* y4 = reinterpret_cast<float4*>(y);
   const uint32_t stride = gridDim.x * kThreads;
@@ -990,6 +998,7 @@ k_ew_dx(EwGeom g, const float* __restrict__ dy, const float* __restrict__ x,
         float* __restrict__ dx, const double* __restrict__ A, const double* __restrict__ B,
         const double* __restrict__ Cc, const double* __restrict__ P,
         const double* __restrict__ Q) {
+  pdl_trigger();  // the next reduction may launch and wait
   const float4* g4 = reinterpret_cast<const float4*>(dy);
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* d4 = reinterpret_cast<float4*>(dx);
@@ -1280,6 +1289,31 @@ unsigned team_grid(K kernel, const Plan& pl) {
   return (unsigned)(grid < 1 ? 1 : grid);
 }
 
+// Launch with programmatic dependent launch allowed (see pdl_trigger / pdl_wait).
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("CGBN_NO_PDL") ? 0 : 1;
+  return v == 1;
+}
+
+template <class K, class... Args>
+void launch_pdl(K kernel, unsigned grid, bool pdl, cudaStream_t st, Args... args) {
+  if (!pdl || !pdl_enabled()) {
+    kernel<<<grid, kThreads, 0, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Clusters of `kc` CTAs of `kernel` that can be co-resident (cached; 0 if unsupported).
 std::map<std::tuple<const void*, int, int>, int> g_cluster_cache;
 
@@ -1391,21 +1425,26 @@ again:
 
 template <class Op, int TL>
 int launch_ct(Geom g, const Op& op, double* out, uint32_t kc, cudaStream_t st) {
-  if (kc == 1) {
-    k_reduce_ct<Op, TL><<<g.grid, kThreads, 0, st>>>(g, op, out);
-    return CGBN_OK;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g.grid);
   cfg.blockDim = dim3(kThreads);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kc;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (kc > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = kc;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce_ct<Op, TL>, g, op, out);
   if (e != cudaSuccess)
     return set_error(CGBN_ERR_CUDA, "cluster reduction launch failed: %s", cudaGetErrorString(e));
@@ -1427,10 +1466,10 @@ int launch_reduce(const Plan& pl, const Op& op, double* out, const WsView& w, cu
   }
   if (pl.team) {
     g.grid = team_grid(k_reduce_team<Op>, pl);
-    k_reduce_team<Op><<<g.grid, kThreads, 0, st>>>(g, op, out);
+    launch_pdl(k_reduce_team<Op>, g.grid, true, st, g, op, out);
   } else {
     g.grid = flat_grid(k_reduce_flat<Op>, pl);
-    k_reduce_flat<Op><<<g.grid, kThreads, 0, st>>>(g, op, out, w.slots, w.tickets);
+    launch_pdl(k_reduce_flat<Op>, g.grid, true, st, g, op, out, w.slots, w.tickets);
   }
   return CGBN_OK;
 }
@@ -1553,31 +1592,6 @@ unsigned ew_grid(K kernel, const EwPlan& ep) {
   const int64_t want = ceil_div((int64_t)ep.g.n4 + 1, kThreads * kEwU);
   if (want < grid) grid = want;
   return (unsigned)(grid < 1 ? 1 : grid);
-}
-
-// Elementwise launches allow programmatic dependent launch (CGBN_NO_PDL=1 disables it).
-bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) v = getenv("CGBN_NO_PDL") ? 0 : 1;
-  return v == 1;
-}
-
-template <class K, class... Args>
-void launch_pdl(K kernel, unsigned grid, bool pdl, cudaStream_t st, Args... args) {
-  if (!pdl || !pdl_enabled()) {
-    kernel<<<grid, kThreads, 0, st>>>(args...);
-    return;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 // pdl: the kernel before this launch on `st` is one of ours that does not write x
@@ -1803,7 +1817,7 @@ int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int lay
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
-  k_finalize_fwd<<<chan_blocks(C), 256, 0, st>>>(parts, F);
+  launch_pdl(k_finalize_fwd, chan_blocks(C), true, st, parts, F);
   launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
   return check_launch("cgbn_fwd_normalize");
 }
@@ -1907,7 +1921,7 @@ int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t H
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const BwdFinal F =
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
-  k_finalize_bwd<<<chan_blocks(C), 256, 0, st>>>(parts, F);
+  launch_pdl(k_finalize_bwd, chan_blocks(C), true, st, parts, F);
   launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
   return check_launch("cgbn_bwd_dx");
 }
