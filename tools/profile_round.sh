@@ -3,7 +3,7 @@
 # GPU tests, graph-mode per-kernel microbenchmarks, the full bench line, the ncu launch
 # list of one bench step, and ncu --set full captures of the dominant kernels.
 set -u
-OUT=gpurun_out/prof_round
+OUT=${1:-gpurun_out/prof_round}
 mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 300 python tools/kbench.py --graph > $OUT/kbench_graph.jsonl 2>&1
@@ -18,6 +18,10 @@ $CMD > $OUT/step_plain.json 2>&1 && \
 # full sets of the dominant kernels on the largest ResNet-50 shape
 K="python tools/kbench.py --shape 32,256,56,56 --iters 3"
 $K > $OUT/kb_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_ew_dx|k_reduce_flat|k_ew_affine" \
+  ncu --set full --clock-control none --import-source on -k regex:"k_ew_dx|k_reduce|k_ew_affine" \
       -s 0 -c 12 -o $OUT/full $K > $OUT/ncu_full.log 2>&1
+K2="python tools/kbench.py --shape 32,128,28,28 --iters 3"
+$K2 > $OUT/kb2_plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_reduce" \
+      -s 0 -c 4 -o $OUT/full_mid $K2 > $OUT/ncu_full_mid.log 2>&1
 echo done
