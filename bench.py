@@ -35,20 +35,50 @@ UNIT = "GB/s"
 BYTES_PER_ELEM = 32  # fwd 12 + bwd 20
 
 
-def resnet50_bn_shapes(batch=32):
-    """The 53 BN layers of torchvision ResNet-50 (v1.5: stride on conv2) at 224x224."""
-    shapes = [(batch, 64, 112, 112)]  # stem bn1
-    cfg = [(64, 256, 3, 56, 56), (128, 512, 4, 56, 28), (256, 1024, 6, 28, 14),
-           (512, 2048, 3, 14, 7)]
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _cdiv(a, b):
+    return -(-a // b)
+
+
+def resnet50_bn_shapes(batch=32, h=224, w=None):
+    """The 53 BN layers of torchvision ResNet-50 (v1.5: stride on conv2); feature maps
+    are ceil(input / stride) (224x224 -> 112, 56, 28, 14, 7)."""
+    w = h if w is None else w
+    sh, sw = _cdiv(h, 2), _cdiv(w, 2)
+    shapes = [(batch, 64, sh, sw)]  # stem bn1
+    res = [(_cdiv(h, s), _cdiv(w, s)) for s in (4, 8, 16, 32)]
+    cfg = [(64, 256, 3, res[0], res[0]), (128, 512, 4, res[0], res[1]),
+           (256, 1024, 6, res[1], res[2]), (512, 2048, 3, res[2], res[3])]
     for width, out, blocks, in_hw, hw in cfg:
         for b in range(blocks):
             h1 = in_hw if b == 0 else hw
-            shapes.append((batch, width, h1, h1))   # bn1 (after 1x1 conv, input res)
-            shapes.append((batch, width, hw, hw))   # bn2 (after strided 3x3)
-            shapes.append((batch, out, hw, hw))     # bn3
+            shapes.append((batch, width) + h1)   # bn1 (after 1x1 conv, input res)
+            shapes.append((batch, width) + hw)   # bn2 (after strided 3x3)
+            shapes.append((batch, out) + hw)     # bn3
             if b == 0:
-                shapes.append((batch, out, hw, hw))  # downsample bn
+                shapes.append((batch, out) + hw)  # downsample bn
     return shapes
+
+
+def fpn_neck_shapes(batch=2, h=800, w=1333, c=256):
+    """One BN per FPN level P2..P6 at 800x1333."""
+    return [(batch, c, _cdiv(h, s), _cdiv(w, s)) for s in (4, 8, 16, 32, 64)]
+
+
+# SURVEY.md 8(d) configurations. The default (what the driver runs) is config 2.
+WORKLOADS = {
+    "resnet50_bn_b32": ("config 2: ResNet-50 BN layers, 32 images/GPU at 224x224",
+                        lambda: resnet50_bn_shapes(32)),
+    "fpn_neck_800x1333": ("config 3: FPN neck BN (C=256, P2..P6), 2 images/GPU at 800x1333",
+                          lambda: fpn_neck_shapes(2)),
+    "megdet_r50fpn_800x1333": ("config 4: MegDet R50 backbone + FPN neck BN, 2 images/GPU "
+                               "at 800x1333", lambda: resnet50_bn_shapes(2, 800, 1333)
+                               + fpn_neck_shapes(2)),
+    "latency_2048x7x7": ("config 5: one latency-bound layer [1,2048,7,7]",
+                         lambda: [(1, 2048, 7, 7)]),
+}
 
 
 def numel(s):
@@ -187,7 +217,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     n = args.gpus
-    shapes = resnet50_bn_shapes(32)
+    shapes = WORKLOADS[args.workload][1]()
     bb = _reference_module()
     kind = "reference" if bb is not None else "port"
     # warmup
@@ -213,7 +243,7 @@ def run_reference_arm(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": "resnet50_bn_b32 (sampled: batch 2 per layer-step)",
+        "config": {"workload": f"{args.workload} (sampled: batch 2 per layer-step)",
                    "parallelism": f"cgbn_group{n}", "bn_group_size": n},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample, "host_cpus": os.cpu_count()},
@@ -345,7 +375,7 @@ def run_gpu_arm(args):
     cg.set_strict(False)
     cg.set_fused(args.fused)
 
-    shapes = resnet50_bn_shapes(32)
+    shapes = WORKLOADS[args.workload][1]()
     elems = [numel(s) for s in shapes]
     step_bytes_rank = BYTES_PER_ELEM * sum(elems)
     gen = torch.Generator(device=dev)
@@ -381,13 +411,21 @@ def run_gpu_arm(args):
 
     use_graph = not args.no_graph
     graph = None
+    graph_note = "cuda graph of the whole step" if use_graph else "eager"
     if use_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
-        for _ in range(2):
-            graph.replay()
-        torch.cuda.synchronize()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 - e.g. a collective that cannot be captured
+            print(f"[bench] graph capture failed ({exc!r}); timing eager steps", file=sys.stderr)
+            graph = None
+            graph_note = "eager (graph capture failed)"
+            torch.cuda.synchronize()
+            barrier()
 
     def run_once():
         if graph is not None:
@@ -401,16 +439,31 @@ def run_gpu_arm(args):
     time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for _ in range(args.steps):
-        run_once()
-    t1.record()
-    torch.cuda.synchronize()
+    # Working sets under 2x L2 (the small SURVEY configs) are timed step by step with an
+    # L2 flush (256 MB write) between steps, outside the timed events.
+    l2_flush = 8 * sum(elems) < 2 * L2_BYTES
+    if l2_flush:
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for e0, e1 in evs:
+            flush_buf.zero_()
+            e0.record()
+            run_once()
+            e1.record()
+        torch.cuda.synchronize()
+        ms_total = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    else:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            run_once()
+        t1.record()
+        torch.cuda.synchronize()
+        ms_total = t0.elapsed_time(t1)
     barrier()
     clocks = sampler.stop()
-    ms_total = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([ms_total], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -531,9 +584,9 @@ def run_gpu_arm(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = cpu_sample(shapes, 1, args.cpu_budget_s)
         cpu = {"value": res["gbs"], "unit": UNIT, "cores": 1, "kind": res["kind"],
-               "sample": (f"{res['units']} ResNet-50 BN layer shapes at batch 2 (cycling the "
-                          f"53 layers), f64, sync_bn_forward+backward via "
-                          f"DeviceGroup(1); {res['seconds']:.1f} s"),
+               "sample": (f"{res['units']} {args.workload} BN layer shapes at batch 2 "
+                          f"(cycling the {len(shapes)} layers), f64, sync_bn_forward+backward"
+                          f" via DeviceGroup(1); {res['seconds']:.1f} s"),
                "host_cpus": os.cpu_count()}
 
     if world > 1:
@@ -544,15 +597,19 @@ def run_gpu_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (fp64 statistics)", "data": "synthetic (torch.randn, seeded per rank)",
-            "config": {"workload": "resnet50_bn_b32", "layers": len(shapes),
-                       "per_gpu_batch": 32, "elements_per_gpu": sum(elems),
+            "config": {"workload": args.workload, "describe": WORKLOADS[args.workload][0],
+                       "layers": len(shapes),
+                       "per_gpu_batch": shapes[0][0], "elements_per_gpu": sum(elems),
                        "alg_bytes_per_elem": BYTES_PER_ELEM,
                        "parallelism": f"cgbn_group{world}", "bn_group_size": world,
                        "layout": "NCHW", "relu": False,
-                       "l2_policy": ("inputs > L2: 53 layers' x+dy = "
-                                     f"{8 * sum(elems) / 1e9:.2f} GB per step >> 126 MB L2; "
-                                     "intra-layer re-reads of x may hit L2"),
-                       "cuda_graph": use_graph},
+                       "l2_policy": (("L2 flushed (256 MB write) before every timed step; "
+                                      f"x+dy = {8 * sum(elems) / 1e6:.1f} MB per step")
+                                     if l2_flush else
+                                     (f"inputs > L2: {len(shapes)} layers' x+dy = "
+                                      f"{8 * sum(elems) / 1e9:.2f} GB per step >> 126 MB L2; "
+                                      "intra-layer re-reads of x may hit L2")),
+                       "cuda_graph": graph is not None, "launch": graph_note},
             "per_gpu_gbs": value / world,
             "per_gpu_hbm_frac": value / world / hbm_peak,
             "kernels": kern,
@@ -575,6 +632,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet50_bn_b32",
+                    help="SURVEY 8(d) configuration (default: config 2, the driver's)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes/launch of the dominant kernel (recorded as-is)")
