@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CGBN_ABI_VERSION 2
+#define CGBN_ABI_VERSION 3
 
 #define CGBN_LAYOUT_NCHW 0
 #define CGBN_LAYOUT_NHWC 1
@@ -167,6 +167,30 @@ int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void*
  * NULL. ws as for cgbn_fwd_stats. */
 int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
                      double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream);
+
+/* Reference-literal forward statistics (bigbatch's own algorithm, selected with
+ * set_forward_exchange("reference")). Two-pass (the reference
+ * default, batchnorm.py:125-132): cgbn_channel_sum -> exchange [sum | m] ->
+ * cgbn_centered_sumsq -> exchange -> cgbn_fwd_normalize_sums(centered = 1). One-pass
+ * (batchnorm.py:119-124): cgbn_channel_sum with sum_sq -> exchange [sum | sum_sq | m] ->
+ * cgbn_fwd_normalize_sums(centered = 0).
+ *
+ * cgbn_centered_sumsq: out[c] = sum over this rank's elements of (x - mean_c)^2 in fp64,
+ * with mean_c = sum[c] / count[0] from the group-folded first exchange
+ * (batchnorm.py:128-129). */
+int cgbn_centered_sumsq(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                        const double* sum, const double* count, double* out, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* Normalise from group sums: mean = sum[c] / m, var = sq[c] / m (centered != 0) or
+ * max(sq[c] / m - mean^2, 0) (centered == 0), m = count[0]; then what
+ * cgbn_fwd_normalize does after its fold (batchnorm.py:121-124, 131-141). */
+int cgbn_fwd_normalize_sums(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                            const double* sum, const double* sq, const double* count,
+                            int centered, const float* gamma, const float* beta, double eps,
+                            double momentum, float* running_mean, float* running_var,
+                            double* saved, int relu, float* y, unsigned* status, void* ws,
+                            size_t ws_bytes, void* stream);
 
 /* Per-channel affine map out = scale[c] * x + shift[c] (fp64 coefficients, device
  * arrays of C doubles). Device counterpart of the reference's channel_affine

@@ -14,6 +14,7 @@ from .batchnorm import (
     bn_forward_local,
     bn_update_running,
     check_status,
+    set_forward_exchange,
     set_fused,
     set_strict,
     sync_bn_backward,
@@ -38,7 +39,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BatchNormError", "BNForwardCache", "BNLayerState", "bn_backward_local", "bn_forward_local",
-    "bn_update_running", "check_status", "set_fused", "set_strict", "sync_bn_backward", "sync_bn_forward",
+    "bn_update_running", "check_status", "set_forward_exchange", "set_fused", "set_strict", "sync_bn_backward", "sync_bn_forward",
     "DEFAULT_TIMEOUT_S", "SCOPE_BN_GROUP", "SCOPE_WORLD", "CollectiveError",
     "CollectiveProtocolError", "CollectiveTimeoutError", "DeviceGroup", "DeviceHandle",
     "DistHandle", "SoloHandle", "allreduce_sum", "ChannelStats", "NonFiniteError", "TensorError",

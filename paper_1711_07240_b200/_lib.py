@@ -55,6 +55,9 @@ SIGNATURES = {
     "cgbn_xhat": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
     "cgbn_fold_sum": (_i, [_pp, _i, _i64, _i, _p, _p]),
     "cgbn_channel_sum": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
+    "cgbn_centered_sumsq": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p, _sz, _p]),
+    "cgbn_fwd_normalize_sums": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _i, _p, _p, _d, _d,
+                                     _p, _p, _p, _i, _p, _p, _p, _sz, _p]),
     "cgbn_channel_affine": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p]),
     "cgbn_fused_supported": (_i, [_i64, _i64, _i64, _i, _i]),
     "cgbn_fwd_fused": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _d, _d, _p, _p, _p, _i, _p, _p, _p,

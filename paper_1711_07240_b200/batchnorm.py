@@ -267,6 +267,97 @@ def _local_exchange(vec, info):
     return [vec], [info]
 
 
+_exchange_mode = "merged"
+
+
+def set_forward_exchange(mode: str) -> str:
+    """How the training forward combines the ranks' statistics; returns the previous mode.
+
+    ``"merged"`` (default): one exchange per forward of each rank's fp64 (mean, M2,
+    count), merged with Chan's pairwise update in ascending rank order. It has the
+    numerics of the reference's two-pass algorithm (no E[x^2] - mean^2 cancellation)
+    for either ``one_pass`` value, at one exchange and two reads of x.
+
+    ``"reference"``: bigbatch's own arithmetic, literally (batchnorm.py:118-132).
+    ``one_pass=False`` (the reference default) exchanges [sum | m], reads x again for
+    sum (x - mean)^2 and exchanges that (two exchanges, three reads of x);
+    ``one_pass=True`` exchanges [sum | sum x^2 | m] and uses max(E[x^2] - mean^2, 0).
+    Group sums are folded in ascending rank order, like the reference's allreduce_sum.
+    """
+    global _exchange_mode
+    if mode not in ("merged", "reference"):
+        raise ValueError(f"forward exchange must be 'merged' or 'reference', got {mode!r}")
+    prev, _exchange_mode = _exchange_mode, mode
+    return prev
+
+
+def _fold_parts(parts, st):
+    """Ascending-rank fold of the exchanged fp64 vectors (collectives.py:293-295)."""
+    if len(parts) == 1:
+        return parts[0]
+    lib = _lib.load()
+    out = torch.empty_like(parts[0])
+    arr, keep = _lib.ptr_array([p.data_ptr() for p in parts])
+    _lib.check(lib.cgbn_fold_sum(arr, len(parts), parts[0].numel(), _lib.DTYPE_F64,
+                                 out.data_ptr(), st), "cgbn_fold_sum")
+    return out
+
+
+def _train_forward_reference(g, state, exchange, scope_key, one_pass, relu, what):
+    """set_forward_exchange("reference"): batchnorm.py:118-132 step by step on the
+    device (see include/cgbn.h, cgbn_centered_sumsq / cgbn_fwd_normalize_sums)."""
+    c = g.C
+    dev = g.x.device
+    lib = _lib.load()
+    st = stream_ptr(dev)
+    e = g.N * c * g.HW
+    saved = torch.empty(3 * c + 1, dtype=torch.float64, device=dev)
+    y = same_layout_like(g)
+    status = status_word(dev)
+    ws = workspace(dev, lib.cgbn_workspace_bytes(g.N, c, g.HW, g.layout))
+    n = 2 * c + 1 if one_pass else c + 1
+    packed = torch.empty(n, dtype=torch.float64, device=dev)
+    with _Span("fwd_sums", 4 * e):
+        _lib.check(lib.cgbn_channel_sum(
+            g.x.data_ptr(), g.N, c, g.HW, g.layout, packed.data_ptr(),
+            packed.data_ptr() + 8 * c if one_pass else None, ws.data_ptr(), ws.numel(), st),
+            "cgbn_channel_sum")
+    packed[n - 1:].fill_(float(g.count))  # local count (batchnorm.py:120, 126)
+    parts, infos = exchange(packed, g.count)
+    total = None
+    if infos is not None and all(i is not None for i in infos):
+        total = int(sum(infos))
+        if total < 2:
+            raise BatchNormError(
+                f"training-mode statistics need at least 2 elements per channel, got {total}")
+    tot = _fold_parts(parts, st)
+    sum_p, cnt_p = tot.data_ptr(), tot.data_ptr() + 8 * (n - 1)
+    keep = [tot]
+    if one_pass:
+        sq_p, centered = tot.data_ptr() + 8 * c, 0
+    else:
+        sq = torch.empty(c, dtype=torch.float64, device=dev)
+        with _Span("fwd_centered_sumsq", 4 * e):
+            _lib.check(lib.cgbn_centered_sumsq(
+                g.x.data_ptr(), g.N, c, g.HW, g.layout, sum_p, cnt_p, sq.data_ptr(),
+                ws.data_ptr(), ws.numel(), st), "cgbn_centered_sumsq")
+        parts2, _ = exchange(sq, None)
+        sq_t = _fold_parts(parts2, st)
+        keep.append(sq_t)
+        sq_p, centered = sq_t.data_ptr(), 1
+    rm, rv = state.running_mean.data_ptr(), state.running_var.data_ptr()
+    with _Span("fwd_normalize", 8 * e):
+        _lib.check(lib.cgbn_fwd_normalize_sums(
+            g.x.data_ptr(), g.N, c, g.HW, g.layout, sum_p, sq_p, cnt_p, centered,
+            state.gamma.data_ptr(), state.beta.data_ptr(), float(state.eps),
+            float(state.running_momentum), rm, rv, saved.data_ptr(), int(bool(relu)),
+            y.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), st),
+            "cgbn_fwd_normalize_sums")
+    _raise_status(what, status, total)
+    return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
+                             relu=bool(relu), one_pass=bool(one_pass), _total_count=total)
+
+
 def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
                    one_pass: bool, relu: bool, what: str):
     """The CGBN forward (batchnorm.py:115-144) on the device.
@@ -277,6 +368,11 @@ def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
     enabled (set_fused) and the activation fits on chip.
     """
     g = _check_layout(x, state)
+    if _exchange_mode == "reference":
+        if group_size == 1 and g.count < 2:
+            raise BatchNormError(
+                f"training-mode statistics need at least 2 elements per channel, got {g.count}")
+        return _train_forward_reference(g, state, exchange, scope_key, one_pass, relu, what)
     c = g.C
     dev = g.x.device
     lib = _lib.load()

@@ -368,10 +368,9 @@ __device__ __forceinline__ void load_fwd_chan_async(const FwdFinal& F, uint32_t 
   }
 }
 
-__device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
-                                                     double mean, double M2, bool write,
-                                                     const FwdChan& v, double& P, double& Q) {
-  const double var = fmax(M2 / n, 0.0);
+__device__ __forceinline__ void finalize_fwd_channel_var(const FwdFinal& F, uint32_t c, double n,
+                                                         double mean, double var, bool write,
+                                                         const FwdChan& v, double& P, double& Q) {
   const double inv_std = 1.0 / sqrt(var + F.eps);
   affine_coeffs(mean, inv_std, (double)v.gamma, (double)v.beta, P, Q);
   if (F.P) { F.P[c] = P; F.Q[c] = Q; }
@@ -392,6 +391,12 @@ __device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t
     F.rmean[c] = (float)((1.0 - rho) * (double)v.rmean + rho * mean);
     F.rvar[c] = (float)((1.0 - rho) * (double)v.rvar + rho * unbiased);
   }
+}
+
+__device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
+                                                     double mean, double M2, bool write,
+                                                     const FwdChan& v, double& P, double& Q) {
+  finalize_fwd_channel_var(F, c, n, mean, fmax(M2 / n, 0.0), write, v, P, Q);
 }
 
 __device__ __forceinline__ void finalize_fwd_channel(const FwdFinal& F, uint32_t c, double n,
@@ -494,7 +499,7 @@ __device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32
 // ----------------------------------------------------------------------------------
 // Reduction ops: per-channel fp64 sums of two quantities.
 
-enum FinishMode { kPartial = 0, kRawSums = 1, kLocalFinal = 2 };
+enum FinishMode { kPartial = 0, kRawSums = 1, kLocalFinal = 2, kSumSq = 3 };
 
 // Forward statistics: sums of d = x - K (K = first element of the channel on this rank,
 // the same for every CTA of the channel; d is exact in fp64) -> (mean, M2, count).
@@ -506,13 +511,16 @@ struct StatsOp {
   const float* __restrict__ x;
   double K;
   bool shift;
+  const double* __restrict__ ksum;    // kSumSq: shift by the group mean ksum[c] / *kcount
+  const double* __restrict__ kcount;
   int mode;                   // FinishMode
   double* __restrict__ out2;  // kRawSums: sum_sq destination (may be null)
   FwdFinal F;                 // kLocalFinal
   struct Regs { float v[VEC]; uint32_t m; };
   struct Init { double K; };
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
-    K = shift ? (double)__ldg(x + (size_t)c * g.HW) : 0.0;
+    if (ksum) K = ksum[c] / kcount[0];
+    else K = shift ? (double)__ldg(x + (size_t)c * g.HW) : 0.0;
   }
   __device__ __forceinline__ Init get_init() const { return Init{K}; }
   __device__ __forceinline__ void set_init(const Init& i) { K = i.K; }
@@ -547,6 +555,10 @@ struct StatsOp {
     if (mode == kRawSums) {
       out[c] = S1;
       if (out2) out2[c] = S2;
+      return;
+    }
+    if (mode == kSumSq) {  // sum of (x - group mean)^2 (reference two-pass, batchnorm.py:128-129)
+      out[c] = S2;
       return;
     }
     const double mean = K + S1 / n;
@@ -897,6 +909,22 @@ __global__ void k_finalize_bwd(Parts parts, BwdFinal F) {
 }
 
 // Eval (batchnorm.py:158-166) and x_hat coefficient tables.
+// Reference-literal statistics (batchnorm.py:119-132): group sums [sum | sq | m] ->
+// mean = sum/m, var = sq/m (two-pass: sq = sum (x - mean)^2) or max(sq/m - mean^2, 0)
+// (one-pass: sq = sum x^2), then the forward finisher.
+__global__ void k_finalize_sums(const double* __restrict__ sum, const double* __restrict__ sq,
+                                const double* __restrict__ count, int centered, FwdFinal F) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= F.C) return;
+  const double m = count[0];
+  const double mean = sum[c] / m;
+  const double var = centered ? sq[c] / m : fmax(sq[c] / m - mean * mean, 0.0);
+  double P, Q;
+  finalize_fwd_channel_var(F, c, m, mean, var, true, load_fwd_chan(F, c), P, Q);
+}
+
 __global__ void k_coef_eval(const float* gamma, const float* beta, const float* rmean,
                             const float* rvar, double eps, double* P, double* Q, uint32_t C) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1493,7 +1521,8 @@ int launch_tma_reduce(const Plan& pl, const TOp& op, double* out, const WsView& 
 // Forward statistics in mode kPartial / kRawSums / kLocalFinal.
 template <int VEC>
 int run_stats(const Plan& pl, const float* x, bool shift, int mode, double* out, double* out2,
-              const FwdFinal* F, const WsView& w, cudaStream_t st) {
+              const FwdFinal* F, const WsView& w, cudaStream_t st,
+              const double* ksum = nullptr, const double* kcount = nullptr) {
   if (VEC == 4 && pl.tma && shift && mode == kPartial) {
     tma::TmaStats op;
     op.x = x;
@@ -1504,6 +1533,8 @@ int run_stats(const Plan& pl, const float* x, bool shift, int mode, double* out,
   op.x = x;
   op.K = 0.0;
   op.shift = shift;
+  op.ksum = ksum;
+  op.kcount = kcount;
   op.mode = mode;
   op.out2 = out2;
   if (F) op.F = *F;
@@ -1537,12 +1568,13 @@ int run_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double
 }
 
 int dispatch_stats(const Plan& pl, const float* x, bool shift, int mode, double* out,
-                   double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st) {
+                   double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st,
+                   const double* ksum = nullptr, const double* kcount = nullptr) {
   switch (pl.vec) {
-    case 5: return run_stats<5>(pl, x, shift, mode, out, out2, F, w, st);
-    case 4: return run_stats<4>(pl, x, shift, mode, out, out2, F, w, st);
-    case 2: return run_stats<2>(pl, x, shift, mode, out, out2, F, w, st);
-    default: return run_stats<1>(pl, x, shift, mode, out, out2, F, w, st);
+    case 5: return run_stats<5>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+    case 4: return run_stats<4>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+    case 2: return run_stats<2>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+    default: return run_stats<1>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
   }
 }
 
@@ -1810,6 +1842,42 @@ int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layou
   pl.tma = false;
   CGBN_TRY(dispatch_stats(pl, x, false, kRawSums, sum, sum_sq, nullptr, w, st));
   return check_launch("cgbn_channel_sum");
+}
+
+int cgbn_centered_sumsq(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                        const double* sum, const double* count, double* out, void* ws,
+                        size_t ws_bytes, void* stream) {
+  CGBN_REQUIRE(x && sum && count && out, "cgbn_centered_sumsq: NULL pointer");
+  const void* ptrs[] = {x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  pl.tma = false;
+  CGBN_TRY(dispatch_stats(pl, x, false, kSumSq, out, nullptr, nullptr, w, st, sum, count));
+  return check_launch("cgbn_centered_sumsq");
+}
+
+int cgbn_fwd_normalize_sums(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+                            const double* sum, const double* sq, const double* count,
+                            int centered, const float* gamma, const float* beta, double eps,
+                            double momentum, float* running_mean, float* running_var,
+                            double* saved, int relu, float* y, unsigned* status, void* ws,
+                            size_t ws_bytes, void* stream) {
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  CGBN_REQUIRE(sum && sq && count, "cgbn_fwd_normalize_sums: NULL pointer");
+  const void* ptrs[] = {x, y};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  launch_pdl(k_finalize_sums, chan_blocks(C), true, st, sum, sq, count, centered ? 1 : 0, F);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  return check_launch("cgbn_fwd_normalize_sums");
 }
 
 int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int layout,

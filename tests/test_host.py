@@ -156,3 +156,10 @@ def test_product_path_refuses_cpu_tensors():
     h = SoloHandle(device="cpu")
     with pytest.raises(cg.CollectiveProtocolError, match="CUDA"):
         cg.allreduce_sum(h, cg.SCOPE_WORLD, torch.zeros(3))
+
+
+def test_set_forward_exchange_modes():
+    prev = cg.set_forward_exchange("reference")
+    assert cg.set_forward_exchange(prev) == "reference"
+    with pytest.raises(ValueError):
+        cg.set_forward_exchange("two_pass")
