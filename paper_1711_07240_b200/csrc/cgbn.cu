@@ -882,6 +882,165 @@ k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
 }
 
 // ----------------------------------------------------------------------------------
+// Row reductions for channels_last (NHWC) and 2-D (N, C) activations: M = N*H*W rows of
+// C contiguous floats (C % 4 == 0). Thread = one float4 of 4 adjacent channels; the
+// threads of a CTA cover a channel slice of CS4 float4 (<= 256) and rpp = 256 / CS4 rows
+// per pass, so every warp load is a contiguous 512-byte row segment. A CTA reduces a
+// block of rows; its per-channel partials are folded over the rpp thread rows in shared
+// memory (ascending) and stored in slots[c * nb + row block]; k_fold_rows then folds
+// the nb row blocks of each channel with one warp (fixed lane order + shuffle tree) and
+// runs the channel finisher of the matching NCHW op. Deterministic, no atomics.
+
+struct NGeom {
+  uint32_t M;        // rows
+  uint32_t C, C4;    // channels, float4 per row
+  uint32_t CS4;      // float4 per channel slice (<= 256)
+  uint32_t rpp;      // rows per pass = 256 / CS4
+  uint32_t nslices;  // ceil(C4 / CS4)
+  uint32_t nb;       // row blocks per slice
+};
+
+// Forward statistics over rows: the shift K of every channel is the NCHW op's (row 0).
+struct StatsRows {
+  static constexpr int kU = 8;
+  static constexpr int kIn = 1;
+  StatsOp<1> base;
+  Geom gg;
+  struct State { double K[4]; };
+  struct Regs { float4 v; };
+  __device__ __forceinline__ void init(uint32_t c4, State& s) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      StatsOp<1> o = base;
+      o.init(gg, 4 * c4 + j);
+      s.K[j] = o.K;
+    }
+  }
+  __device__ __forceinline__ void load(size_t u, Regs& r) const {
+    r.v = __ldg(reinterpret_cast<const float4*>(base.x) + u);
+  }
+  __device__ __forceinline__ void acc(const State& s, const Regs& r, double (&a)[4],
+                                      double (&b)[4]) const {
+    const float v[4] = {r.v.x, r.v.y, r.v.z, r.v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double d = (double)v[j] - s.K[j];
+      a[j] += d;
+      b[j] = __fma_rn(d, d, b[j]);
+    }
+  }
+};
+
+// Backward sums over rows: [sum g, sum g*(x - mean)] with the forward's ReLU mask.
+template <bool RELU>
+struct BwdRows {
+  static constexpr int kU = 4;
+  static constexpr int kIn = 2;
+  BwdOp<1, RELU> base;
+  Geom gg;
+  struct State { double mean[4], P[4], Q[4]; };
+  struct Regs { float4 g, x; };
+  __device__ __forceinline__ void init(uint32_t c4, State& s) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      BwdOp<1, RELU> o = base;
+      o.init(gg, 4 * c4 + j);
+      s.mean[j] = o.mean;
+      s.P[j] = RELU ? o.P : 0.0;
+      s.Q[j] = RELU ? o.Q : 0.0;
+    }
+  }
+  __device__ __forceinline__ void load(size_t u, Regs& r) const {
+    r.g = __ldg(reinterpret_cast<const float4*>(base.dy) + u);
+    r.x = __ldg(reinterpret_cast<const float4*>(base.x) + u);
+  }
+  __device__ __forceinline__ void acc(const State& s, const Regs& r, double (&a)[4],
+                                      double (&b)[4]) const {
+    const float gv[4] = {r.g.x, r.g.y, r.g.z, r.g.w};
+    const float xv[4] = {r.x.x, r.x.y, r.x.z, r.x.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double gk = (double)gv[j];
+      if (RELU && !(bn_out(s.P[j], s.Q[j], xv[j]) > 0.0)) gk = 0.0;
+      a[j] += gk;
+      b[j] = __fma_rn(gk, (double)xv[j] - s.mean[j], b[j]);
+    }
+  }
+};
+
+template <class NOp>
+__global__ void __launch_bounds__(kThreads, 3)
+k_reduce_rows(NGeom g, NOp op, double2* __restrict__ slots) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double2 sm[4][kThreads];
+  const uint32_t slice = blockIdx.x % g.nslices, rb = blockIdx.x / g.nslices;
+  const uint32_t k = threadIdx.x % g.CS4, ro = threadIdx.x / g.CS4;
+  const uint32_t c4 = slice * g.CS4 + k;
+  const bool active = ro < g.rpp && c4 < g.C4;
+  const uint32_t r0 = (uint32_t)((uint64_t)rb * g.M / g.nb);
+  const uint32_t r1 = (uint32_t)((uint64_t)(rb + 1) * g.M / g.nb);
+  double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+  if (active) {
+    typename NOp::State s;
+    op.init(c4, s);
+    constexpr int U = NOp::kU;
+    for (uint32_t r = r0 + ro; r < r1; r += U * g.rpp) {
+      typename NOp::Regs v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t rr = r + u * g.rpp;
+        if (rr < r1) op.load((size_t)rr * g.C4 + c4, v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (r + u * g.rpp < r1) op.acc(s, v[u], a, b);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sm[j][threadIdx.x] = make_double2(a[j], b[j]);
+  __syncthreads();
+  if (ro == 0 && c4 < g.C4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2 t = sm[j][k];
+      for (uint32_t q = 1; q < g.rpp; ++q) {
+        const double2 v = sm[j][q * g.CS4 + k];
+        t.x += v.x;
+        t.y += v.y;
+      }
+      slots[(size_t)(4 * c4 + j) * g.nb + rb] = t;
+    }
+  }
+}
+
+// One warp per channel: fold the nb row-block partials (lane-strided, then the fixed
+// shuffle tree) and finish the channel with the NCHW op's finisher.
+template <class Op>
+__global__ void __launch_bounds__(kThreads)
+k_fold_rows(Geom g, Op op, const double2* __restrict__ slots, uint32_t nb,
+            double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t c = (blockIdx.x * kThreads + threadIdx.x) >> 5, l = threadIdx.x & 31;
+  if (c >= g.C) return;
+  double a = 0.0, b = 0.0;
+  const double2* p = slots + (size_t)c * nb;
+  for (uint32_t i = l; i < nb; i += 32) {
+    const double2 t = __ldcg(p + i);
+    a += t.x;
+    b += t.y;
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (l == 0) {
+    Op o = op;
+    o.init(g, c);
+    o.finish(g, c, a, b, out);
+  }
+}
+
+// ----------------------------------------------------------------------------------
 // Finalize kernels (one thread per channel): group partials -> coefficient tables.
 
 __global__ void k_finalize_fwd(Parts parts, FwdFinal F) {
@@ -974,6 +1133,36 @@ __device__ __forceinline__ void chan4(const EwGeom& g, uint32_t e, uint32_t (&c)
   }
 }
 
+// Channel indices of the 4 elements of unit jm (CM 3: NHWC / 2-D with C % 4 == 0 -- the
+// float4 holds channels c0..c0+3, one division) and the matching coefficient loads.
+template <int CM>
+__device__ __forceinline__ void ew_chan(const EwGeom& g, uint32_t jm, uint32_t (&c)[4]) {
+  if constexpr (CM == 3) {
+    const uint32_t e = 4 * jm;
+    c[0] = e - g.dc.div(e) * g.C;
+    c[1] = c[0] + 1;
+    c[2] = c[0] + 2;
+    c[3] = c[0] + 3;
+  } else {
+    chan4<CM>(g, 4 * jm, c);
+  }
+}
+
+template <int CM>
+__device__ __forceinline__ void ew_coef(const double* __restrict__ T, const uint32_t (&c)[4],
+                                        double (&t)[4]) {
+  if constexpr (CM == 3) {  // 32-byte aligned: c[0] % 4 == 0 and the table is 16-aligned
+    const double2 a = __ldg(reinterpret_cast<const double2*>(T + c[0]));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(T + c[0] + 2));
+    t[0] = a.x; t[1] = a.y; t[2] = b.x; t[3] = b.y;
+  } else if constexpr (CM == 0) {
+    t[0] = t[1] = t[2] = t[3] = __ldg(T + c[0]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = __ldg(T + c[k]);
+  }
+}
+
 constexpr int kEwU = 4;
 
 template <bool RELU, int CM>
@@ -1000,16 +1189,14 @@ k_ew_affine(EwGeom g, const float* __restrict__ x, float* __restrict__ y,
       if (j >= g.n4) continue;
       const uint32_t jm = ew_unit(g, j);
       uint32_t c[4];
-      chan4<CM>(g, 4 * jm, c);
+      ew_chan<CM>(g, jm, c);
       float o[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-      double p = 0.0, q = 0.0;
+      double p[4], q[4];
+      ew_coef<CM>(P, c, p);
+      ew_coef<CM>(Q, c, q);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (CM != 0 || k == 0) {  // CM 0: one coefficient pair serves the whole float4
-          p = __ldg(&P[c[k]]);
-          q = __ldg(&Q[c[k]]);
-        }
-        double t = __fma_rn(p, (double)o[k], q);
+        double t = __fma_rn(p[k], (double)o[k], q[k]);
         if (RELU) t = t > 0.0 ? t : 0.0;
         o[k] = (float)t;
       }
@@ -1019,7 +1206,7 @@ k_ew_affine(EwGeom g, const float* __restrict__ x, float* __restrict__ y,
   }
   if (blockIdx.x == 0 && threadIdx.x < g.tail) {
     const uint32_t e = 4 * g.n4 + threadIdx.x;
-    const uint32_t c = CM == 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
+    const uint32_t c = CM >= 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
     double t = __fma_rn(P[c], (double)x[e], Q[c]);
     if (RELU) t = t > 0.0 ? t : 0.0;
     y[e] = (float)t;
@@ -1056,25 +1243,23 @@ k_ew_dx(EwGeom g, const float* __restrict__ dy, const float* __restrict__ x,
       if (j >= g.n4) continue;
       const uint32_t jm = ew_unit(g, j);
       uint32_t c[4];
-      chan4<CM>(g, 4 * jm, c);
+      ew_chan<CM>(g, jm, c);
       const float gi[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
       const float xi[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
       float o[4];
-      double a = 0.0, b = 0.0, cc = 0.0, p = 0.0, q = 0.0;
+      double a[4], b[4], cc[4], p[4] = {0.0, 0.0, 0.0, 0.0}, q[4] = {0.0, 0.0, 0.0, 0.0};
+      ew_coef<CM>(A, c, a);
+      ew_coef<CM>(B, c, b);
+      ew_coef<CM>(Cc, c, cc);
+      if (RELU) {
+        ew_coef<CM>(P, c, p);
+        ew_coef<CM>(Q, c, q);
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (CM != 0 || k == 0) {
-          a = __ldg(&A[c[k]]);
-          b = __ldg(&B[c[k]]);
-          cc = __ldg(&Cc[c[k]]);
-          if (RELU) {
-            p = __ldg(&P[c[k]]);
-            q = __ldg(&Q[c[k]]);
-          }
-        }
         double gk = (double)gi[k];
-        if (RELU && !(bn_out(p, q, xi[k]) > 0.0)) gk = 0.0;
-        o[k] = (float)__fma_rn(a, gk, __fma_rn(b, (double)xi[k], cc));
+        if (RELU && !(bn_out(p[k], q[k], xi[k]) > 0.0)) gk = 0.0;
+        o[k] = (float)__fma_rn(a[k], gk, __fma_rn(b[k], (double)xi[k], cc[k]));
       }
       d4[jm] = make_float4(o[0], o[1], o[2], o[3]);
     }
@@ -1082,7 +1267,7 @@ k_ew_dx(EwGeom g, const float* __restrict__ dy, const float* __restrict__ x,
   }
   if (blockIdx.x == 0 && threadIdx.x < g.tail) {
     const uint32_t e = 4 * g.n4 + threadIdx.x;
-    const uint32_t c = CM == 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
+    const uint32_t c = CM >= 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
     double gk = (double)dy[e];
     if (RELU && !(bn_out(P[c], Q[c], x[e]) > 0.0)) gk = 0.0;
     dx[e] = (float)__fma_rn(A[c], gk, __fma_rn(B[c], (double)x[e], Cc[c]));
@@ -1129,13 +1314,39 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Workspace: tickets + barrier words | (C + max grid) double2 per-CTA partial slots |
 // coefficient table (5 x C doubles: P, Q, A, B, Cc).
-size_t slots_bytes(int64_t N, int64_t C, int64_t HW, int sms) {
-  (void)N;
-  (void)HW;
-  return ((size_t)C + (size_t)sms * kMaxCtasPerSm) * sizeof(double2);
+// Row reductions (NHWC / 2-D, C % 4 == 0): rows per block >= 32 keeps the partial
+// slots (nb * C double2) under 1/8 of the activation bytes.
+bool rows_layout(int64_t C, int64_t HW, int layout) {
+  return (layout == CGBN_LAYOUT_NHWC || HW == 1) && C % 4 == 0 && !getenv("CGBN_NO_ROWS");
 }
-size_t ws_bytes_for(int64_t N, int64_t C, int64_t HW, int sms) {
-  return kTicketBytes + slots_bytes(N, C, HW, sms) + 5 * (size_t)C * sizeof(double);
+
+NGeom rows_geom(int64_t N, int64_t C, int64_t HW, int64_t ctas) {
+  NGeom g;
+  g.M = (uint32_t)(N * HW);
+  g.C = (uint32_t)C;
+  g.C4 = (uint32_t)(C / 4);
+  g.CS4 = g.C4 < (uint32_t)kThreads ? g.C4 : (uint32_t)kThreads;
+  g.rpp = (uint32_t)kThreads / g.CS4;
+  g.nslices = (g.C4 + g.CS4 - 1) / g.CS4;
+  int64_t nb = ceil_div(ctas, (int64_t)g.nslices);
+  const int64_t cap = (int64_t)g.M / 32;
+  if (nb > cap) nb = cap;
+  if (nb > (int64_t)g.M) nb = g.M;
+  g.nb = (uint32_t)(nb < 1 ? 1 : nb);
+  return g;
+}
+
+size_t slots_bytes(int64_t N, int64_t C, int64_t HW, int layout, int sms) {
+  size_t n = (size_t)C + (size_t)sms * kMaxCtasPerSm;
+  if (rows_layout(C, HW, layout)) {
+    const NGeom g = rows_geom(N, C, HW, (int64_t)sms * kMaxCtasPerSm);
+    const size_t r = (size_t)g.nb * (size_t)C;
+    if (r > n) n = r;
+  }
+  return n * sizeof(double2);
+}
+size_t ws_bytes_for(int64_t N, int64_t C, int64_t HW, int layout, int sms) {
+  return kTicketBytes + slots_bytes(N, C, HW, layout, sms) + 5 * (size_t)C * sizeof(double);
 }
 
 struct WsView {
@@ -1149,17 +1360,21 @@ struct WsView {
   double* Cc;
 };
 
-int ws_view(void* ws, size_t ws_bytes, int64_t N, int64_t C, int64_t HW, WsView* v) {
+int ws_view(void* ws, size_t ws_bytes, int64_t N, int64_t C, int64_t HW, int layout,
+            WsView* v) {
   const int sms = num_sms_cached();
-  const size_t need = ws_bytes_for(N, C, HW, sms);
+  const size_t need = ws_bytes_for(N, C, HW, layout, sms);
   if (!ws || ws_bytes < need)
     return set_error(CGBN_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need,
                      ws_bytes);
+  if (reinterpret_cast<uintptr_t>(ws) % 16)
+    return set_error(CGBN_ERR_INVALID, "workspace must be 16-byte aligned");
   char* b = reinterpret_cast<char*>(ws);
   v->tickets = reinterpret_cast<unsigned*>(b);
   v->bar = v->tickets + kTicketWords;
   v->slots = reinterpret_cast<double2*>(b + kTicketBytes);
-  double* coef = reinterpret_cast<double*>(b + kTicketBytes + slots_bytes(N, C, HW, sms));
+  double* coef =
+      reinterpret_cast<double*>(b + kTicketBytes + slots_bytes(N, C, HW, layout, sms));
   v->P = coef;
   v->Q = coef + C;
   v->A = coef + 2 * C;
@@ -1236,6 +1451,7 @@ int validate_shape(int64_t N, int64_t C, int64_t HW, int layout) {
 
 struct Plan {
   int vec;
+  bool rows;  // NHWC / 2-D with C % 4 == 0: row reduction (k_reduce_rows + k_fold_rows)
   bool team;
   bool ct;   // NCHW: cluster-team reduction (k_reduce_ct) when it fills the GPU
   bool tma;  // NCHW, HW % 4 == 0, 16-byte aligned, CGBN_PATH=tma
@@ -1277,6 +1493,7 @@ int make_plan(int64_t N, int64_t C, int64_t HW, int layout, const void* const* p
   out->vec = vec;
   out->team = g.Lv <= kTeamMaxLv;
   out->ct = layout == CGBN_LAYOUT_NCHW && !getenv("CGBN_NO_CT");
+  out->rows = rows_layout(C, HW, layout) && (align % 16) == 0;
   out->g = g;
   out->elems = N * C * HW;
   out->tma = layout == CGBN_LAYOUT_NCHW && HW % 4 == 0 && (align % 16) == 0 &&
@@ -1518,6 +1735,20 @@ int launch_tma_reduce(const Plan& pl, const TOp& op, double* out, const WsView& 
   return CGBN_OK;
 }
 
+// Row reduction (NHWC / 2-D): k_reduce_rows -> k_fold_rows (finisher of `op`).
+template <class NOp, class Op>
+int launch_rows(const Plan& pl, const NOp& nop, const Op& op, double* out, const WsView& w,
+                cudaStream_t st) {
+  const int64_t N = 1, HW = pl.g.count;  // rows = N*HW of the original geometry
+  const NGeom ng = rows_geom(N, pl.g.C, HW, resident_ctas(k_reduce_rows<NOp>));
+  const unsigned grid = ng.nslices * ng.nb;
+  launch_pdl(k_reduce_rows<NOp>, grid, true, st, ng, nop, w.slots);
+  Geom g = pl.g;
+  const unsigned fgrid = (unsigned)ceil_div((int64_t)pl.g.C * 32, kThreads);
+  launch_pdl(k_fold_rows<Op>, fgrid, true, st, g, op, (const double2*)w.slots, ng.nb, out);
+  return CGBN_OK;
+}
+
 // Forward statistics in mode kPartial / kRawSums / kLocalFinal.
 template <int VEC>
 int run_stats(const Plan& pl, const float* x, bool shift, int mode, double* out, double* out2,
@@ -1538,6 +1769,14 @@ int run_stats(const Plan& pl, const float* x, bool shift, int mode, double* out,
   op.mode = mode;
   op.out2 = out2;
   if (F) op.F = *F;
+  if constexpr (VEC == 1) {
+    if (pl.rows) {
+      StatsRows nop;
+      nop.base = op;
+      nop.gg = pl.g;
+      return launch_rows(pl, nop, op, out, w, st);
+    }
+  }
   return launch_reduce(pl, op, out, w, st);
 }
 
@@ -1564,6 +1803,14 @@ int run_bwd_reduce(const Plan& pl, const float* dy, const float* x, const double
   op.mean = op.P = op.Q = 0.0;
   op.mode = mode;
   if (F) op.F = *F;
+  if constexpr (VEC == 1) {
+    if (pl.rows) {
+      BwdRows<RELU> nop;
+      nop.base = op;
+      nop.gg = pl.g;
+      return launch_rows(pl, nop, op, out, w, st);
+    }
+  }
   return launch_reduce(pl, op, out, w, st);
 }
 
@@ -1624,7 +1871,7 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, const void* const* ptr
   // high-n planes of every channel last, so they are the likeliest L2 hits (measured
   // +1.5% on the ResNet-50 step, up to 7% on the 100 MB layers; CGBN_EW_FORWARD=1 off).
   g.rev = getenv("CGBN_EW_FORWARD") ? 0u : 1u;
-  if (layout == CGBN_LAYOUT_NHWC || HW == 1) out->cm = 2;
+  if (layout == CGBN_LAYOUT_NHWC || HW == 1) out->cm = (C % 4 == 0) ? 3 : 2;
   else out->cm = (HW % 4 == 0) ? 0 : 1;
   return CGBN_OK;
 }
@@ -1649,14 +1896,18 @@ void launch_ew_affine_t(const EwPlan& ep, const float* x, float* y, const double
 
 void launch_ew_affine(const EwPlan& ep, bool relu, const float* x, float* y, const double* P,
                       const double* Q, cudaStream_t st, bool pdl = true) {
+  int cm = ep.cm;
+  if (cm == 3 && (((uintptr_t)P | (uintptr_t)Q) % 16) != 0) cm = 2;  // caller's tables
   if (relu) {
-    if (ep.cm == 0) launch_ew_affine_t<true, 0>(ep, x, y, P, Q, pdl, st);
-    else if (ep.cm == 1) launch_ew_affine_t<true, 1>(ep, x, y, P, Q, pdl, st);
-    else launch_ew_affine_t<true, 2>(ep, x, y, P, Q, pdl, st);
+    if (cm == 0) launch_ew_affine_t<true, 0>(ep, x, y, P, Q, pdl, st);
+    else if (cm == 1) launch_ew_affine_t<true, 1>(ep, x, y, P, Q, pdl, st);
+    else if (cm == 2) launch_ew_affine_t<true, 2>(ep, x, y, P, Q, pdl, st);
+    else launch_ew_affine_t<true, 3>(ep, x, y, P, Q, pdl, st);
   } else {
-    if (ep.cm == 0) launch_ew_affine_t<false, 0>(ep, x, y, P, Q, pdl, st);
-    else if (ep.cm == 1) launch_ew_affine_t<false, 1>(ep, x, y, P, Q, pdl, st);
-    else launch_ew_affine_t<false, 2>(ep, x, y, P, Q, pdl, st);
+    if (cm == 0) launch_ew_affine_t<false, 0>(ep, x, y, P, Q, pdl, st);
+    else if (cm == 1) launch_ew_affine_t<false, 1>(ep, x, y, P, Q, pdl, st);
+    else if (cm == 2) launch_ew_affine_t<false, 2>(ep, x, y, P, Q, pdl, st);
+    else launch_ew_affine_t<false, 3>(ep, x, y, P, Q, pdl, st);
   }
 }
 
@@ -1673,11 +1924,13 @@ void launch_ew_dx(const EwPlan& ep, bool relu, const float* dy, const float* x, 
   if (relu) {
     if (ep.cm == 0) launch_ew_dx_t<true, 0>(ep, dy, x, dx, w, st);
     else if (ep.cm == 1) launch_ew_dx_t<true, 1>(ep, dy, x, dx, w, st);
-    else launch_ew_dx_t<true, 2>(ep, dy, x, dx, w, st);
+    else if (ep.cm == 2) launch_ew_dx_t<true, 2>(ep, dy, x, dx, w, st);
+    else launch_ew_dx_t<true, 3>(ep, dy, x, dx, w, st);
   } else {
     if (ep.cm == 0) launch_ew_dx_t<false, 0>(ep, dy, x, dx, w, st);
     else if (ep.cm == 1) launch_ew_dx_t<false, 1>(ep, dy, x, dx, w, st);
-    else launch_ew_dx_t<false, 2>(ep, dy, x, dx, w, st);
+    else if (ep.cm == 2) launch_ew_dx_t<false, 2>(ep, dy, x, dx, w, st);
+    else launch_ew_dx_t<false, 3>(ep, dy, x, dx, w, st);
   }
 }
 
@@ -1814,7 +2067,7 @@ int cgbn_num_sms(void) { return num_sms_cached(); }
 
 size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout) {
   if (validate_shape(N, C, HW, layout)) return 0;
-  return ws_bytes_for(N, C, HW, num_sms_cached());
+  return ws_bytes_for(N, C, HW, layout, num_sms_cached());
 }
 
 int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
@@ -1824,7 +2077,7 @@ int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CGBN_TRY(dispatch_stats(pl, x, true, kPartial, partial, nullptr, nullptr, w, st));
   return check_launch("cgbn_fwd_stats");
@@ -1837,7 +2090,7 @@ int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layou
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   pl.tma = false;
   CGBN_TRY(dispatch_stats(pl, x, false, kRawSums, sum, sum_sq, nullptr, w, st));
@@ -1852,7 +2105,7 @@ int cgbn_centered_sumsq(const float* x, int64_t N, int64_t C, int64_t HW, int la
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 1, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   pl.tma = false;
   CGBN_TRY(dispatch_stats(pl, x, false, kSumSq, out, nullptr, nullptr, w, st, sum, count));
@@ -1871,7 +2124,7 @@ int cgbn_fwd_normalize_sums(const float* x, int64_t N, int64_t C, int64_t HW, in
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
@@ -1892,7 +2145,7 @@ int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int lay
   Parts parts;
   CGBN_TRY(fill_parts(&parts, partials, G));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
@@ -1913,7 +2166,7 @@ int cgbn_fwd_train_local(const float* x, int64_t N, int64_t C, int64_t HW, int l
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, eptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
@@ -1934,7 +2187,7 @@ int cgbn_fwd_eval(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_coef_eval<<<chan_blocks(C), 256, 0, st>>>(gamma, beta, running_mean, running_var, eps, w.P,
                                               w.Q, (uint32_t)C);
@@ -1949,7 +2202,7 @@ int cgbn_xhat(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, ptrs, 2, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_coef_xhat<<<chan_blocks(C), 256, 0, st>>>(saved, w.P, w.Q, (uint32_t)C);
   launch_ew_affine(ep, false, x, xhat, w.P, w.Q, st);
@@ -1976,7 +2229,7 @@ int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64
   Plan pl;
   CGBN_TRY(make_plan(N, C, HW, layout, ptrs, 2, &pl));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, partial,
                                nullptr, w, st));
@@ -1996,7 +2249,7 @@ int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t H
   Parts parts;
   CGBN_TRY(fill_parts(&parts, partials, G));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const BwdFinal F =
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
@@ -2019,7 +2272,7 @@ int cgbn_bwd_local(const float* dy, const float* x, int64_t N, int64_t C, int64_
   EwPlan ep;
   CGBN_TRY(make_ew(N, C, HW, layout, eptrs, 3, &ep));
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const BwdFinal F =
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
@@ -2045,7 +2298,7 @@ int cgbn_fwd_fused(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
   if (!fused_plan(N, C, HW, layout, (uintptr_t)x | (uintptr_t)y, 1, &fg))
     return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_fwd_fused: shape/layout not eligible");
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
   F.P = F.Q = nullptr;  // the fused kernel keeps its coefficients in shared memory
@@ -2069,7 +2322,7 @@ int cgbn_bwd_fused(const float* dy, const float* x, int64_t N, int64_t C, int64_
   if (!fused_plan(N, C, HW, layout, (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, 2, &fg))
     return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_bwd_fused: shape/layout not eligible");
   WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, &w));
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   BwdFinal F = make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
   F.A = F.B = F.Cc = F.P = F.Q = nullptr;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

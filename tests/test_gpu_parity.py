@@ -140,6 +140,43 @@ def test_oracle_parity_shapes(shape, world, loc):
             assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_BWD, (key, r)
 
 
+@pytest.mark.parametrize("shapes,relu,loc", [
+    ([(2, 64, 56, 56)] * 4, False, 0.0),            # config 1 in channels_last
+    ([(3, 256, 14, 14), (1, 256, 14, 14)], True, 0.0),  # unequal shards + ReLU
+    ([(2, 2048, 7, 7)] * 2, False, 3.0),            # two channel slices, shifted mean
+    ([(2, 100, 9, 9)] * 2, True, 0.0),              # C % 4 == 0, odd plane
+    ([(2, 30, 5, 5)] * 2, False, 0.0),              # C % 4 != 0: generic path
+    ([(4, 64, 56, 56)], False, 1000.0),             # single rank, adversarial mean
+])
+def test_channels_last_row_kernels(shapes, relu, loc):
+    """NHWC activations: the row reductions (k_reduce_rows + k_fold_rows) and the
+    channels_last elementwise mode against the oracle."""
+    world = len(shapes)
+    xs, dys, gamma, beta, g, ref = _oracle_case(shapes, seed=sum(shapes[0]) + world, loc=loc,
+                                                relu=relu)
+    outs = run_group(world, g, xs, dys, gamma, beta, relu=relu, channels_last=True)
+    for r in range(world):
+        for key in ("y", "mu", "var", "running_mean", "running_var"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_FWD, (key, r)
+        for key in ("dx", "dgamma", "dbeta"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_BWD, (key, r)
+    for r in range(1, world):
+        assert np.array_equal(outs[r]["mu"], outs[0]["mu"])
+        assert np.array_equal(outs[r]["dgamma"], outs[0]["dgamma"])
+
+
+@pytest.mark.parametrize("n,c", [(64, 256), (7, 1024), (33, 12), (5, 3)])
+def test_two_d_rows(n, c):
+    """(N, C) activations (the reference's 2-D layout) through the row kernels."""
+    xs, dys, gamma, beta, g, ref = _oracle_case([(n, c)] * 2, seed=n + c)
+    outs = run_group(2, g, xs, dys, gamma, beta)
+    for r in range(2):
+        for key in ("y", "mu", "var"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_FWD, (key, r)
+        for key in ("dx", "dgamma", "dbeta"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_BWD, (key, r)
+
+
 def test_relu_fused_parity_config1():
     xs, dys, gamma, beta, g, ref = _oracle_case([(2, 64, 56, 56)] * 4, seed=7, relu=True)
     outs = run_group(4, g, xs, dys, gamma, beta, relu=True)
