@@ -13,8 +13,12 @@
  *    memory on the device current to the calling thread. `stream` is a cudaStream_t
  *    passed as void* (NULL = legacy default stream). Every call is asynchronous
  *    (stream-ordered) and performs no allocation and no host synchronisation.
- *  - Activations are fp32, contiguous. `layout` is CGBN_LAYOUT_NCHW (x[N][C][HW]; a 2-D
- *    (N, C) tensor is NCHW with HW == 1) or CGBN_LAYOUT_NHWC (x[N][HW][C]).
+ *  - Activations are contiguous fp32 (the reference's f32 path), bf16 or fp16; statistics,
+ *    coefficients and every reduction are fp64, outputs are rounded once to the
+ *    activation type. `layout` is CGBN_LAYOUT_NCHW (x[N][C][HW]; a 2-D (N, C) tensor is
+ *    NCHW with HW == 1) or CGBN_LAYOUT_NHWC (x[N][HW][C]), OR'd with the activation
+ *    dtype CGBN_ACT_F32 (0, default) / CGBN_ACT_BF16 / CGBN_ACT_F16. gamma, beta and the
+ *    running statistics stay fp32 for every activation dtype.
  *  - Statistics travel between kernels and ranks as fp64 "partials":
  *      forward  partial (2C+1 doubles): [mean_r (C) | M2_r (C) | count_r (1)]
  *      backward partial (2C   doubles): [sum dy (C) | sum dy*(x-mean) (C)]
@@ -42,10 +46,16 @@
 extern "C" {
 #endif
 
-#define CGBN_ABI_VERSION 3
+#define CGBN_ABI_VERSION 4
 
 #define CGBN_LAYOUT_NCHW 0
 #define CGBN_LAYOUT_NHWC 1
+
+/* Activation dtype, OR'd into `layout` (bf16 / fp16 activations with
+ * fp32 parameters and fp64 statistics). */
+#define CGBN_ACT_F32 0x00
+#define CGBN_ACT_BF16 0x10
+#define CGBN_ACT_F16 0x20
 
 #define CGBN_MAX_GROUP 64
 
@@ -83,7 +93,7 @@ size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout);
  * sequential_sum_rows pair, tensor.py:121-140) as called from _train_forward
  * (batchnorm.py:118) — one read of x, deterministic fixed-order cross-CTA fold.
  * Writes `partial` (2C+1 doubles). */
-int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_fwd_stats(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                    double* partial, void* ws, size_t ws_bytes, void* stream);
 
 /* Forward, step 2 (G ranks): fold the G gathered partials (ascending rank order),
@@ -100,33 +110,33 @@ int cgbn_fwd_stats(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
  *             the backward reads it (it replaces BNForwardCache.mu/var/total_count —
  *             x_hat is recomputed from x instead of being stored, batchnorm.py:142).
  *  running_mean/var may be NULL (no update). momentum in [0, 1]. */
-int cgbn_fwd_normalize(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_fwd_normalize(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                        const double* const* partials, int G,
                        const float* gamma, const float* beta, double eps, double momentum,
                        float* running_mean, float* running_var, double* saved, int relu,
-                       float* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+                       void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
 
 /* Single-rank training forward (G == 1: bn_forward_local, batchnorm.py:147-157, or a BN
  * group of one): the statistics kernel's last CTA per channel finalises the channel
  * directly (no partial, no exchange), then the elementwise pass. Two launches. Same
  * outputs and contract as cgbn_fwd_stats + cgbn_fwd_normalize with G == 1. */
-int cgbn_fwd_train_local(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_fwd_train_local(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                          const float* gamma, const float* beta, double eps, double momentum,
                          float* running_mean, float* running_var, double* saved, int relu,
-                         float* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+                         void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
 
 /* Eval-mode forward: y = gamma * (x - running_mean) / sqrt(running_var + eps) + beta.
  * Replaces bn_forward_local(mode="eval") (batchnorm.py:158-166); no collective and the
  * running statistics are left untouched. */
-int cgbn_fwd_eval(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_fwd_eval(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                   const float* gamma, const float* beta, const float* running_mean,
-                  const float* running_var, double eps, int relu, float* y, void* ws,
+                  const float* running_var, double eps, int relu, void* y, void* ws,
                   size_t ws_bytes, void* stream);
 
 /* Backward, step 1: this rank's partial [sum g, sum g*(x-mean)] with g = dy (times the
  * ReLU mask recomputed from x when relu != 0). Replaces the two sequential_sum_rows
  * calls of _backward_core (batchnorm.py:198-201). Writes `partial` (2C doubles). */
-int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW,
+int cgbn_bwd_reduce(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
                     int layout, const double* saved, const float* gamma, const float* beta,
                     int relu, double* partial, void* ws, size_t ws_bytes, void* stream);
 
@@ -136,24 +146,24 @@ int cgbn_bwd_reduce(const float* dy, const float* x, int64_t N, int64_t C, int64
  * x_hat*dgamma/m) (batchnorm.py:204-209). As in the reference, `eps` is the backward
  * state's eps while x_hat keeps the forward's normalisation. dgamma/dbeta (C floats
  * each) may be NULL. Two launches (finalize, memory-order elementwise). */
-int cgbn_bwd_dx(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_bwd_dx(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                 const double* const* partials, int G, const double* saved,
-                const float* gamma, const float* beta, double eps, int relu, float* dx,
+                const float* gamma, const float* beta, double eps, int relu, void* dx,
                 float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
                 void* stream);
 
 /* Single-rank backward (G == 1: bn_backward_local, batchnorm.py:213-218, or a BN group
  * of one): reduce kernel that finalises each channel, then the elementwise dx pass.
  * Same outputs as cgbn_bwd_reduce + cgbn_bwd_dx with G == 1. */
-int cgbn_bwd_local(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW,
+int cgbn_bwd_local(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
                    int layout, const double* saved, const float* gamma, const float* beta,
-                   double eps, int relu, float* dx, float* dgamma, float* dbeta,
+                   double eps, int relu, void* dx, float* dgamma, float* dbeta,
                    unsigned* status, void* ws, size_t ws_bytes, void* stream);
 
 /* x_hat = (x - mean) * inv_std from a saved forward context (the reference caches
  * x_hat in BNForwardCache, batchnorm.py:142; here it is recomputed on demand). */
-int cgbn_xhat(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
-              const double* saved, float* xhat, void* ws, size_t ws_bytes, void* stream);
+int cgbn_xhat(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+              const double* saved, void* xhat, void* ws, size_t ws_bytes, void* stream);
 
 /* Ascending-rank fold of G device vectors of n elements (dtype CGBN_DTYPE_F32/F64):
  * out = v[0] + v[1] + ... + v[G-1], evaluated left to right. This is the arithmetic of
@@ -165,7 +175,7 @@ int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void*
 /* Per-channel sums of an activation (sum and optional sum of squares, fp64 out).
  * Device counterpart of the reference's channel_sum (tensor.py:143-153). sum_sq may be
  * NULL. ws as for cgbn_fwd_stats. */
-int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_channel_sum(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                      double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream);
 
 /* Reference-literal forward statistics (bigbatch's own algorithm, selected with
@@ -178,25 +188,25 @@ int cgbn_channel_sum(const float* x, int64_t N, int64_t C, int64_t HW, int layou
  * cgbn_centered_sumsq: out[c] = sum over this rank's elements of (x - mean_c)^2 in fp64,
  * with mean_c = sum[c] / count[0] from the group-folded first exchange
  * (batchnorm.py:128-129). */
-int cgbn_centered_sumsq(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_centered_sumsq(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                         const double* sum, const double* count, double* out, void* ws,
                         size_t ws_bytes, void* stream);
 
 /* Normalise from group sums: mean = sum[c] / m, var = sq[c] / m (centered != 0) or
  * max(sq[c] / m - mean^2, 0) (centered == 0), m = count[0]; then what
  * cgbn_fwd_normalize does after its fold (batchnorm.py:121-124, 131-141). */
-int cgbn_fwd_normalize_sums(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_fwd_normalize_sums(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                             const double* sum, const double* sq, const double* count,
                             int centered, const float* gamma, const float* beta, double eps,
                             double momentum, float* running_mean, float* running_var,
-                            double* saved, int relu, float* y, unsigned* status, void* ws,
+                            double* saved, int relu, void* y, unsigned* status, void* ws,
                             size_t ws_bytes, void* stream);
 
 /* Per-channel affine map out = scale[c] * x + shift[c] (fp64 coefficients, device
  * arrays of C doubles). Device counterpart of the reference's channel_affine
  * (tensor.py:156-170). */
-int cgbn_channel_affine(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
-                        const double* scale, const double* shift, float* out, void* stream);
+int cgbn_channel_affine(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                        const double* scale, const double* shift, void* out, void* stream);
 
 /* Single-launch fused forward / backward for a single-rank group (G == 1:
  * bn_forward_local / bn_backward_local, or a BN group of one). One cooperative kernel
@@ -210,13 +220,13 @@ int cgbn_channel_affine(const float* x, int64_t N, int64_t C, int64_t HW, int la
  * entry points). cgbn_fused_supported() answers that question without launching
  * (backward != 0: the backward variant). */
 int cgbn_fused_supported(int64_t N, int64_t C, int64_t HW, int layout, int backward);
-int cgbn_fwd_fused(const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_fwd_fused(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                    const float* gamma, const float* beta, double eps, double momentum,
-                   float* running_mean, float* running_var, double* saved, int relu, float* y,
+                   float* running_mean, float* running_var, double* saved, int relu, void* y,
                    unsigned* status, void* ws, size_t ws_bytes, void* stream);
-int cgbn_bwd_fused(const float* dy, const float* x, int64_t N, int64_t C, int64_t HW, int layout,
+int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                    const double* saved, const float* gamma, const float* beta, double eps,
-                   int relu, float* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
+                   int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
                    size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus

@@ -17,6 +17,9 @@ LIB_PATH = os.environ.get("CGBN_LIB", os.path.join(_HERE, "libcgbn.so"))
 # Keep in sync with include/cgbn.h
 LAYOUT_NCHW = 0
 LAYOUT_NHWC = 1
+ACT_F32 = 0x00   # activation dtype, OR'd into the layout argument
+ACT_BF16 = 0x10
+ACT_F16 = 0x20
 MAX_GROUP = 64
 OK = 0
 ERR_INVALID = 1

@@ -502,13 +502,14 @@ def _backward_core(dy, cache: BNForwardCache, state: BNLayerState, exchange, gro
     if cache.channels != c:
         raise BatchNormError("cache does not match this layer state")
     gx = geometry(cache.x, "x", BatchNormError)
-    if gx.layout == _lib.LAYOUT_NHWC:
+    if gx.mem == _lib.LAYOUT_NHWC:
         dy = dy.contiguous(memory_format=torch.channels_last)
     else:
         dy = dy.contiguous()
     gd = geometry(dy, "dy", BatchNormError)
     if gd.layout != gx.layout:
-        raise BatchNormError("dy and x must share a memory layout")
+        raise BatchNormError(f"dy ({dy.dtype}) and x ({gx.x.dtype}) must share a memory layout "
+                             "and dtype")
     dev = gx.x.device
     lib = _lib.load()
     st = stream_ptr(dev)

@@ -31,7 +31,8 @@ class Geometry:
     N: int
     C: int
     HW: int
-    layout: int
+    layout: int  # the C ABI's format word: memory layout | activation dtype (include/cgbn.h)
+    mem: int = 0  # memory layout alone (LAYOUT_NCHW / LAYOUT_NHWC)
 
     @property
     def count(self) -> int:
@@ -53,23 +54,33 @@ def geometry(x, what: str = "x", err=TensorError) -> Geometry:
         raise err(f"tensor extents must be positive, got shape {tuple(x.shape)}")
     if not x.is_cuda:
         raise err(f"{what} must be a CUDA tensor (the CGBN path has no CPU fallback)")
-    if x.dtype != torch.float32:
-        raise err(f"{what} must be float32, got {x.dtype}")
+    act = _ACT.get(x.dtype)
+    if act is None:
+        raise err(f"{what} must be float32, bfloat16 or float16, got {x.dtype}")
+
+    def geo(t, n, c, hw, mem):
+        return Geometry(t, n, c, hw, mem | act, mem)
+
     if x.dim() == 2:
         x = x.contiguous()
-        return Geometry(x, int(x.shape[0]), int(x.shape[1]), 1, _lib.LAYOUT_NCHW)
+        return geo(x, int(x.shape[0]), int(x.shape[1]), 1, _lib.LAYOUT_NCHW)
     n, c, h, w = (int(e) for e in x.shape)
     if x.is_contiguous():
-        return Geometry(x, n, c, h * w, _lib.LAYOUT_NCHW)
+        return geo(x, n, c, h * w, _lib.LAYOUT_NCHW)
     if x.is_contiguous(memory_format=torch.channels_last):
-        return Geometry(x, n, c, h * w, _lib.LAYOUT_NHWC)
+        return geo(x, n, c, h * w, _lib.LAYOUT_NHWC)
     x = x.contiguous()
-    return Geometry(x, n, c, h * w, _lib.LAYOUT_NCHW)
+    return geo(x, n, c, h * w, _lib.LAYOUT_NCHW)
+
+
+# Activation dtypes: storage only -- statistics are fp64 and gamma,
+# beta and the running statistics stay fp32 for every activation dtype.
+_ACT = {torch.float32: _lib.ACT_F32, torch.bfloat16: _lib.ACT_BF16, torch.float16: _lib.ACT_F16}
 
 
 def same_layout_like(g: Geometry) -> torch.Tensor:
     """Uninitialised output with the input's shape and memory layout."""
-    if g.layout == _lib.LAYOUT_NHWC:
+    if g.mem == _lib.LAYOUT_NHWC:
         return torch.empty_like(g.x, memory_format=torch.channels_last)
     return torch.empty_like(g.x, memory_format=torch.contiguous_format)
 

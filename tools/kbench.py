@@ -24,7 +24,7 @@ from paper_1711_07240_b200 import _lib  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 
 
-def run_shape(shape, iters, layout, relu, graph=False):
+def run_shape(shape, iters, layout, relu, graph=False, dtype=torch.float32):
     lib = _lib.load()
     dev = torch.device("cuda", 0)
     st0 = torch.cuda.current_stream().cuda_stream
@@ -38,9 +38,9 @@ def run_shape(shape, iters, layout, relu, graph=False):
     sets = min(sets, 64)
     bufs = []
     for _ in range(sets):
-        x = torch.randn(shape, device=dev)
-        dy = torch.randn(shape, device=dev)
-        if layout == _lib.LAYOUT_NHWC:
+        x = torch.randn(shape, device=dev).to(dtype)
+        dy = torch.randn(shape, device=dev).to(dtype)
+        if (layout & 0xF) == _lib.LAYOUT_NHWC:
             x = x.contiguous(memory_format=torch.channels_last)
             dy = dy.contiguous(memory_format=torch.channels_last)
         bufs.append((x, dy, torch.empty_like(x), torch.empty_like(x)))
@@ -143,7 +143,9 @@ def run_shape(shape, iters, layout, relu, graph=False):
             e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / iters
-        out[name] = {"us": round(us, 2), "alg_gbs": round(bpe * e / (us * 1e-6) / 1e9, 1)}
+        esz = torch.finfo(dtype).bits // 8
+        out[name] = {"us": round(us, 2),
+                     "alg_gbs": round(bpe * esz / 4 * e / (us * 1e-6) / 1e9, 1)}
     return out
 
 
@@ -154,14 +156,20 @@ def main():
     ap.add_argument("--nhwc", action="store_true")
     ap.add_argument("--relu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="time inside a CUDA graph")
+    ap.add_argument("--dtype", choices=["f32", "bf16", "f16"], default="f32",
+                    help="activation dtype (bytes per element scale the GB/s)")
     args = ap.parse_args()
     shapes = [tuple(int(v) for v in s.split(",")) for s in args.shape] or [
         (32, 64, 112, 112), (32, 256, 56, 56), (32, 64, 56, 56), (32, 512, 28, 28),
         (32, 128, 28, 28), (32, 1024, 14, 14), (32, 256, 14, 14), (32, 2048, 7, 7),
         (32, 512, 7, 7), (2, 256, 200, 334), (2, 64, 400, 667), (1, 2048, 7, 7)]
     layout = _lib.LAYOUT_NHWC if args.nhwc else _lib.LAYOUT_NCHW
+    dtype, act = {"f32": (torch.float32, _lib.ACT_F32), "bf16": (torch.bfloat16, _lib.ACT_BF16),
+                  "f16": (torch.float16, _lib.ACT_F16)}[args.dtype]
     for s in shapes:
-        print(json.dumps(run_shape(s, args.iters, layout, args.relu, args.graph)), flush=True)
+        r = run_shape(s, args.iters, layout | act, args.relu, args.graph, dtype)
+        r["dtype"] = args.dtype
+        print(json.dumps(r), flush=True)
 
 
 if __name__ == "__main__":
