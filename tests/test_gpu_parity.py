@@ -367,3 +367,31 @@ def test_fused_run_to_run_bitwise_and_matches_split_closely():
         cg.set_fused(prev)
     assert O.rel_err(a["mu"], s["mu"]) <= 1e-9
     assert O.rel_err(a["y"], s["y"]) <= 1e-6
+
+
+@pytest.mark.parametrize("layout,dtype", [("nchw", torch.float32), ("nhwc", torch.float32),
+                                          ("nchw", torch.bfloat16), ("2d", torch.float32)])
+def test_nonfinite_detected_every_path(layout, dtype):
+    """NaN in x is reported as NonFiniteError through every reduction path (cluster-team,
+    rows, 16-bit), and Inf in dy through the backward (tensor.py:59-60)."""
+    dev = _dev()
+    shape = (4, 32) if layout == "2d" else (2, 8, 6, 6)
+    x = torch.randn(shape, device=dev).to(dtype)
+    if layout == "nhwc":
+        x = x.contiguous(memory_format=torch.channels_last)
+    x[(1, 2) if layout == "2d" else (1, 2, 3, 4)] = float("nan")
+    c = shape[1]
+    st = cg.BNLayerState(gamma=np.ones(c), beta=np.zeros(c))
+    with pytest.raises(cg.NonFiniteError):
+        cg.bn_forward_local(x, st)
+    x2 = torch.randn(shape, device=dev).to(dtype)
+    if layout == "nhwc":
+        x2 = x2.contiguous(memory_format=torch.channels_last)
+    st = cg.BNLayerState(gamma=np.ones(c), beta=np.zeros(c))
+    _, cache = cg.bn_forward_local(x2, st)
+    dy = torch.randn(shape, device=dev).to(dtype)
+    if layout == "nhwc":
+        dy = dy.contiguous(memory_format=torch.channels_last)
+    dy[(0, 3) if layout == "2d" else (0, 5, 1, 2)] = float("inf")
+    with pytest.raises(cg.NonFiniteError):
+        cg.bn_backward_local(dy, cache, st)
