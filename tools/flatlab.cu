@@ -312,7 +312,11 @@ __global__ void __launch_bounds__(kT, MINB) vct(G g, const float* __restrict__ x
     if (a + b == 12345.0) out[blockIdx.x] = a;
     return;
   }
-  if (c < g.C) {
+  if (TAILMODE == 5 && c < g.C) {
+    const double K = (double)__ldg(x + (size_t)c * g.HW);
+    if (tq == 0) sK[team] = K;
+    range<true>(g, x, c, j0 + tq, j1, K, a, b);  // pipelined, stride kT
+  } else if (c < g.C) {
     const double K = (double)__ldg(x + (size_t)c * g.HW);
     if (tq == 0) sK[team] = K;
     if (F32) {
@@ -526,6 +530,7 @@ int main(int argc, char** argv) {
           timeit("V8f compile-time tpc, fp32 acc", [&](const float* p) { launch_vct<4, true>(g, p, out, bestK, bestL, st, true); });
           timeit("V8t1 no reduction tail", [&](const float* p) { launch_vct<4, false, 1>(g, p, out, bestK, bestL, st, true); });
           timeit("V8t2 block reduce only", [&](const float* p) { launch_vct<4, false, 2>(g, p, out, bestK, bestL, st, true); });
+          if (bestL == 0) timeit("V8p pipelined (nch=1)", [&](const float* p) { launch_vct<4, false, 5>(g, p, out, bestK, bestL, st, true); });
           timeit("V8t3 linear addresses", [&](const float* p) { launch_vct<4, false, 3>(g, p, out, bestK, bestL, st, true); });
           timeit("V8t4 incremental addresses", [&](const float* p) { launch_vct<4, false, 4>(g, p, out, bestK, bestL, st, true); });
         }
