@@ -32,6 +32,7 @@ from .collectives import (
     DistHandle,
     SoloHandle,
     allreduce_sum,
+    world_mean_allreduce,
 )
 from .tensor import ChannelStats, NonFiniteError, TensorError, channel_affine, channel_sum
 
@@ -42,6 +43,6 @@ __all__ = [
     "bn_update_running", "check_status", "set_forward_exchange", "set_fused", "set_strict", "sync_bn_backward", "sync_bn_forward",
     "DEFAULT_TIMEOUT_S", "SCOPE_BN_GROUP", "SCOPE_WORLD", "CollectiveError",
     "CollectiveProtocolError", "CollectiveTimeoutError", "DeviceGroup", "DeviceHandle",
-    "DistHandle", "SoloHandle", "allreduce_sum", "ChannelStats", "NonFiniteError", "TensorError",
+    "DistHandle", "SoloHandle", "allreduce_sum", "world_mean_allreduce", "ChannelStats", "NonFiniteError", "TensorError",
     "channel_affine", "channel_sum",
 ]

@@ -440,12 +440,52 @@ def _all_gather_rows(vec: torch.Tensor, g: int, pg) -> torch.Tensor:
 # allreduce_sum on device vectors
 
 
+def _device_fold(rows, out) -> None:
+    """out = rows[0] + rows[1] + ... in ascending order (cgbn_fold_sum, device)."""
+    lib = _lib.load()
+    arr, keep = _lib.ptr_array([p.data_ptr() for p in rows])
+    dt = _lib.DTYPE_F64 if out.dtype == torch.float64 else _lib.DTYPE_F32
+    _lib.check(lib.cgbn_fold_sum(arr, len(rows), out.numel(), dt, out.data_ptr(),
+                                 torch.cuda.current_stream(out.device).cuda_stream),
+               "cgbn_fold_sum")
+
+
+# Vectors at least this long take the sharded path on torch.distributed handles.
+SHARDED_MIN_ELEMS = 1 << 16
+
+
+def _sharded_allreduce(v: torch.Tensor, g: int, pg, fold) -> torch.Tensor:
+    """Ascending-rank allreduce of a long vector over torch.distributed, moving 2x the
+    vector per rank instead of the all-gather's G x: an all-to-all delivers shard k of
+    every rank to rank k (a reduce-scatter), rank k folds its shard's G rows in ascending
+    rank order (`fold`, the device kernel in production), and an all-gather returns the
+    folded shards. Every element is folded once, by its shard's owner, so the result is
+    bitwise identical on every rank and equal to the full-vector fold."""
+    import torch.distributed as dist
+    n = v.numel()
+    shard = -(-n // g)
+    pad = shard * g - n
+    src = torch.cat([v, v.new_zeros(pad)]) if pad else v
+    recv = torch.empty(g * shard, dtype=v.dtype, device=v.device)
+    dist.all_to_all_single(recv, src.contiguous(), group=pg)
+    rows = list(recv.view(g, shard).unbind(0))  # row r = rank r's copy of my shard
+    mine = torch.empty(shard, dtype=v.dtype, device=v.device)
+    fold(rows, mine)
+    out = torch.empty(g * shard, dtype=v.dtype, device=v.device)
+    if v.is_cuda:
+        dist.all_gather_into_tensor(out, mine, group=pg)
+    else:
+        dist.all_gather(list(out.view(g, shard).unbind(0)), mine, group=pg)
+    return out[:n]
+
+
 def allreduce_sum(handle: _HandleBase, scope: str, v) -> torch.Tensor:
     """Elementwise sum of every rank's 1-D device vector; all ranks receive the result.
 
     Accumulation runs in ascending rank order (collectives.py:260-298), so the result is
     bitwise identical on every rank and across runs. ``v`` must be a CUDA float32 or
-    float64 tensor (no CPU fallback).
+    float64 tensor (no CPU fallback). On a torch.distributed handle, vectors of at least
+    SHARDED_MIN_ELEMS elements use the sharded reduce-scatter / fold / all-gather path.
     """
     if not isinstance(v, torch.Tensor):
         raise CollectiveProtocolError(f"rank {handle.rank}: payload must be a torch.Tensor")
@@ -457,12 +497,39 @@ def allreduce_sum(handle: _HandleBase, scope: str, v) -> torch.Tensor:
     if v.dtype not in (torch.float32, torch.float64):
         raise CollectiveProtocolError(f"rank {handle.rank}: payload dtype {v.dtype} unsupported")
     v = v.contiguous()
+    if isinstance(handle, DistHandle) and v.numel() >= SHARDED_MIN_ELEMS:
+        scope_key, ranks = handle._scope_info(scope)
+        seq = handle._next_seq(scope_key)
+        if handle.validate:
+            handle._validate(handle._groups[scope_key], ranks, scope_key, seq, "allreduce", v)
+        if len(ranks) == 1:
+            return v.clone()
+        return _sharded_allreduce(v, len(ranks), handle._groups[scope_key], _device_fold)
     parts, _ = handle.exchange(scope, "allreduce", v)
     out = torch.empty_like(v)
-    lib = _lib.load()
-    arr, keep = _lib.ptr_array([p.data_ptr() for p in parts])
-    dt = _lib.DTYPE_F64 if v.dtype == torch.float64 else _lib.DTYPE_F32
-    _lib.check(lib.cgbn_fold_sum(arr, len(parts), v.numel(), dt, out.data_ptr(),
-                                 torch.cuda.current_stream(v.device).cuda_stream),
-               "cgbn_fold_sum")
+    _device_fold(parts, out)
     return out
+
+
+def world_mean_allreduce(handle: _HandleBase, grads: dict, loss=None):
+    """The data-parallel gradient step of the reference trainer (trainer.py:419-428):
+    concatenate the gradients in sorted-key order (plus the task loss), allreduce_sum at
+    world scope (ascending-rank fold), divide by the world size and split back.
+
+    ``grads`` maps names to CUDA tensors of one float dtype. Returns (mean grads dict,
+    mean loss or None). Every rank receives bitwise-identical values."""
+    keys = sorted(grads)
+    if not keys:
+        raise ValueError("world_mean_allreduce needs at least one gradient")
+    dt = grads[keys[0]].dtype
+    dev = grads[keys[0]].device
+    flat = [grads[k].reshape(-1).to(dt) for k in keys]
+    if loss is not None:
+        flat.append(torch.as_tensor([float(loss)], dtype=dt, device=dev))
+    mean = allreduce_sum(handle, SCOPE_WORLD, torch.cat(flat)) / handle.world_size
+    out, off = {}, 0
+    for k in keys:
+        n = grads[k].numel()
+        out[k] = mean[off:off + n].view(grads[k].shape)
+        off += n
+    return out, (float(mean[-1].item()) if loss is not None else None)

@@ -99,3 +99,53 @@ def test_world4_subgroups_of_two():
     assert not np.array_equal(out[0]["parts"][0], out[2]["parts"][0])
     for d in out:
         assert d["world_sum"] == 10.0
+
+
+def _sharded_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1711_07240_b200.collectives import _sharded_allreduce
+
+        def cpu_fold(rows, out):  # ascending-rank left fold (stands in for cgbn_fold_sum)
+            acc = rows[0].clone()
+            for r in rows[1:]:
+                acc = acc + r
+            out.copy_(acc)
+
+        res = {"rank": rank}
+        for n in (1, 7, 1000, 4099):
+            v = torch.from_numpy(np.random.default_rng(100 * n + rank).standard_normal(n)
+                                 .astype(np.float32))
+            res[n] = _sharded_allreduce(v, world, None, cpu_fold).numpy()
+        q.put(res)
+        dist.destroy_process_group()
+    except Exception as exc:  # noqa: BLE001
+        q.put({"rank": rank, "error": repr(exc)})
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_allreduce_transport(world):
+    """Reduce-scatter (all-to-all) -> per-shard ascending fold -> all-gather equals the
+    full-vector ascending fold, bitwise, on every rank (uneven lengths pad)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+    for d in out:
+        assert "error" not in d, d
+    for n in (1, 7, 1000, 4099):
+        vecs = [np.random.default_rng(100 * n + r).standard_normal(n).astype(np.float32)
+                for r in range(world)]
+        want = vecs[0].copy()
+        for x in vecs[1:]:
+            want = want + x
+        for d in out:
+            assert np.array_equal(d[n], want), (n, d["rank"])

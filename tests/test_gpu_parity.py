@@ -395,3 +395,36 @@ def test_nonfinite_detected_every_path(layout, dtype):
     dy[(0, 3) if layout == "2d" else (0, 5, 1, 2)] = float("inf")
     with pytest.raises(cg.NonFiniteError):
         cg.bn_backward_local(dy, cache, st)
+
+
+def test_world_mean_allreduce_matches_trainer_step():
+    """trainer.py:419-428: sorted-key concatenation + loss, ascending fold / world, split
+    back; bitwise identical on every rank (float32 fold in rank order)."""
+    dev = _dev()
+    rng = np.random.default_rng(11)
+    world = 4
+    shapes = {"b.w": (3, 5), "a.gamma": (7,), "c.b": (2, 2, 2)}
+    grads = [{k: rng.standard_normal(s).astype(np.float32) for k, s in shapes.items()}
+             for _ in range(world)]
+    losses = [float(rng.standard_normal()) for _ in range(world)]
+
+    def worker(h):
+        g = {k: torch.from_numpy(v).to(dev) for k, v in grads[h.rank].items()}
+        mean, loss = cg.world_mean_allreduce(h, g, losses[h.rank])
+        return {k: v.cpu().numpy() for k, v in mean.items()}, loss
+
+    out = cg.DeviceGroup(world, timeout_s=60.0).run(worker)
+    keys = sorted(shapes)
+    flat = [np.concatenate([grads[r][k].ravel() for k in keys] + [np.array([losses[r]], np.float32)])
+            for r in range(world)]
+    acc = flat[0].copy()
+    for f in flat[1:]:
+        acc = acc + f
+    want = acc / np.float32(world)
+    off = 0
+    for k in keys:
+        n = int(np.prod(shapes[k]))
+        for r in range(world):
+            assert np.array_equal(out[r][0][k].ravel(), want[off:off + n]), (k, r)
+        off += n
+    assert all(out[r][1] == float(want[-1]) for r in range(world))
