@@ -605,17 +605,42 @@ def run_gpu_arm(args):
         dx_in = [torch.empty(s, device=dev) for s in shapes]
         ddy_in = [torch.empty(s, device=dev) for s in shapes]
 
+        # H2D on a copy-in stream, compute on the current stream, D2H on a copy-out stream
+        # (the two PCIe directions run on separate copy engines), ordered by events: what
+        # a caller staging host data through the public API would do.
+        s_in = torch.cuda.Stream(device=dev)
+        s_out = torch.cuda.Stream(device=dev)
+        n_l = len(shapes)
+
         def e2e_step():
+            comp = torch.cuda.current_stream(dev)
+            ev_x = [torch.cuda.Event() for _ in range(n_l)]
+            ev_dy = [torch.cuda.Event() for _ in range(n_l)]
+            s_in.wait_stream(comp)  # the previous step is done with the input buffers
+            with torch.cuda.stream(s_in):
+                for i in range(n_l):
+                    dx_in[i].copy_(hx[i], non_blocking=True)
+                    ev_x[i].record(s_in)
+                for i in range(n_l - 1, -1, -1):
+                    ddy_in[i].copy_(hdy[i], non_blocking=True)
+                    ev_dy[i].record(s_in)
             caches = []
             for i, st in enumerate(states):
-                dx_in[i].copy_(hx[i], non_blocking=True)
+                comp.wait_event(ev_x[i])
                 y, cache = cg.sync_bn_forward(handle, dx_in[i], st)
-                hy[i].copy_(y, non_blocking=True)
+                s_out.wait_stream(comp)
+                with torch.cuda.stream(s_out):
+                    hy[i].copy_(y, non_blocking=True)
+                y.record_stream(s_out)
                 caches.append(cache)
-            for i in range(len(shapes) - 1, -1, -1):
-                ddy_in[i].copy_(hdy[i], non_blocking=True)
+            for i in range(n_l - 1, -1, -1):
+                comp.wait_event(ev_dy[i])
                 dxo, dg, db = cg.sync_bn_backward(handle, ddy_in[i], caches[i], states[i])
-                hdx[i].copy_(dxo, non_blocking=True)
+                s_out.wait_stream(comp)
+                with torch.cuda.stream(s_out):
+                    hdx[i].copy_(dxo, non_blocking=True)
+                dxo.record_stream(s_out)
+            comp.wait_stream(s_out)  # the step ends when y and dx are in host memory
 
         e2e_step()
         torch.cuda.synchronize()
@@ -637,8 +662,9 @@ def run_gpu_arm(args):
         e2e = {"value": step_bytes_rank * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 8 * sum(elems), "d2h_bytes_per_step": 8 * sum(elems),
                "ms_per_step": ms_e, "steps": k_e,
-               "path": "sync_bn_forward/sync_bn_backward per layer, pinned host x/dy in, "
-                       "y/dx out, eager (no graph)"}
+               "path": "sync_bn_forward/sync_bn_backward per layer, eager (no graph); pinned "
+                       "host x/dy copied in on a copy-in stream, y/dx copied out on a "
+                       "copy-out stream, event-ordered with the compute stream"}
 
     # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
     cpu = None
