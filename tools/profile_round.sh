@@ -24,4 +24,11 @@ K2="python tools/kbench.py --shape 32,128,28,28 --iters 3"
 $K2 > $OUT/kb2_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_reduce" \
       -s 0 -c 4 -o $OUT/full_mid $K2 > $OUT/ncu_full_mid.log 2>&1
+# summarise the full captures on the box (the .ncu-rep files can exceed gpurun's 64 MiB
+# copy-back limit); keep only the mid-shape report
+for r in $OUT/full.ncu-rep $OUT/full_mid.ncu-rep; do
+  [ -f "$r" ] && python tools/ncu_summary.py "$r" >> $OUT/ncu_full_summary.txt 2>&1
+done
+rm -f $OUT/full.ncu-rep
+du -sh $OUT
 echo done
