@@ -3,24 +3,30 @@
 // The path is HBM-bandwidth bound (no contraction; tensor cores do not apply). Each BN
 // direction is a per-channel reduction followed by an elementwise pass:
 //
-//  * reduction kernels (statistics; backward sums) stream a channel's "stream" — its N
-//    planes of HW floats, C*HW apart in NCHW — with 128-bit loads, several independent
-//    loads in flight per thread (predicated unrolled rounds), and fp64 accumulation per
-//    element. Two work decompositions, chosen per shape:
-//      flat (channel stream > kTeamMaxLv units): persistent grid of resident CTAs; the
-//        channel-major stream is split into equal contiguous CTA slices; a channel
-//        covered by CTAs b0..b1 publishes one partial per CTA in workspace slot (b + c)
-//        and the last CTA to arrive (arrival ticket) folds the slots in index order;
-//      team (small planes): a power-of-two team of 32..256 threads owns a channel.
-//    The CTA that completes a channel also *finishes* it: for a single-rank group
+//  * reduction kernels (statistics; backward sums) stream a channel's "stream" -- its N
+//    planes of HW elements, C*HW apart in NCHW -- with 16-byte loads (4 fp32 or 8
+//    bf16 / fp16 values; masked covers for odd planes), several independent loads in
+//    flight per thread, an incremental address cursor, and fp64 accumulation per element.
+//    Work decompositions, chosen per shape:
+//      cluster-team (k_reduce_ct, NCHW default): a thread-block cluster of KC CTAs owns
+//        whole channels; in each CTA a team of 2^TL threads streams its rank's share of
+//        one channel, warp partials meet in shared memory and the KC CTA partials are
+//        folded over DSMEM in rank order (tools/flatlab.cu measured the decomposition);
+//      rows (k_reduce_rows + k_fold_rows, NHWC and (N, C)): threads own 4 adjacent
+//        channels and walk rows with contiguous loads; row-block partials are folded
+//        one warp per channel;
+//      flat / team: fallbacks (channel counts too small for clusters to fill the GPU;
+//        NHWC with C % 4 != 0).
+//    The thread that completes a channel also *finishes* it: for a single-rank group
 //    (G == 1) it computes mean/var/inv_std (resp. dgamma/dbeta), updates the running
 //    statistics and writes the channel's affine coefficients into a table in the
 //    workspace; for G > 1 it writes the rank partial that the group exchanges, and a
 //    small finalize kernel folds the G partials (ascending rank order) into the same
 //    table after the exchange.
 //  * elementwise kernels (normalise, dx) are a memory-order grid-stride sweep over the
-//    whole tensor in float4 units (fully coalesced for every layout — NCHW with any HW,
-//    NHWC, (N, C)), looking up each element's channel coefficients in the table.
+//    whole tensor in 16-byte units (coalesced for every layout), run from the end of the
+//    tensor for L2 reuse, looking up each element's channel coefficients in the table.
+//  * every kernel uses programmatic dependent launch (pdl_wait / pdl_trigger).
 //
 // Every reduction folds in a fixed order, so results are bitwise run-to-run
 // reproducible without float atomics, and all ranks of a group compute identical
@@ -2249,7 +2255,8 @@ int cgbn_abi_version(void) { return CGBN_ABI_VERSION; }
 #define CGBN_STR(x) CGBN_STR2(x)
 const char* cgbn_build_info(void) {
   return "cgbn sm_100a; nvcc " CGBN_STR(__CUDACC_VER_MAJOR__) "." CGBN_STR(__CUDACC_VER_MINOR__)
-         "; reduce flat/team + memory-order elementwise; fused cooperative (opt-in)";
+         "; cluster-team / row reductions (fp64) + memory-order elementwise, PDL; fp32 / bf16 / "
+         "fp16 activations; fused cooperative and TMA variants opt-in";
 }
 
 const char* cgbn_last_error(void) { return g_last_error.c_str(); }
