@@ -428,3 +428,20 @@ def test_world_mean_allreduce_matches_trainer_step():
             assert np.array_equal(out[r][0][k].ravel(), want[off:off + n]), (k, r)
         off += n
     assert all(out[r][1] == float(want[-1]) for r in range(world))
+
+
+@pytest.mark.parametrize("shape,cl", [
+    ((1, 65535, 2, 2), False),   # C at the ABI limit: cluster-team clusters loop over groups
+    ((2, 8192, 3, 3), False),    # masked-free scalar units, looping clusters
+    ((2, 65532, 1, 1), True),    # channels_last rows kernel: 64 channel slices
+    ((3, 65535), False),         # 2-D with C % 4 != 0 (team fallback)
+])
+def test_max_channels(shape, cl):
+    """The widest layers (C up to 65535, include/cgbn.h) through every decomposition."""
+    xs, dys, gamma, beta, g, ref = _oracle_case([shape] * 2, seed=5)
+    outs = run_group(2, g, xs, dys, gamma, beta, channels_last=cl and len(shape) == 4)
+    for r in range(2):
+        for key in ("y", "mu", "var", "running_var"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_FWD, (key, r)
+        for key in ("dx", "dgamma", "dbeta"):
+            assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_BWD, (key, r)
