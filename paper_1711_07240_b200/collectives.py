@@ -217,16 +217,28 @@ class DeviceHandle(_HandleBase):
         out = []
         if vec.is_cuda:
             cur = torch.cuda.current_stream(vec.device)
+            cross = False
             for r in ranks:
                 p = got[r]
                 if r != self.rank:
                     cur.wait_event(p.event)
                 t = p.tensor
                 if t.device != vec.device:
-                    t = t.to(vec.device, non_blocking=True)
+                    t = t.to(vec.device, non_blocking=True)  # peer copy (NVLink P2P)
+                    cross = True
                 elif r != self.rank:
                     t.record_stream(cur)
                 out.append(t)
+            if cross:
+                # A peer's tensor lives on its own device, where record_stream cannot
+                # reach our stream: finish the copies, then meet every rank once more so
+                # no producer releases (and its allocator reuses) a partial that a
+                # consumer has not copied yet. Every rank of a group that spans devices
+                # has a peer on another device, so all of them take this branch.
+                cur.synchronize()
+                ack = _Post(self.rank, "ack", (0, "ack"), None, None, None)
+                self.group._boards[scope_key].exchange(scope_key, -(seq + 1), ack,
+                                                       self.group.timeout_s)
         else:
             out = [got[r].tensor for r in ranks]
         return out, [got[r].info for r in ranks]
