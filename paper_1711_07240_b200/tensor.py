@@ -10,6 +10,8 @@ word instead of an O(E) host scan (see batchnorm.py).
 
 from __future__ import annotations
 
+import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import torch
@@ -91,31 +93,48 @@ def stream_ptr(device) -> int:
 
 # Workspaces (zero-initialised; the kernels return their tickets to zero) and device
 # status words, one per (device, stream).
-_ws_cache: dict = {}
-_status_cache: dict = {}
+_CACHE_MAX = 64  # streams remembered per cache (DeviceGroup.run makes fresh streams)
+_cache_lock = threading.Lock()
+_ws_cache: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+_status_cache: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+
+
+def _cached(cache, key, make, ok=lambda b: True):
+    """LRU lookup. Evicting a buffer is stream-safe: its block returns to the caching
+    allocator's pool of the stream it was allocated on, after the work queued there."""
+    with _cache_lock:
+        buf = cache.get(key)
+        if buf is not None and ok(buf):
+            cache.move_to_end(key)
+            return buf
+    new = make(buf)
+    with _cache_lock:
+        cache[key] = new
+        cache.move_to_end(key)
+        while len(cache) > _CACHE_MAX:
+            cache.popitem(last=False)
+    return new
 
 
 def workspace(device, nbytes: int) -> torch.Tensor:
+    """Zero-initialised workspace of at least ``nbytes`` for the current stream (the
+    kernels return their tickets to zero, so it is reused as is)."""
     st = torch.cuda.current_stream(device)
-    key = (st.device_index, st.cuda_stream)
-    buf = _ws_cache.get(key)
-    if buf is None or buf.numel() < nbytes:
+
+    def make(old):
         size = max(nbytes, 1 << 16)
-        if buf is not None:
-            size = max(size, 2 * buf.numel())
-        buf = torch.zeros(size, dtype=torch.uint8, device=device)
-        _ws_cache[key] = buf
-    return buf
+        if old is not None:
+            size = max(size, 2 * old.numel())
+        return torch.zeros(size, dtype=torch.uint8, device=device)
+
+    return _cached(_ws_cache, (st.device_index, st.cuda_stream), make,
+                   lambda b: b.numel() >= nbytes)
 
 
 def status_word(device) -> torch.Tensor:
     st = torch.cuda.current_stream(device)
-    key = (st.device_index, st.cuda_stream)
-    buf = _status_cache.get(key)
-    if buf is None:
-        buf = torch.zeros(1, dtype=torch.int32, device=device)
-        _status_cache[key] = buf
-    return buf
+    return _cached(_status_cache, (st.device_index, st.cuda_stream),
+                   lambda old: torch.zeros(1, dtype=torch.int32, device=device))
 
 
 @dataclass
