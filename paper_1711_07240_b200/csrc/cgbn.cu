@@ -1775,6 +1775,15 @@ again:
     latency_bound = false;  // no single-round configuration: rank by fill instead
     goto again;
   }
+  if (const char* f = getenv("CGBN_CT_FORCE")) {  // "tl,kc" (experiments only)
+    int tl = 0, kc = 0;
+    if (sscanf(f, "%d,%d", &tl, &kc) == 2 && tl >= 5 && tl <= 8 && kc >= 1 && kc <= 8) {
+      cfg->tl = tl;
+      cfg->kc = (uint32_t)kc;
+      cfg->grid = (uint32_t)(ceil_div(C, (int64_t)kThreads >> tl) * kc);
+      best_n = cfg->grid;
+    }
+  }
   if (getenv("CGBN_DEBUG_PLAN"))
     fprintf(stderr, "[cgbn] ct C=%lld Lv=%lld in=%d slots=%lld %s -> tl=%d kc=%u grid=%lld\n",
             (long long)C, (long long)Lv, Op::kIn, (long long)slots,
@@ -2056,11 +2065,18 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* c
   return CGBN_OK;
 }
 
+// One round of kEwU units per thread, not a persistent grid: a copy-like kernel streams
+// faster with many short-lived CTAs than with one resident wave that loops (ResNet-50
+// step +3%, 100 MB layers 4-6 us faster; CGBN_EW_PERSISTENT=1 restores the resident
+// grid for A/B).
 template <class K>
 unsigned ew_grid(K kernel, const EwPlan& ep) {
-  int64_t grid = resident_ctas(kernel);
-  const int64_t want = ceil_div((int64_t)ep.g.n4 + 1, kThreads * kEwU);
-  if (want < grid) grid = want;
+  int64_t grid = ceil_div((int64_t)ep.g.n4 + 1, kThreads * kEwU);
+  static const bool persistent = getenv("CGBN_EW_PERSISTENT") != nullptr;
+  if (persistent) {
+    const int64_t res = resident_ctas(kernel);
+    if (grid > res) grid = res;
+  }
   return (unsigned)(grid < 1 ? 1 : grid);
 }
 
