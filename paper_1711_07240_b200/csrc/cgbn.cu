@@ -1249,7 +1249,10 @@ __device__ __forceinline__ void ew_coef(const double* __restrict__ T, const uint
   }
 }
 
-constexpr int kEwU = 4;
+#ifndef CGBN_EWU
+#define CGBN_EWU 2
+#endif
+constexpr int kEwU = CGBN_EWU;  // 16-byte units per elementwise thread (one round): 2 measured best of 1/2/4/8 (ResNet-50 79.3% -> 82.0% of HBM vs 4)
 
 template <class T>
 constexpr int ew_ue() { return 16 / (int)sizeof(T); }
