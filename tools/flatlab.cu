@@ -401,6 +401,75 @@ void launch_vct(const G& g, const float* x, double* out, uint32_t KC, uint32_t n
   }
 }
 
+// V9: non-persistent flat reduction. CTA b reduces the units [b*CU, (b+1)*CU) of the
+// channel-major stream in one round (incremental addresses), per channel segment:
+// slot (b + c) + arrival ticket; the last CTA of a channel folds its slots (lane-parallel
+// loads, fixed order) and finishes it.
+template <int UPT>
+__global__ void __launch_bounds__(kT) v9(G g, const float* __restrict__ x, double* out,
+                                           double2* ws, unsigned* tickets) {
+  constexpr uint32_t CU = kT * UPT;
+  __shared__ double sa[kW], sb[kW];
+  __shared__ int s_last;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const uint64_t ub = (uint64_t)blockIdx.x * CU, ue = min(g.T, ub + CU);
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (uint64_t u = ub; u < ue;) {
+    const uint32_t c = (uint32_t)(u / g.Lv);
+    const uint64_t cb = (uint64_t)c * g.Lv;
+    const uint64_t se = min(ue, cb + g.Lv);
+    const double K = (double)__ldg(x + (size_t)c * g.HW);
+    double a = 0, b = 0;
+    const uint32_t j0 = (uint32_t)(u - cb), j1 = (uint32_t)(se - cb);
+    float4 v[UPT];
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+      const uint32_t j = j0 + threadIdx.x + k * kT;
+      if (j < j1) v[k] = __ldg(x4 + voff(g, c, j));
+    }
+#pragma unroll
+    for (int k = 0; k < UPT; ++k)
+      if (j0 + threadIdx.x + k * kT < j1) acc4(v[k], K, a, b);
+    a = wsum(a);
+    b = wsum(b);
+    if (l == 0) { sa[w] = a; sb[w] = b; }
+    __syncthreads();
+    const uint32_t b0 = (uint32_t)(cb / CU), b1 = (uint32_t)((cb + g.Lv - 1) / CU);
+    if (threadIdx.x == 0) {
+      a = sa[0]; b = sb[0];
+      for (int i = 1; i < kW; ++i) { a += sa[i]; b += sb[i]; }
+      int last = 1;
+      if (b0 != b1) {
+        ws[(size_t)blockIdx.x + c] = make_double2(a, b);
+        __threadfence();
+        last = atomicAdd(&tickets[c], 1u) == b1 - b0;
+      } else {
+        out[c] = K + a / g.count;
+        out[g.C + c] = fmax(b - a * (a / g.count), 0.0);
+        last = 0;
+      }
+      s_last = last;
+    }
+    __syncthreads();
+    if (s_last && w == 0) {
+      __threadfence();
+      double x1 = 0, x2 = 0;
+      for (uint32_t i = b0 + l; i <= b1; i += 32) {
+        const double2 t = __ldcg(&ws[(size_t)i + c]);
+        x1 += t.x; x2 += t.y;
+      }
+      x1 = wsum(x1); x2 = wsum(x2);
+      if (l == 0) {
+        out[c] = K + x1 / g.count;
+        out[g.C + c] = fmax(x2 - x1 * (x1 / g.count), 0.0);
+        tickets[c] = 0;
+      }
+    }
+    __syncthreads();
+    u = se;
+  }
+}
+
 int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -414,7 +483,7 @@ int main(int argc, char** argv) {
   double *out, *wsd;
   unsigned* tk;
   cudaMalloc(&out, 1 << 20);
-  cudaMalloc(&wsd, 1 << 22);
+  cudaMalloc(&wsd, 1 << 26);
   cudaMalloc(&tk, 1 << 18);
   cudaMemset(tk, 0, 1 << 18);
   cudaStream_t st;
@@ -532,6 +601,14 @@ int main(int argc, char** argv) {
           timeit("V8t2 block reduce only", [&](const float* p) { launch_vct<4, false, 2>(g, p, out, bestK, bestL, st, true); });
           if (bestL == 0) timeit("V8p pipelined (nch=1)", [&](const float* p) { launch_vct<4, false, 5>(g, p, out, bestK, bestL, st, true); });
           timeit("V8t3 linear addresses", [&](const float* p) { launch_vct<4, false, 3>(g, p, out, bestK, bestL, st, true); });
+          {
+            const uint32_t g4 = (uint32_t)((g.T + kT * 4 - 1) / (kT * 4));
+            timeit("V9 nonpersistent flat UPT4", [&](const float* p) { v9<4><<<g4, kT, 0, st>>>(g, p, out, (double2*)wsd, tk); });
+            const uint32_t g8 = (uint32_t)((g.T + kT * 8 - 1) / (kT * 8));
+            timeit("V9 nonpersistent flat UPT8", [&](const float* p) { v9<8><<<g8, kT, 0, st>>>(g, p, out, (double2*)wsd, tk); });
+            const uint32_t g2 = (uint32_t)((g.T + kT * 2 - 1) / (kT * 2));
+            timeit("V9 nonpersistent flat UPT2", [&](const float* p) { v9<2><<<g2, kT, 0, st>>>(g, p, out, (double2*)wsd, tk); });
+          }
           timeit("V8t4 incremental addresses", [&](const float* p) { launch_vct<4, false, 4>(g, p, out, bestK, bestL, st, true); });
         }
         timeit("V7 cluster16 mb4", [&](const float* p) { vclu<16, 4><<<Q * 16, kT, 0, st>>>(g, p, out, Q); });
