@@ -311,8 +311,17 @@ __device__ __forceinline__ void stv(T* __restrict__ p, const double (&t)[V]) {
 
 // Loads in flight per thread per round: ~128 B for one input stream, ~128 B total for
 // two (NIN = number of input streams).
+#ifndef CGBN_RED_U1
+#define CGBN_RED_U1 8  // loads in flight per thread per round, one input stream
+#endif
+#ifndef CGBN_RED_U2
+#define CGBN_RED_U2 4  // units per round with two input streams (dy, x)
+#endif
+#ifndef CGBN_CT_MINB
+#define CGBN_CT_MINB 4  // k_reduce_ct CTAs per SM (register bound)
+#endif
 template <int VM, int NIN = 1>
-constexpr int unroll_for() { return (NIN == 1 || VM == 1) ? 8 : 4; }
+constexpr int unroll_for() { return (NIN == 1 || VM == 1) ? CGBN_RED_U1 : CGBN_RED_U2; }
 
 // Visit units j = start, start+stride, ... < end of channel c in rounds of U: the U
 // (predicated) loads of a round are issued before any of them is used.
@@ -906,7 +915,7 @@ __device__ __forceinline__ double2 ld_dsmem(const double2* p, uint32_t rank) {
 }
 
 template <class Op, int TL>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, CGBN_CT_MINB)
 k_reduce_ct(Geom g, Op op, double* __restrict__ out) {
   pdl_wait();  // inputs may come from the previous kernel (PDL launch)
   pdl_trigger();
