@@ -531,7 +531,9 @@ def run_gpu_arm(args):
         ms_total = float(tt.item())
     ms_step = ms_total / args.steps
     value = step_bytes_rank * world / (ms_step * 1e-3) / 1e9
-    launches_per_step = 4 * len(shapes)
+    # our kernels per layer: G == 1 reduce + elementwise per direction; G > 1 adds the
+    # finalize kernel that folds the exchanged partials (NCCL kernels not counted)
+    launches_per_step = (4 if world == 1 else 6) * len(shapes)
 
     # ---- per-kernel times: one CUDA graph per kernel family replays that kernel's 53
     # launches of the step (same layer buffers, step order) through the C ABI; CUDA
