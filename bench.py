@@ -430,7 +430,7 @@ def run_gpu_arm(args):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        handle = cg.DistHandle(bn_group_size=world)
+        handle = cg.DistHandle(bn_group_size=world, transport=args.transport)
     else:
         handle = cg.SoloHandle(dev)
     cg.set_strict(False)
@@ -568,31 +568,46 @@ def run_gpu_arm(args):
                     "alg_bytes_per_elem": kern[dom]["bytes_per_elem"],
                     "peak_source": peak_src, "timing": timing_mode}
 
-    # ---- statistics exchange latency (N>1): NCCL all-gather of the fwd partial
+    # ---- statistics exchange latency (N>1): NCCL all-gather vs the one-shot P2P
+    # exchange, eager per call, max over ranks
     exch = None
     if world > 1:
-        exch = {}
-        for c in (256, 2048):
+        def time_exchange(h, c, reps=200):
             v = torch.zeros(2 * c + 1, dtype=torch.float64, device=dev)
             for _ in range(5):
-                handle.exchange(cg.SCOPE_BN_GROUP, "probe", v)
+                h.exchange(cg.SCOPE_BN_GROUP, "probe", v)
             torch.cuda.synchronize()
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            reps = 200
             e0.record()
             for _ in range(reps):
-                handle.exchange(cg.SCOPE_BN_GROUP, "probe", v)
+                h.exchange(cg.SCOPE_BN_GROUP, "probe", v)
             e1.record()
             torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) * 1e3 / reps
-            tt = torch.tensor([us], device=dev, dtype=torch.float64)
+            tt = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], device=dev,
+                              dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            exch[f"C{c}_us"] = float(tt.item())
-        exch["transport"] = "NCCL all_gather_into_tensor (eager, per call)"
-        exch["per_step_exchanges"] = 2 * len(shapes)
-        exch["est_share_of_step"] = (exch["C256_us"] * 2 * len(shapes) * 1e-3) / ms_step
+            return float(tt.item())
+
+        exch = {"step_transport": args.transport, "per_step_exchanges": 2 * len(shapes)}
+        hn = cg.DistHandle(bn_group_size=world, transport="nccl")
+        exch["nccl"] = {f"C{c}_us": time_exchange(hn, c) for c in (256, 2048)}
+        exch["nccl"]["how"] = "all_gather_into_tensor of the fp64 partial (2C+1), eager"
+        try:
+            hp = handle if args.transport == "p2p" else cg.DistHandle(
+                bn_group_size=world, transport="p2p", p2p_timeout_s=2.0)
+            exch["p2p"] = {f"C{c}_us": time_exchange(hp, c) for c in (256, 2048)}
+            exch["p2p"]["how"] = ("one single-CTA kernel per rank: NVLink pushes into CUDA-IPC "
+                                  "regions, release/acquire epoch flags, eager")
+            cg.check_status(dev)
+            if hp is not handle:
+                hp.close()
+        except Exception as exc:  # noqa: BLE001 - reported, not fatal
+            exch["p2p"] = {"error": repr(exc)[:300]}
+        used = exch.get(args.transport, {})
+        if "C256_us" in used:
+            exch["est_share_of_step"] = used["C256_us"] * 2 * len(shapes) * 1e-3 / ms_step
 
     # ---- e2e: public API with host (pinned) buffers, H2D/D2H inside the timed region
     e2e = None
@@ -725,6 +740,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="BN-group statistics exchange at N>1 (NCCL all-gather or one-shot P2P)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet50_bn_b32",
                     help="SURVEY 8(d) configuration (default: config 2, the driver's)")
     ap.add_argument("--no-graph", action="store_true")

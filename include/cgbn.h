@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CGBN_ABI_VERSION 4
+#define CGBN_ABI_VERSION 5
 
 #define CGBN_LAYOUT_NCHW 0
 #define CGBN_LAYOUT_NHWC 1
@@ -66,6 +66,7 @@ extern "C" {
 
 #define CGBN_STATUS_NONFINITE 1u  /* NaN/Inf reached the statistics (tensor.py:59-60) */
 #define CGBN_STATUS_SMALL_COUNT 2u /* total count < 2 (batchnorm.py:133-137) */
+#define CGBN_STATUS_EXCHANGE_TIMEOUT 4u /* a P2P exchange peer did not arrive in time */
 
 #define CGBN_DTYPE_F32 0
 #define CGBN_DTYPE_F64 1
@@ -164,6 +165,32 @@ int cgbn_bwd_local(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
  * x_hat in BNForwardCache, batchnorm.py:142; here it is recomputed on demand). */
 int cgbn_xhat(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
               const double* saved, void* xhat, void* ws, size_t ws_bytes, void* stream);
+
+/* One-shot P2P exchange of the statistics partial over NVLink / NVSwitch (
+ * the alternative to the NCCL all-gather; replaces the star gather of
+ * collectives.py:224-252). Each rank of a BN group allocates one region of
+ * cgbn_p2p_region_bytes(G, max_len) bytes (cgbn_p2p_alloc, zeroed; returns the
+ * 64-byte CUDA IPC handle), shares the handles, and opens its peers' regions
+ * (cgbn_p2p_open). cgbn_p2p_exchange is one single-CTA kernel: it pushes `vec` (n <=
+ * max_len doubles) into every region, publishes an epoch flag (release, system scope),
+ * waits for every peer's flag (acquire; after timeout_s it sets
+ * CGBN_STATUS_EXCHANGE_TIMEOUT and continues instead of hanging) and writes the G rows
+ * in rank order to out[G * n]. Every rank of the group must issue the same sequence of
+ * exchanges. regions[q] is rank q's region as mapped in this process.
+ *
+ * cgbn_p2p_emulate runs the same per-rank routine as a cooperative launch of G CTAs on
+ * one GPU (CTA b = rank b, regions all local): the protocol check used by the tests.
+ * skip >= 0 makes that rank sit the exchange out. */
+size_t cgbn_p2p_region_bytes(int G, int64_t max_len);
+int cgbn_p2p_alloc(size_t bytes, void** region, void* ipc_handle);
+int cgbn_p2p_open(const void* ipc_handle, void** region);
+int cgbn_p2p_close(void* region);
+int cgbn_p2p_free(void* region);
+int cgbn_p2p_exchange(const double* vec, int64_t n, int rank, int G, void* const* regions,
+                      int64_t max_len, double* out, unsigned* status, double timeout_s,
+                      void* stream);
+int cgbn_p2p_emulate(const double* vecs, int64_t n, int G, void* const* regions, int64_t max_len,
+                     double* outs, unsigned* status, double timeout_s, int skip, void* stream);
 
 /* Ascending-rank fold of G device vectors of n elements (dtype CGBN_DTYPE_F32/F64):
  * out = v[0] + v[1] + ... + v[G-1], evaluated left to right. This is the arithmetic of

@@ -27,6 +27,7 @@ ERR_CUDA = 2
 ERR_UNSUPPORTED = 3
 STATUS_NONFINITE = 1
 STATUS_SMALL_COUNT = 2
+STATUS_EXCHANGE_TIMEOUT = 4
 DTYPE_F32 = 0
 DTYPE_F64 = 1
 
@@ -59,6 +60,13 @@ SIGNATURES = {
     "cgbn_fold_sum": (_i, [_pp, _i, _i64, _i, _p, _p]),
     "cgbn_channel_sum": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
     "cgbn_centered_sumsq": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p, _sz, _p]),
+    "cgbn_p2p_region_bytes": (_sz, [_i, _i64]),
+    "cgbn_p2p_alloc": (_i, [_sz, _pp, _p]),
+    "cgbn_p2p_open": (_i, [_p, _pp]),
+    "cgbn_p2p_close": (_i, [_p]),
+    "cgbn_p2p_free": (_i, [_p]),
+    "cgbn_p2p_exchange": (_i, [_p, _i64, _i, _i, _pp, _i64, _p, _p, _d, _p]),
+    "cgbn_p2p_emulate": (_i, [_p, _i64, _i, _pp, _i64, _p, _p, _d, _i, _p]),
     "cgbn_fwd_normalize_sums": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _i, _p, _p, _d, _d,
                                      _p, _p, _p, _i, _p, _p, _p, _sz, _p]),
     "cgbn_channel_affine": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p]),

@@ -41,7 +41,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .collectives import SCOPE_BN_GROUP
+from .collectives import SCOPE_BN_GROUP, CollectiveTimeoutError
 from .tensor import NonFiniteError, geometry, same_layout_like, status_word, stream_ptr, workspace
 
 
@@ -243,6 +243,9 @@ def _raise_status(what: str, status: torch.Tensor, count=None):
     if v == 0:
         return
     status.zero_()
+    if v & _lib.STATUS_EXCHANGE_TIMEOUT:
+        raise CollectiveTimeoutError(
+            f"{what}: a peer did not join the P2P statistics exchange in time")
     if v & _lib.STATUS_NONFINITE:
         raise NonFiniteError(f"{what}: non-finite values in tensor data")
     if v & _lib.STATUS_SMALL_COUNT:

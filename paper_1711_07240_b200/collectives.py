@@ -29,6 +29,7 @@ Two transports:
 
 from __future__ import annotations
 
+import ctypes
 import threading
 import time
 from dataclasses import dataclass, field
@@ -366,12 +367,74 @@ class SoloHandle(_HandleBase):
 # torch.distributed transport (one process per GPU)
 
 
+class _P2PGroup:
+    """One-shot NVLink / NVSwitch exchange for one BN group of a torch.distributed job
+    (include/cgbn.h cgbn_p2p_*): each rank's region is shared with the group by CUDA
+    IPC, and an exchange is one single-CTA kernel per rank -- push, publish an epoch
+    flag, wait for the peers' flags, copy the G rows out in rank order. The consumer
+    kernels fold the rows exactly as on the NCCL path, so results are bitwise equal."""
+
+    def __init__(self, ranks, my_rank, pg, device, max_len: int, timeout_s: float):
+        import torch.distributed as dist
+        lib = _lib.load()
+        self.G = len(ranks)
+        self.idx = ranks.index(my_rank)
+        self.max_len = int(max_len)
+        self.timeout_s = float(timeout_s)
+        self.device = device
+        nbytes = lib.cgbn_p2p_region_bytes(self.G, self.max_len)
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        with torch.cuda.device(device):
+            _lib.check(lib.cgbn_p2p_alloc(nbytes, ctypes.byref(own), handle), "cgbn_p2p_alloc")
+        handles = [None] * self.G
+        dist.all_gather_object(handles, bytes(handle), group=pg)
+        self._own = own.value
+        self._opened = []
+        ptrs = []
+        with torch.cuda.device(device):
+            for q, h in enumerate(handles):
+                if q == self.idx:
+                    ptrs.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                _lib.check(lib.cgbn_p2p_open(hb, ctypes.byref(p)), "cgbn_p2p_open")
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+        self._regions, self._keep = _lib.ptr_array(ptrs)
+
+    def exchange(self, vec: torch.Tensor) -> list:
+        from .tensor import status_word
+        lib = _lib.load()
+        n = vec.numel()
+        out = torch.empty(self.G * n, dtype=torch.float64, device=vec.device)
+        status = status_word(vec.device)
+        _lib.check(lib.cgbn_p2p_exchange(
+            vec.data_ptr(), n, self.idx, self.G, self._regions, self.max_len, out.data_ptr(),
+            status.data_ptr(), self.timeout_s, torch.cuda.current_stream(vec.device).cuda_stream),
+            "cgbn_p2p_exchange")
+        return [out[q * n:(q + 1) * n] for q in range(self.G)]
+
+    def close(self):
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            torch.cuda.synchronize(self.device)
+            for p in self._opened:
+                lib.cgbn_p2p_close(p)
+            if self._own:
+                lib.cgbn_p2p_free(self._own)
+        self._opened, self._own = [], None
+
+
 class DistHandle(_HandleBase):
     """This process's rank in a torch.distributed job, with BN sub-groups of
     ``bn_group_size`` contiguous ranks. The exchange is an all-gather of the packed
     partial on the scope's communicator (NCCL on GPUs, gloo on CPU)."""
 
-    def __init__(self, bn_group_size: int | None = None, validate: bool = False):
+    def __init__(self, bn_group_size: int | None = None, validate: bool = False,
+                 transport: str = "nccl", p2p_max_len: int = 2 * 65535 + 1,
+                 p2p_timeout_s: float = 10.0, device=None):
         import torch.distributed as dist
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised before DistHandle")
@@ -392,8 +455,25 @@ class DistHandle(_HandleBase):
                 pg = dist.new_group(list(range(i * g, (i + 1) * g)))
                 self._groups[f"bn{i}"] = pg
         backend = dist.get_backend()
-        self._device = (torch.device("cuda", torch.cuda.current_device())
-                        if backend == "nccl" else torch.device("cpu"))
+        if device is not None:
+            self._device = torch.device(device)
+        else:
+            self._device = (torch.device("cuda", torch.cuda.current_device())
+                            if backend == "nccl" else torch.device("cpu"))
+        # statistics transport of the BN group: "nccl" (all-gather on the group's
+        # communicator) or "p2p" (one-shot NVLink exchange over CUDA-IPC regions,
+        # include/cgbn.h cgbn_p2p_*); world-scope collectives always use NCCL
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        self.transport = transport
+        self._p2p = None
+        if transport == "p2p" and g > 1:
+            if self._device.type != "cuda":
+                raise ValueError("the p2p transport needs a CUDA device")
+            gi = self.rank // g
+            self._p2p = _P2PGroup(list(range(gi * g, (gi + 1) * g)), self.rank,
+                                  self._groups[f"bn{gi}"], self._device, p2p_max_len,
+                                  p2p_timeout_s)
 
     def __repr__(self):
         return f"DistHandle(rank={self.rank}, world={self.world_size}, g={self.bn_group_size})"
@@ -412,8 +492,17 @@ class DistHandle(_HandleBase):
             self._validate(pg, ranks, scope_key, seq, kind, vec)
         if g == 1:
             return [vec], None
+        if (self._p2p is not None and scope == SCOPE_BN_GROUP and vec.is_cuda
+                and vec.dtype == torch.float64 and vec.numel() <= self._p2p.max_len):
+            return self._p2p.exchange(vec.contiguous()), None
         out = _all_gather_rows(vec, g, pg)
         return [out[i] for i in range(g)], None
+
+    def close(self):
+        """Release the P2P regions (collective-free; call on every rank)."""
+        if self._p2p is not None:
+            self._p2p.close()
+            self._p2p = None
 
     def _validate(self, pg, ranks, scope_key, seq, kind, vec):
         """Optional host-side protocol check (one extra tiny all-gather): every rank

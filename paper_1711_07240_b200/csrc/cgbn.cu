@@ -1396,6 +1396,7 @@ __global__ void k_fold_sum(Parts P, int64_t n, T* __restrict__ out) {
 
 #include "cgbn_tma.cuh"
 #include "cgbn_fused.cuh"
+#include "cgbn_p2p.cuh"
 
 namespace {
 
@@ -2596,6 +2597,101 @@ int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
                 : launch_cooperative(fused::k_fused_bwd<false>, fg.grid, fused::kSmemBytes, st,
                                      fg, dyf, xf, dxf, F, w.slots, w.bar));
   return check_launch("cgbn_bwd_fused");
+}
+
+size_t cgbn_p2p_region_bytes(int G, int64_t max_len) {
+  if (G < 1 || G > CGBN_MAX_GROUP || max_len < 1) return 0;
+  return p2p::region_bytes(G, max_len);
+}
+
+int cgbn_p2p_alloc(size_t bytes, void** region, void* ipc_handle) {
+  CGBN_REQUIRE(region && ipc_handle && bytes > 0, "cgbn_p2p_alloc: bad argument");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cgbn_p2p_alloc: cudaMalloc: %s", cudaGetErrorString(e));
+  e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess)
+    e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(ipc_handle), p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return set_error(CGBN_ERR_CUDA, "cgbn_p2p_alloc: %s", cudaGetErrorString(e));
+  }
+  *region = p;
+  return CGBN_OK;
+}
+
+int cgbn_p2p_open(const void* ipc_handle, void** region) {
+  CGBN_REQUIRE(region && ipc_handle, "cgbn_p2p_open: NULL pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(region, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cgbn_p2p_open: %s", cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
+int cgbn_p2p_close(void* region) {
+  const cudaError_t e = cudaIpcCloseMemHandle(region);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cgbn_p2p_close: %s", cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
+int cgbn_p2p_free(void* region) {
+  const cudaError_t e = cudaFree(region);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cgbn_p2p_free: %s", cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
+namespace {
+int fill_peers(p2p::Peers* P, void* const* regions, int G) {
+  if (G < 1 || G > p2p::kMaxPeers)
+    return set_error(CGBN_ERR_INVALID, "group size %d outside [1, %d]", G, p2p::kMaxPeers);
+  if (!regions) return set_error(CGBN_ERR_INVALID, "regions array is NULL");
+  for (int q = 0; q < G; ++q) {
+    if (!regions[q]) return set_error(CGBN_ERR_INVALID, "regions[%d] is NULL", q);
+    P->base[q] = static_cast<char*>(regions[q]);
+  }
+  for (int q = G; q < p2p::kMaxPeers; ++q) P->base[q] = nullptr;
+  return CGBN_OK;
+}
+}  // namespace
+
+int cgbn_p2p_exchange(const double* vec, int64_t n, int rank, int G, void* const* regions,
+                      int64_t max_len, double* out, unsigned* status, double timeout_s,
+                      void* stream) {
+  CGBN_REQUIRE(vec && out, "cgbn_p2p_exchange: NULL pointer");
+  CGBN_REQUIRE(n >= 1 && n <= max_len, "cgbn_p2p_exchange: n=%lld outside [1, %lld]",
+               (long long)n, (long long)max_len);
+  CGBN_REQUIRE(rank >= 0 && rank < G, "cgbn_p2p_exchange: rank %d outside [0, %d)", rank, G);
+  CGBN_REQUIRE(timeout_s > 0.0, "cgbn_p2p_exchange: timeout must be positive");
+  p2p::Peers peers;
+  CGBN_TRY(fill_peers(&peers, regions, G));
+  launch_pdl(p2p::k_p2p_exchange, 1u, true, reinterpret_cast<cudaStream_t>(stream), vec, n, rank,
+             G, peers, max_len, out, status, (uint64_t)(timeout_s * 1e9));
+  return check_launch("cgbn_p2p_exchange");
+}
+
+int cgbn_p2p_emulate(const double* vecs, int64_t n, int G, void* const* regions, int64_t max_len,
+                     double* outs, unsigned* status, double timeout_s, int skip, void* stream) {
+  CGBN_REQUIRE(vecs && outs, "cgbn_p2p_emulate: NULL pointer");
+  CGBN_REQUIRE(n >= 1 && n <= max_len, "cgbn_p2p_emulate: n outside [1, max_len]");
+  CGBN_REQUIRE(timeout_s > 0.0, "cgbn_p2p_emulate: timeout must be positive");
+  p2p::Peers peers;
+  CGBN_TRY(fill_peers(&peers, regions, G));
+  // cooperative launch: the G rank-CTAs are guaranteed co-resident while they wait on
+  // each other (the single-GPU stand-in for G processes)
+  const uint64_t tns = (uint64_t)(timeout_s * 1e9);
+  void* args[] = {(void*)&vecs, (void*)&n,      (void*)&G,      (void*)&peers, (void*)&max_len,
+                  (void*)&outs, (void*)&status, (void*)&tns,    (void*)&skip};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)p2p::k_p2p_emulate, dim3(G),
+                                                    dim3(p2p::kThreadsP2P), args, 0,
+                                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cgbn_p2p_emulate: %s", cudaGetErrorString(e));
+  return check_launch("cgbn_p2p_emulate");
 }
 
 int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void* out,
