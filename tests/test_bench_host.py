@@ -1,0 +1,37 @@
+"""bench.py host-side definitions (CPU): the SURVEY 8(d) workloads, the ResNet-50 BN
+layer list, the reference-arm process sizing and the oracle fallback step."""
+
+import bench
+
+
+def test_resnet50_has_53_bn_layers_at_224():
+    s = bench.resnet50_bn_shapes(32)
+    assert len(s) == 53
+    assert s[0] == (32, 64, 112, 112)
+    assert s[-1] == (32, 2048, 7, 7)
+    assert sum(bench.numel(x) for x in s) == 355_647_488
+
+
+def test_detector_workloads_use_ceil_strides():
+    fpn = bench.fpn_neck_shapes(2)
+    assert fpn == [(2, 256, 200, 334), (2, 256, 100, 167), (2, 256, 50, 84),
+                   (2, 256, 25, 42), (2, 256, 13, 21)]
+    meg = bench.WORKLOADS["megdet_r50fpn_800x1333"][1]()
+    assert len(meg) == 58 and meg[0] == (2, 64, 400, 667)
+    assert bench.WORKLOADS["latency_2048x7x7"][1]() == [(1, 2048, 7, 7)]
+
+
+def test_reference_procs_capped_by_cores():
+    n = bench.reference_procs(bench.resnet50_bn_shapes(32), 1)
+    assert 1 <= n <= (len(__import__("os").sched_getaffinity(0)))
+    assert bench.reference_procs(bench.resnet50_bn_shapes(32), 1, requested=1) == 1
+
+
+def test_port_step_counts_algorithmic_bytes():
+    dt, nb = bench.port_step((2, 8, 4, 4), 2, 0)
+    assert nb == 32 * 2 * 8 * 16 * 2 and dt > 0
+
+
+def test_host_cpu_info_keys():
+    info = bench.host_cpu_info()
+    assert {"cpu_model", "host_cpus", "affinity_cpus"} <= set(info)

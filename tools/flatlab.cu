@@ -490,7 +490,7 @@ int main(int argc, char** argv) {
   cudaStreamCreate(&st);
   cudaFuncSetAttribute(vclu<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int mult = argc > 1 ? atoi(argv[1]) : 3;
-  const bool check = argc > 2 && strcmp(argv[2], "sweep") != 0;
+  const bool check = argc > 2 && strcmp(argv[2], "sweep") != 0 && strcmp(argv[2], "grid") != 0;
   const bool sweep = argc > 2 && strcmp(argv[2], "sweep") == 0;
   const char* only = argc > 3 ? argv[3] : nullptr;
   for (auto s : shapes) {
@@ -532,6 +532,16 @@ int main(int argc, char** argv) {
       cudaGraphExecDestroy(ge);
       cudaGraphDestroy(gr);
     };
+    if (argc > 2 && strcmp(argv[2], "grid") == 0) {
+      for (int gcount : {sms * 4, 512, sms * 3, 384, sms * 8}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "V0 memory order grid=%d", gcount);
+        timeit(nm, [&](const float* p) {
+          v0<<<gcount, kT, 0, st>>>(reinterpret_cast<const float4*>(p), E / 4, out);
+        });
+      }
+      continue;
+    }
     if (sweep) {
       timeit("V0 memory order", [&](const float* p) {
         v0<<<sms * 4, kT, 0, st>>>(reinterpret_cast<const float4*>(p), E / 4, out);
