@@ -13,15 +13,18 @@ Same names, arguments, return tuples and exceptions as the reference:
 
 Differences (by design):
 
-* Tensors are torch CUDA float32 (NCHW, channels_last, or (N, C)); statistics are
-  computed and exchanged in fp64. ``relu=True`` fuses the ReLU that follows BN in the
+* Activations are torch CUDA float32, bfloat16 or float16 (NCHW, channels_last, or
+  (N, C)); statistics are computed and exchanged in fp64, gamma / beta / running
+  statistics stay float32. ``relu=True`` fuses the ReLU that follows BN in the
   reference model (model.py:243-246) into the forward and its mask into the backward.
-* One statistics exchange per pass. The forward exchanges each rank's
-  (mean, centred M2, count) and folds them with Chan's pairwise update in ascending rank
-  order; this has the reference two-pass algorithm's numerics (no E[x^2]-E[x]^2
-  cancellation) at the cost of one collective, so ``one_pass`` changes neither cost nor
-  outcome here (the reference's own test_trainer.py:377-387 states "one-pass changes
-  cost, not outcome").
+* One statistics exchange per pass by default (``set_forward_exchange("merged")``). The
+  forward exchanges each rank's (mean, centred M2, count) and folds them with Chan's
+  pairwise update in ascending rank order; this has the reference two-pass algorithm's
+  numerics (no E[x^2]-E[x]^2 cancellation) at the cost of one collective, so
+  ``one_pass`` changes neither cost nor outcome here (the reference's own
+  test_trainer.py:377-387 states "one-pass changes cost, not outcome").
+  ``set_forward_exchange("reference")`` runs the reference's literal arithmetic (two
+  exchanges for ``one_pass=False``).
 * ``BNForwardCache`` keeps the input and the per-channel (mean, var, inv_std, m) on the
   device instead of a full x_hat tensor (the backward recomputes x_hat); ``x_hat``,
   ``mu``, ``var`` and ``total_count`` remain available as attributes.

@@ -2,8 +2,8 @@
 primitives (``channel_sum``, ``channel_affine``; /root/reference/pkg/src/bigbatch/tensor.py).
 
 The reference's ``Tensor`` (tensor.py:39-87) is an immutable f64/f32 numpy array that
-rejects NaN/Inf on construction. Here activations are torch CUDA fp32 tensors, NCHW
-contiguous (or channels_last = NHWC, or 2-D (N, C)); the finiteness contract is kept by
+rejects NaN/Inf on construction. Here activations are torch CUDA fp32 / bf16 / fp16
+tensors, NCHW contiguous (or channels_last = NHWC, or 2-D (N, C)); the finiteness contract is kept by
 the statistics kernels, which report non-finite statistics through a device status
 word instead of an O(E) host scan (see batchnorm.py).
 """
