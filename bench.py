@@ -413,6 +413,74 @@ def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
                  f"reduction; CUDA events on the replay stream, mean of {reps} replays")
 
 
+def select_transport(cg, torch, dist, dev, world, requested, barrier):
+    """Statistics transport for N>1: NCCL all-gather, or the one-shot P2P exchange when it
+    passes a self-test against NCCL (bitwise-equal rows, no timeout) and -- for "auto" --
+    is faster. Every rank takes the same decision (collective MIN / MAX). Returns
+    (handle, report)."""
+    hn = cg.DistHandle(bn_group_size=world, transport="nccl")
+
+    def time_exchange(h, c, reps=200):
+        v = torch.zeros(2 * c + 1, dtype=torch.float64, device=dev)
+        for _ in range(5):
+            h.exchange(cg.SCOPE_BN_GROUP, "probe", v)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            h.exchange(cg.SCOPE_BN_GROUP, "probe", v)
+        e1.record()
+        torch.cuda.synchronize()
+        tt = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    rep = {"requested": requested}
+    rep["nccl"] = {f"C{c}_us": time_exchange(hn, c) for c in (256, 2048)}
+    rep["nccl"]["how"] = "all_gather_into_tensor of the fp64 partial (2C+1), eager"
+    hp, ok = None, 0  # the self-test runs only if every rank set the P2P handle up
+    if requested in ("auto", "p2p"):
+        try:
+            hp = cg.DistHandle(bn_group_size=world, transport="p2p", p2p_timeout_s=1.0)
+            ok = 1
+        except Exception as exc:  # noqa: BLE001
+            rep["p2p_error"] = repr(exc)[:300]
+        t = torch.tensor([ok], device=dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)  # every rank set up, or nobody uses it
+        ok = int(t.item())
+    if ok:
+        try:
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(99 + dist.get_rank())
+            good = True
+            for c in (64, 2048, 64):
+                v = torch.randn(2 * c + 1, dtype=torch.float64, device=dev, generator=gen)
+                rp, _ = hp.exchange(cg.SCOPE_BN_GROUP, "selftest", v)
+                rn, _ = hn.exchange(cg.SCOPE_BN_GROUP, "selftest", v)
+                good = good and all(torch.equal(a, b) for a, b in zip(rp, rn))
+            cg.check_status(dev)  # raises on an exchange timeout
+            ok = int(good)
+        except Exception as exc:  # noqa: BLE001 - reported; NCCL stays available
+            rep["p2p_error"] = repr(exc)[:300]
+            ok = 0
+        t = torch.tensor([ok], device=dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = int(t.item())
+    if requested in ("auto", "p2p"):
+        rep["p2p_selftest"] = "passed" if ok else "failed"
+        if ok:
+            rep["p2p"] = {f"C{c}_us": time_exchange(hp, c) for c in (256, 2048)}
+            rep["p2p"]["how"] = ("one single-CTA kernel per rank: NVLink pushes into CUDA-IPC "
+                                 "regions, release/acquire epoch flags, eager")
+    use_p2p = ok and (requested == "p2p" or rep["p2p"]["C256_us"] < rep["nccl"]["C256_us"])
+    rep["step_transport"] = "p2p" if use_p2p else "nccl"
+    if hp is not None and not use_p2p:
+        hp.close()
+    return (hp if use_p2p else hn), rep
+
+
 def run_gpu_arm(args):
     import numpy as np
     import torch
@@ -430,9 +498,15 @@ def run_gpu_arm(args):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        handle = cg.DistHandle(bn_group_size=world, transport=args.transport)
+
+        def _barrier():
+            dist.barrier(device_ids=[local_rank])
+
+        handle, transport_report = select_transport(cg, torch, dist, dev, world,
+                                                    args.transport, _barrier)
     else:
         handle = cg.SoloHandle(dev)
+        transport_report = None
     cg.set_strict(False)
     cg.set_fused(args.fused)
 
@@ -568,44 +642,12 @@ def run_gpu_arm(args):
                     "alg_bytes_per_elem": kern[dom]["bytes_per_elem"],
                     "peak_source": peak_src, "timing": timing_mode}
 
-    # ---- statistics exchange latency (N>1): NCCL all-gather vs the one-shot P2P
-    # exchange, eager per call, max over ranks
+    # ---- statistics exchange latency (N>1): measured during transport selection
     exch = None
     if world > 1:
-        def time_exchange(h, c, reps=200):
-            v = torch.zeros(2 * c + 1, dtype=torch.float64, device=dev)
-            for _ in range(5):
-                h.exchange(cg.SCOPE_BN_GROUP, "probe", v)
-            torch.cuda.synchronize()
-            barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(reps):
-                h.exchange(cg.SCOPE_BN_GROUP, "probe", v)
-            e1.record()
-            torch.cuda.synchronize()
-            tt = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], device=dev,
-                              dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            return float(tt.item())
-
-        exch = {"step_transport": args.transport, "per_step_exchanges": 2 * len(shapes)}
-        hn = cg.DistHandle(bn_group_size=world, transport="nccl")
-        exch["nccl"] = {f"C{c}_us": time_exchange(hn, c) for c in (256, 2048)}
-        exch["nccl"]["how"] = "all_gather_into_tensor of the fp64 partial (2C+1), eager"
-        try:
-            hp = handle if args.transport == "p2p" else cg.DistHandle(
-                bn_group_size=world, transport="p2p", p2p_timeout_s=2.0)
-            exch["p2p"] = {f"C{c}_us": time_exchange(hp, c) for c in (256, 2048)}
-            exch["p2p"]["how"] = ("one single-CTA kernel per rank: NVLink pushes into CUDA-IPC "
-                                  "regions, release/acquire epoch flags, eager")
-            cg.check_status(dev)
-            if hp is not handle:
-                hp.close()
-        except Exception as exc:  # noqa: BLE001 - reported, not fatal
-            exch["p2p"] = {"error": repr(exc)[:300]}
-        used = exch.get(args.transport, {})
+        exch = dict(transport_report)
+        exch["per_step_exchanges"] = 2 * len(shapes)
+        used = exch.get(exch["step_transport"], {})
         if "C256_us" in used:
             exch["est_share_of_step"] = used["C256_us"] * 2 * len(shapes) * 1e-3 / ms_step
 
@@ -713,7 +755,9 @@ def run_gpu_arm(args):
                                      (f"inputs > L2: {len(shapes)} layers' x+dy = "
                                       f"{8 * sum(elems) / 1e9:.2f} GB per step >> 126 MB L2; "
                                       "intra-layer re-reads of x may hit L2")),
-                       "cuda_graph": graph is not None, "launch": graph_note},
+                       "cuda_graph": graph is not None, "launch": graph_note,
+                       "exchange_transport": (transport_report or {}).get(
+                           "step_transport", "none (one rank)")},
             "per_gpu_gbs": value / world,
             "per_gpu_hbm_frac": value / world / hbm_peak,
             "kernels": kern,
@@ -740,8 +784,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
-    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
-                    help="BN-group statistics exchange at N>1 (NCCL all-gather or one-shot P2P)")
+    ap.add_argument("--transport", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="BN-group statistics exchange at N>1: NCCL all-gather, the one-shot "
+                         "P2P exchange, or auto (P2P if it passes its self-test and is faster)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet50_bn_b32",
                     help="SURVEY 8(d) configuration (default: config 2, the driver's)")
     ap.add_argument("--no-graph", action="store_true")

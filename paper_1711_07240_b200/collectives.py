@@ -386,9 +386,15 @@ class _P2PGroup:
         own = ctypes.c_void_p()
         handle = (ctypes.c_char * 64)()
         with torch.cuda.device(device):
-            _lib.check(lib.cgbn_p2p_alloc(nbytes, ctypes.byref(own), handle), "cgbn_p2p_alloc")
+            rc = lib.cgbn_p2p_alloc(nbytes, ctypes.byref(own), handle)
+        # every rank reaches the gather, so a failure on one rank cannot strand the others
         handles = [None] * self.G
-        dist.all_gather_object(handles, bytes(handle), group=pg)
+        dist.all_gather_object(handles, bytes(handle) if rc == _lib.OK else None, group=pg)
+        if any(h is None for h in handles):
+            if rc == _lib.OK:
+                lib.cgbn_p2p_free(own.value)
+            bad = [ranks[q] for q, h in enumerate(handles) if h is None]
+            raise CollectiveError(f"P2P region allocation failed on rank(s) {bad}")
         self._own = own.value
         self._opened = []
         ptrs = []
