@@ -137,3 +137,33 @@ def test_p2p_ipc_setup_two_processes():
         assert "error" not in d, d
         assert d["G"] == 2 and d["opened"] == 1 and d["idx"] == d["rank"]
         assert all(r for r in d["regions"])
+
+
+def test_p2p_exchange_kernel_in_cuda_graph_single_rank():
+    """cgbn_p2p_exchange captured in a CUDA graph: the device-side epoch advances on every
+    replay (both halves of the double buffer) and the fixed output follows the input.
+    G = 1, so the kernel never waits on another rank."""
+    lib = _lib.load()
+    max_len, n = 64, 17
+    reg = Regions(1, max_len)
+    try:
+        vec = torch.zeros(n, dtype=torch.float64, device="cuda")
+        out = torch.zeros(n, dtype=torch.float64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                _lib.check(lib.cgbn_p2p_exchange(vec.data_ptr(), n, 0, 1, reg.arr, max_len,
+                                                 out.data_ptr(), status.data_ptr(), 1.0,
+                                                 side.cuda_stream), "exchange")
+        torch.cuda.current_stream().wait_stream(side)
+        for it in range(5):
+            vec.copy_(torch.arange(n, dtype=torch.float64, device="cuda") * (it + 1))
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out, vec), it
+        assert int(status.item()) == 0
+    finally:
+        reg.free()
