@@ -1,0 +1,283 @@
+// cgbn_common.cuh — errors, reduction geometry and the unit cursor, typed vector I/O, load rounds
+// Part of the single translation unit cgbn.cu (included there, in order).
+
+#pragma once
+
+namespace {
+
+// ----------------------------------------------------------------------------------
+// Errors
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "%s: CUDA launch failed: %s", what, cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
+// ----------------------------------------------------------------------------------
+// Geometry
+
+// Unsigned 32-bit division by a runtime-constant divisor, valid for every n < 2^32
+// (Hacker's Delight round-up method): t = umulhi(n, m), q = (t + ((n - t) >> s1)) >> s2
+// with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1, s1 = min(l, 1), s2 = l - s1.
+struct FastDiv {
+  uint32_t m, s1, s2;
+  void init(uint32_t d) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    s1 = l < 1 ? l : 1;
+    s2 = l - s1;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t = __umulhi(n, m);
+    return (t + ((n - t) >> s1)) >> s2;
+  }
+};
+
+// Reduction-kernel geometry. Element offset of vector unit j of channel c:
+// (c*HWv + j + (j / HWv) * gap) * VEC with gap = (C-1)*HWv. NCHW: HWv = HW/VEC.
+// NHWC and 2-D (N, C): HWv = 1, VEC = 1.
+// VM (vector mode) 1, 2, 4: exact vectors of VM floats (HW % VM == 0); VM 5 = "masked
+// float4": planes whose length is not a multiple of 4 (ResNet 7x7, FPN 25x42 / 13x21) are
+// read as the aligned float4 cover of each plane (ceil(HW/4) + 1 units per plane) with a
+// per-element mask, so odd planes also stream with 128-bit loads.
+struct Geom {
+  uint32_t C;
+  uint32_t Lv;        // vector units per channel stream (N*HWv)
+  uint32_t HWv;       // vector units per plane
+  uint32_t grid;      // CTAs of this launch
+  uint32_t tpc_log2;  // team kernels: log2(threads per channel)
+  uint32_t HW;        // floats per plane (1 for NHWC / 2-D)
+  uint64_t T;         // C * Lv
+  uint64_t gap;       // (C-1)*HWv
+  FastDiv dhw;        // division by HWv
+  double count;       // elements per channel on this rank (N*HW)
+};
+
+// Vector modes (elements per load unit): 1, 2, 4, 8 exact; 5 = masked 4-element cover
+// (fp32), 9 = masked 8-element cover (bf16 / fp16). A unit is at most 16 bytes.
+constexpr int vec_of(int vm) { return vm == 5 ? 4 : vm == 9 ? 8 : vm; }
+constexpr bool masked_vm(int vm) { return vm == 5 || vm == 9; }
+
+// Unit cursor: the position of one thread in a channel stream, advanced by a fixed
+// stride without a division per unit. P = (n*C + c)*HWv is the vector-unit index of the
+// start of plane (n, c), o the unit within the plane, ps = (n*C + c)*HW the plane start
+// in floats (masked mode). All fit in 32 bits (N*C*HW < 2^32). tools/flatlab.cu measured
+// the per-unit FastDiv + 64-bit multiply addressing at 1.2-2 us per launch on ResNet
+// mid shapes.
+struct Cursor {
+  uint32_t P, o, ps;
+};
+
+struct Step {
+  uint32_t q, r;  // stride = q*HWv + r
+};
+
+__device__ __forceinline__ Cursor cursor_at(const Geom& g, uint32_t c, uint32_t j) {
+  const uint32_t n = g.dhw.div(j);
+  const uint32_t nc = n * g.C + c;
+  return Cursor{nc * g.HWv, j - n * g.HWv, nc * g.HW};
+}
+
+__device__ __forceinline__ Step step_of(const Geom& g, uint32_t stride) {
+  const uint32_t q = g.dhw.div(stride);
+  return Step{q, stride - q * g.HWv};
+}
+
+__device__ __forceinline__ void advance(const Geom& g, Cursor& k, const Step& s) {
+  const uint32_t CHWv = g.C * g.HWv, CHW = g.C * g.HW;
+  k.o += s.r;
+  k.P += s.q * CHWv;
+  k.ps += s.q * CHW;
+  if (k.o >= g.HWv) {
+    k.o -= g.HWv;
+    k.P += CHWv;
+    k.ps += CHW;
+  }
+}
+
+// Address (in floats) and element mask of the unit under the cursor.
+template <int VM>
+__device__ __forceinline__ uint32_t unit_addr(const Geom& g, const Cursor& k, uint32_t& mask) {
+  constexpr uint32_t V = vec_of(VM);
+  if constexpr (!masked_vm(VM)) {
+    mask = (1u << V) - 1u;
+    return (k.P + k.o) * V;
+  } else {
+    const uint32_t base = (k.ps & ~(V - 1u)) + V * k.o;
+    const int lo = (int)(k.ps - base);            // plane start relative to the unit
+    const int hi = lo + (int)g.HW;                // plane end relative to the unit
+    mask = 0u;
+#pragma unroll
+    for (int e = 0; e < (int)V; ++e) mask |= (e >= lo && e < hi) ? (1u << e) : 0u;
+    return base;
+  }
+}
+
+// flat: CTA b owns stream units [cta_begin(b), cta_begin(b+1)).
+__device__ __forceinline__ uint64_t cta_begin(const Geom& g, uint32_t b) {
+  return (uint64_t)b * g.T / g.grid;
+}
+// The CTA whose slice contains unit u: the largest b with cta_begin(b) <= u.
+__device__ __forceinline__ uint32_t cta_of(const Geom& g, uint64_t u) {
+  return (uint32_t)(((u + 1) * (uint64_t)g.grid - 1) / g.T);
+}
+
+struct Seg {
+  uint32_t c, j0, j1;
+};
+
+template <class F>
+__device__ __forceinline__ void for_each_segment(const Geom& g, F&& f) {
+  const uint64_t u_end = cta_begin(g, blockIdx.x + 1);
+  for (uint64_t u = cta_begin(g, blockIdx.x); u < u_end;) {
+    const uint32_t c = (uint32_t)(u / g.Lv);
+    const uint64_t cbase = (uint64_t)c * g.Lv;
+    const uint64_t s_end = min(u_end, cbase + g.Lv);
+    f(Seg{c, (uint32_t)(u - cbase), (uint32_t)(s_end - cbase)});
+    u = s_end;
+  }
+}
+
+struct Parts {
+  const double* p[CGBN_MAX_GROUP];
+  int G;
+};
+
+// ----------------------------------------------------------------------------------
+// Vector load / store of activation elements (fp32, bf16 or fp16 storage; every kernel
+// computes in fp64 and rounds once on output).
+
+template <class T>
+__device__ __forceinline__ float h2f(unsigned short h);
+template <>
+__device__ __forceinline__ float h2f<__nv_bfloat16>(unsigned short h) {
+  return __bfloat162float(__ushort_as_bfloat16(h));
+}
+template <>
+__device__ __forceinline__ float h2f<__half>(unsigned short h) {
+  return __half2float(__ushort_as_half(h));
+}
+
+// one element, as float
+template <class T>
+__device__ __forceinline__ float ld1(const T* __restrict__ p) {
+  if constexpr (sizeof(T) == 4) return __ldg(reinterpret_cast<const float*>(p));
+  else return h2f<T>(__ldg(reinterpret_cast<const unsigned short*>(p)));
+}
+
+// fp64 -> storage, rounded once
+template <class T>
+__device__ __forceinline__ uint32_t rnd(double v) {
+  if constexpr (sizeof(T) == 4) return __float_as_uint((float)v);
+  else if constexpr (std::is_same<T, __nv_bfloat16>::value)
+    return __bfloat16_as_ushort(__double2bfloat16(v));
+  else return __half_as_ushort(__double2half(v));
+}
+
+template <class T>
+__device__ __forceinline__ void st1(T* p, double v) {
+  if constexpr (sizeof(T) == 4) *reinterpret_cast<float*>(p) = (float)v;
+  else *reinterpret_cast<unsigned short*>(p) = (unsigned short)rnd<T>(v);
+}
+
+// V elements of T held as raw 32-bit words (the registers of one vector load).
+template <class T, int V>
+struct Vec {
+  static constexpr int kBytes = V * (int)sizeof(T);
+  static constexpr int kWords = kBytes >= 4 ? kBytes / 4 : 1;
+  uint32_t w[kWords];
+  __device__ __forceinline__ void load(const T* __restrict__ p) {
+    if constexpr (kBytes == 16) {
+      const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+    } else if constexpr (kBytes == 8) {
+      const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+      w[0] = t.x; w[1] = t.y;
+    } else if constexpr (kBytes == 4) {
+      w[0] = __ldg(reinterpret_cast<const unsigned*>(p));
+    } else {
+      w[0] = __ldg(reinterpret_cast<const unsigned short*>(p));
+    }
+  }
+  __device__ __forceinline__ float get(int k) const {
+    if constexpr (sizeof(T) == 4) return __uint_as_float(w[k]);
+    else return h2f<T>((unsigned short)(w[k >> 1] >> (16 * (k & 1))));
+  }
+};
+
+// Round V fp64 values to T and store them as one vector.
+template <class T, int V>
+__device__ __forceinline__ void stv(T* __restrict__ p, const double (&t)[V]) {
+  if constexpr (sizeof(T) == 4) {
+    if constexpr (V == 4) {
+      *reinterpret_cast<float4*>(p) = make_float4((float)t[0], (float)t[1], (float)t[2], (float)t[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) reinterpret_cast<float*>(p)[k] = (float)t[k];
+    }
+  } else {
+    static_assert(V % 2 == 0, "16-bit stores pack pairs");
+    uint32_t w[V / 2];
+#pragma unroll
+    for (int k = 0; k < V / 2; ++k) w[k] = rnd<T>(t[2 * k]) | (rnd<T>(t[2 * k + 1]) << 16);
+    if constexpr (V == 8) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    else if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+    else *reinterpret_cast<uint32_t*>(p) = w[0];
+  }
+}
+
+// Loads in flight per thread per round: ~128 B for one input stream, ~128 B total for
+// two (NIN = number of input streams).
+#ifndef CGBN_RED_U1
+#define CGBN_RED_U1 8  // loads in flight per thread per round, one input stream
+#endif
+#ifndef CGBN_RED_U2
+#define CGBN_RED_U2 4  // units per round with two input streams (dy, x)
+#endif
+#ifndef CGBN_CT_MINB
+#define CGBN_CT_MINB 4  // k_reduce_ct CTAs per SM (register bound)
+#endif
+template <int VM, int NIN = 1>
+constexpr int unroll_for() { return (NIN == 1 || VM == 1) ? CGBN_RED_U1 : CGBN_RED_U2; }
+
+// Visit units j = start, start+stride, ... < end of channel c in rounds of U: the U
+// (predicated) loads of a round are issued before any of them is used.
+template <int U, class Op, class Body>
+__device__ __forceinline__ void strided_rounds(const Geom& g, uint32_t c, uint32_t start,
+                                               uint32_t end, uint32_t stride, const Op& op,
+                                               Body&& body) {
+  if (start >= end) return;
+  Cursor k = cursor_at(g, c, start);
+  const Step s = step_of(g, stride);
+  for (uint32_t i = start; i < end; i += U * stride) {
+    typename Op::Regs r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = i + u * stride;
+      if (j < end) op.load(g, k, r[u]);
+      advance(g, k, s);  // after U steps: the next round's first unit
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = i + u * stride;
+      if (j < end) body(u, j, r[u]);
+    }
+  }
+}
+
+}  // namespace

@@ -1,0 +1,879 @@
+// cgbn_host.cuh — host-side planning, configuration choice and launches
+// Part of the single translation unit cgbn.cu (included there, in order).
+
+#pragma once
+
+namespace {
+
+// ----------------------------------------------------------------------------------
+// Host-side planning
+
+int num_sms_cached() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Workspace: tickets + barrier words | (C + max grid) double2 per-CTA partial slots |
+// coefficient table (5 x C doubles: P, Q, A, B, Cc).
+// Row reductions (NHWC / 2-D, C % 4 == 0): rows per block >= 32 keeps the partial
+// slots (nb * C double2) under 1/8 of the activation bytes.
+bool rows_layout(int64_t C, int64_t HW, int layout) {
+  return (layout == CGBN_LAYOUT_NHWC || HW == 1) && C % 4 == 0 && !getenv("CGBN_NO_ROWS");
+}
+
+NGeom rows_geom(int64_t N, int64_t C, int64_t HW, int64_t ctas) {
+  NGeom g;
+  g.M = (uint32_t)(N * HW);
+  g.C = (uint32_t)C;
+  g.C4 = (uint32_t)(C / 4);
+  g.CS4 = g.C4 < (uint32_t)kThreads ? g.C4 : (uint32_t)kThreads;
+  g.rpp = (uint32_t)kThreads / g.CS4;
+  g.nslices = (g.C4 + g.CS4 - 1) / g.CS4;
+  int64_t nb = ceil_div(ctas, (int64_t)g.nslices);
+  const int64_t cap = (int64_t)g.M / 32;
+  if (nb > cap) nb = cap;
+  if (nb > (int64_t)g.M) nb = g.M;
+  g.nb = (uint32_t)(nb < 1 ? 1 : nb);
+  return g;
+}
+
+size_t slots_bytes(int64_t N, int64_t C, int64_t HW, int layout, int sms) {
+  size_t n = (size_t)C + (size_t)sms * kMaxCtasPerSm;
+  if (rows_layout(C, HW, layout)) {
+    const NGeom g = rows_geom(N, C, HW, (int64_t)sms * kMaxCtasPerSm);
+    const size_t r = (size_t)g.nb * (size_t)C;
+    if (r > n) n = r;
+  }
+  return n * sizeof(double2);
+}
+size_t ws_bytes_for(int64_t N, int64_t C, int64_t HW, int layout, int sms) {
+  return kTicketBytes + slots_bytes(N, C, HW, layout, sms) + 5 * (size_t)C * sizeof(double);
+}
+
+struct WsView {
+  unsigned* tickets;
+  unsigned* bar;
+  double2* slots;
+  double* P;
+  double* Q;
+  double* A;
+  double* B;
+  double* Cc;
+};
+
+int ws_view(void* ws, size_t ws_bytes, int64_t N, int64_t C, int64_t HW, int layout,
+            WsView* v) {
+  const int sms = num_sms_cached();
+  const size_t need = ws_bytes_for(N, C, HW, layout, sms);
+  if (!ws || ws_bytes < need)
+    return set_error(CGBN_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need,
+                     ws_bytes);
+  if (reinterpret_cast<uintptr_t>(ws) % 16)
+    return set_error(CGBN_ERR_INVALID, "workspace must be 16-byte aligned");
+  char* b = reinterpret_cast<char*>(ws);
+  v->tickets = reinterpret_cast<unsigned*>(b);
+  v->bar = v->tickets + kTicketWords;
+  v->slots = reinterpret_cast<double2*>(b + kTicketBytes);
+  double* coef =
+      reinterpret_cast<double*>(b + kTicketBytes + slots_bytes(N, C, HW, layout, sms));
+  v->P = coef;
+  v->Q = coef + C;
+  v->A = coef + 2 * C;
+  v->B = coef + 3 * C;
+  v->Cc = coef + 4 * C;
+  return CGBN_OK;
+}
+
+// Per-(kernel, device) caches. Keyed by the kernel's address: kernels of one signature
+// share a function-pointer type, so a per-template static would alias them.
+std::mutex g_cache_mu;
+std::map<std::pair<const void*, int>, int> g_occ_cache;
+std::map<std::pair<const void*, int>, bool> g_smem_done;
+
+template <class K>
+int64_t resident_ctas(K kernel) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_occ_cache.find(key);
+    if (it != g_occ_cache.end()) occ = it->second;
+  }
+  if (occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0) != cudaSuccess ||
+        occ <= 0)
+      occ = 1;
+    if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_occ_cache[key] = occ;
+  }
+  return (int64_t)num_sms_cached() * occ;
+}
+
+template <class K>
+void smem_optin(K kernel, size_t smem_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_smem_done.count(key)) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+  g_smem_done[key] = true;
+}
+
+// CGBN_PATH=tma selects the TMA streaming statistics reductions (A/B measurement);
+// CGBN_PATH=reg disables every TMA / cp.async variant.
+int path_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CGBN_PATH");
+    v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : 0;
+  }
+  return v;
+}
+
+// The ABI's `layout` argument carries the activation dtype in bits 4..7
+// (CGBN_ACT_F32 / CGBN_ACT_BF16 / CGBN_ACT_F16, include/cgbn.h).
+int split_fmt(int* layout, int* act) {
+  const int f = *layout;
+  *act = (f >> 4) & 0xF;
+  *layout = f & 0xF;
+  if (f & ~0xFF) return set_error(CGBN_ERR_INVALID, "unknown layout/format bits 0x%x", f);
+  if (*act > 2) return set_error(CGBN_ERR_INVALID, "unknown activation dtype %d", *act);
+  return CGBN_OK;
+}
+
+int act_bytes(int act) { return act == 0 ? 4 : 2; }
+
+int validate_shape(int64_t N, int64_t C, int64_t HW, int layout) {
+  if (N < 1 || C < 1 || HW < 1)
+    return set_error(CGBN_ERR_INVALID, "extents must be positive, got N=%lld C=%lld HW=%lld",
+                     (long long)N, (long long)C, (long long)HW);
+  if (layout != CGBN_LAYOUT_NCHW && layout != CGBN_LAYOUT_NHWC)
+    return set_error(CGBN_ERR_INVALID, "unknown layout %d", layout);
+  if (C > 65535) return set_error(CGBN_ERR_INVALID, "C=%lld exceeds 65535", (long long)C);
+  if (N * HW >= (1ll << 31))
+    return set_error(CGBN_ERR_INVALID, "per-channel count N*HW=%lld must be < 2^31",
+                     (long long)(N * HW));
+  if (N * C * HW >= (1ll << 32))
+    return set_error(CGBN_ERR_INVALID, "tensor of %lld elements exceeds 2^32",
+                     (long long)(N * C * HW));
+  return CGBN_OK;
+}
+
+struct Plan {
+  int act;  // activation dtype (0 fp32, 1 bf16, 2 fp16)
+  int vec;
+  bool rows;  // NHWC / 2-D with C % 4 == 0: row reduction (k_reduce_rows + k_fold_rows)
+  bool team;
+  bool ct;   // NCHW: cluster-team reduction (k_reduce_ct) when it fills the GPU
+  bool tma;  // NCHW, HW % 4 == 0, 16-byte aligned, CGBN_PATH=tma
+  Geom g;
+  tma::TGeom tg;
+  int64_t elems;
+};
+
+// Reduction plan. `ptrs` are every activation pointer the kernel touches; the vector
+// width is the widest one that divides the plane length and the alignment of all.
+int make_plan(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* const* ptrs,
+              int nptr, Plan* out) {
+  int rc = validate_shape(N, C, HW, layout);
+  if (rc) return rc;
+  int64_t planeN = N, planeHW = HW;
+  if (layout == CGBN_LAYOUT_NHWC) { planeN = N * HW; planeHW = 1; }
+  uintptr_t align = 0;
+  for (int k = 0; k < nptr; ++k) align |= (uintptr_t)ptrs[k];
+  const int es = act_bytes(act);
+  const int64_t vmax = 16 / es;  // elements per 16-byte unit
+  const int64_t E = N * C * HW;
+  int vec = 1;
+  if (planeHW % vmax == 0 && (align % 16) == 0) vec = (int)vmax;
+  else if (es == 2 && planeHW % 4 == 0 && (align % 8) == 0)
+    vec = 4;  // exact 8-byte units: faster than masked 16-byte covers (bf16 14x14 stats 4.4 -> 3.3 us)
+  else if (layout == CGBN_LAYOUT_NCHW && HW >= 16 && (align % 16) == 0 && E % vmax == 0 &&
+           E + 2 * vmax < (1ll << 32) && !getenv("CGBN_NO_MASKED"))
+    vec = es == 4 ? 5 : 9;  // masked 16-byte cover of odd planes (never leaves the tensor)
+  else if (es == 2 && planeHW % 4 == 0 && (align % 8) == 0) vec = 4;
+  else if (planeHW % 2 == 0 && (align % (2 * es)) == 0) vec = 2;
+  const int V = vec_of(vec);
+  Geom g;
+  g.C = (uint32_t)C;
+  g.HW = (uint32_t)planeHW;
+  g.HWv = (uint32_t)(masked_vm(vec) ? (planeHW + V - 1) / V + 1 : planeHW / vec);
+  g.Lv = (uint32_t)(planeN * g.HWv);
+  g.gap = (uint64_t)(C - 1) * g.HWv;
+  g.dhw.init(g.HWv);
+  g.count = (double)(N * HW);
+  g.T = (uint64_t)C * g.Lv;
+  g.grid = 1;
+  // team size: smallest power of two in [32, 256] giving <= ~8 units per thread
+  uint32_t tl = 5;
+  while (tl < 8 && (((uint64_t)g.Lv + (1ull << tl) - 1) >> tl) > 8) ++tl;
+  g.tpc_log2 = tl;
+  out->act = act;
+  out->vec = vec;
+  out->team = g.Lv <= kTeamMaxLv;
+  out->ct = layout == CGBN_LAYOUT_NCHW && !getenv("CGBN_NO_CT");
+  out->rows = rows_layout(C, HW, layout) && (align % 16) == 0;
+  out->g = g;
+  out->elems = N * C * HW;
+  out->tma = act == 0 && layout == CGBN_LAYOUT_NCHW && HW % 4 == 0 && (align % 16) == 0 &&
+             path_override() == 1;
+  tma::TGeom& tg = out->tg;
+  tg.C = (uint32_t)C;
+  tg.HW = (uint32_t)HW;
+  tg.L = (uint32_t)(N * HW);
+  tg.T4 = (uint64_t)C * tg.L / 4;
+  tg.dhw.init((uint32_t)HW);
+  tg.count = (double)(N * HW);
+  int64_t tgrid = ceil_div((int64_t)tg.T4, 1024);
+  if (tgrid > num_sms_cached()) tgrid = num_sms_cached();
+  tg.grid = (uint32_t)(tgrid < 1 ? 1 : tgrid);
+  return CGBN_OK;
+}
+
+int fill_parts(Parts* P, const double* const* partials, int G) {
+  if (G < 1 || G > CGBN_MAX_GROUP)
+    return set_error(CGBN_ERR_INVALID, "group size %d outside [1, %d]", G, CGBN_MAX_GROUP);
+  if (!partials) return set_error(CGBN_ERR_INVALID, "partials array is NULL");
+  for (int r = 0; r < G; ++r) {
+    if (!partials[r]) return set_error(CGBN_ERR_INVALID, "partials[%d] is NULL", r);
+    P->p[r] = partials[r];
+  }
+  for (int r = G; r < CGBN_MAX_GROUP; ++r) P->p[r] = nullptr;
+  P->G = G;
+  return CGBN_OK;
+}
+
+template <class K>
+unsigned flat_grid(K kernel, const Plan& pl) {
+  int64_t grid = resident_ctas(kernel);
+  const int64_t want = ceil_div(pl.elems, kMinElemsPerCta);
+  if (want < grid) grid = want;
+  return (unsigned)(grid < 1 ? 1 : grid);
+}
+
+template <class K>
+unsigned team_grid(K kernel, const Plan& pl) {
+  const int64_t cpt = kThreads >> pl.g.tpc_log2;
+  int64_t grid = ceil_div(pl.g.C, cpt);
+  const int64_t res = resident_ctas(kernel);
+  if (grid > res) grid = res;
+  return (unsigned)(grid < 1 ? 1 : grid);
+}
+
+// Launch with programmatic dependent launch allowed (see pdl_trigger / pdl_wait).
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("CGBN_NO_PDL") ? 0 : 1;
+  return v == 1;
+}
+
+template <class K, class... Args>
+void launch_pdl(K kernel, unsigned grid, bool pdl, cudaStream_t st, Args... args) {
+  if (!pdl || !pdl_enabled()) {
+    kernel<<<grid, kThreads, 0, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// Clusters of `kc` CTAs of `kernel` that can be co-resident (cached; 0 if unsupported).
+std::map<std::tuple<const void*, int, int>, int> g_cluster_cache;
+
+template <class K>
+int64_t cluster_capacity(K kernel, uint32_t kc) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, (int)kc);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cluster_cache.find(key);
+    if (it != g_cluster_cache.end()) return (int64_t)it->second * kc;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kc * 64);
+  cfg.blockDim = dim3(kThreads);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cluster_cache[key] = n;
+  return (int64_t)n * kc;
+}
+
+struct CtCfg {
+  int tl;
+  uint32_t kc, grid;
+};
+
+// Cluster-team configuration, from the lab sweep (tools/flatlab.cu "sweep", B200,
+// ResNet-50 shapes). Cluster sizes are powers of two; U = vector loads of each input a
+// thread keeps in flight per round.
+//  - latency-bound (the whole stream fits in one round of the resident slots): the
+//    fewest CTAs whose threads need a single round, unclustered first (a cluster costs
+//    ~1 us of barrier + DSMEM at these sizes);
+//  - bandwidth-bound: the largest grid that fits in one wave (bytes in flight), then the
+//    smaller cluster, then the larger team.
+// Returns false when nothing fills a quarter of the slots (tiny C: the flat kernel
+// spreads one channel over more CTAs than a cluster holds).
+template <class Op>
+int64_t ct_cluster_cap(int tl, uint32_t kc) {
+  switch (tl) {
+    case 8: return cluster_capacity(k_reduce_ct<Op, 8>, kc);
+    case 7: return cluster_capacity(k_reduce_ct<Op, 7>, kc);
+    case 6: return cluster_capacity(k_reduce_ct<Op, 6>, kc);
+    default: return cluster_capacity(k_reduce_ct<Op, 5>, kc);
+  }
+}
+
+template <class Op>
+bool choose_ct(const Plan& pl, CtCfg* cfg) {
+  constexpr int64_t U = unroll_for<Op::kVec, Op::kIn>();
+  const int64_t slots = resident_ctas(k_reduce_ct<Op, 8>);
+  const int64_t C = pl.g.C, Lv = pl.g.Lv;
+  bool latency_bound = C * Lv <= slots * kThreads * U;
+  int64_t best_n = 0;
+  double best = 1e30;
+again:
+  for (uint32_t kc = 1; kc <= 8; kc *= 2) {
+    for (int tl = 8; tl >= 5; --tl) {
+      const int64_t tpc = 1 << tl;
+      if (kc > 1 && Lv / kc < tpc) continue;  // every thread keeps >= 1 unit
+      const int64_t n = ceil_div(C, (int64_t)kThreads >> tl) * kc;
+      if (n > slots) continue;
+      const int64_t units = ceil_div(Lv, (int64_t)kc * tpc);
+      double score;
+      if (latency_bound) {
+        if (units > U) continue;
+        score = (kc > 1 ? 1e6 : 0.0) + (double)n;  // unclustered, then fewest CTAs
+      } else {
+        score = -(double)n * 16.0 + kc;  // most CTAs, then smallest cluster
+      }
+      if (score >= best) continue;
+      if (kc > 1 && n > ct_cluster_cap<Op>(tl, kc)) continue;
+      best = score;
+      best_n = n;
+      cfg->tl = tl;
+      cfg->kc = kc;
+      cfg->grid = (uint32_t)n;
+    }
+  }
+  if (latency_bound && best_n == 0) {
+    latency_bound = false;  // no single-round configuration: rank by fill instead
+    goto again;
+  }
+  if (const char* f = getenv("CGBN_CT_FORCE")) {  // "tl,kc" (experiments only)
+    int tl = 0, kc = 0;
+    if (sscanf(f, "%d,%d", &tl, &kc) == 2 && tl >= 5 && tl <= 8 && kc >= 1 && kc <= 8) {
+      cfg->tl = tl;
+      cfg->kc = (uint32_t)kc;
+      cfg->grid = (uint32_t)(ceil_div(C, (int64_t)kThreads >> tl) * kc);
+      best_n = cfg->grid;
+    }
+  }
+  if (getenv("CGBN_DEBUG_PLAN"))
+    fprintf(stderr, "[cgbn] ct C=%lld Lv=%lld in=%d slots=%lld %s -> tl=%d kc=%u grid=%lld\n",
+            (long long)C, (long long)Lv, Op::kIn, (long long)slots,
+            latency_bound ? "latency" : "bandwidth", best_n ? cfg->tl : -1, best_n ? cfg->kc : 0,
+            (long long)best_n);
+  if (best_n == 0 && ceil_div(C, kThreads >> 5) > slots) {
+    // very wide layers: 8 channels per CTA, CTAs loop over channel groups
+    cfg->tl = 5;
+    cfg->kc = 1;
+    cfg->grid = (uint32_t)slots;
+    return true;
+  }
+  return best_n * 4 >= slots;
+}
+
+template <class Op, int TL>
+int launch_ct(Geom g, const Op& op, double* out, uint32_t kc, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (kc > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = kc;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce_ct<Op, TL>, g, op, out);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cluster reduction launch failed: %s", cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
+template <class Op>
+int launch_reduce(const Plan& pl, const Op& op, double* out, const WsView& w, cudaStream_t st) {
+  Geom g = pl.g;
+  CtCfg cc;
+  if (pl.ct && choose_ct<Op>(pl, &cc)) {
+    g.grid = cc.grid;
+    switch (cc.tl) {
+      case 8: return launch_ct<Op, 8>(g, op, out, cc.kc, st);
+      case 7: return launch_ct<Op, 7>(g, op, out, cc.kc, st);
+      case 6: return launch_ct<Op, 6>(g, op, out, cc.kc, st);
+      default: return launch_ct<Op, 5>(g, op, out, cc.kc, st);
+    }
+  }
+  if (pl.team) {
+    g.grid = team_grid(k_reduce_team<Op>, pl);
+    launch_pdl(k_reduce_team<Op>, g.grid, true, st, g, op, out);
+  } else {
+    g.grid = flat_grid(k_reduce_flat<Op>, pl);
+    launch_pdl(k_reduce_flat<Op>, g.grid, true, st, g, op, out, w.slots, w.tickets);
+  }
+  return CGBN_OK;
+}
+
+template <class TOp>
+int launch_tma_reduce(const Plan& pl, const TOp& op, double* out, const WsView& w,
+                      cudaStream_t st) {
+  smem_optin(tma::k_tma_reduce<TOp>, tma::kSmemBytes);
+  tma::k_tma_reduce<TOp><<<pl.tg.grid, tma::kThreadsTma, tma::kSmemBytes, st>>>(
+      pl.tg, op, out, w.slots, w.tickets);
+  return CGBN_OK;
+}
+
+// Row reduction (NHWC / 2-D): k_reduce_rows -> k_fold_rows (finisher of `op`).
+template <class NOp, class Op>
+int launch_rows(const Plan& pl, const NOp& nop, const Op& op, double* out, const WsView& w,
+                cudaStream_t st) {
+  const int64_t N = 1, HW = pl.g.count;  // rows = N*HW of the original geometry
+  const NGeom ng = rows_geom(N, pl.g.C, HW, resident_ctas(k_reduce_rows<NOp>));
+  const unsigned grid = ng.nslices * ng.nb;
+  launch_pdl(k_reduce_rows<NOp>, grid, true, st, ng, nop, w.slots);
+  Geom g = pl.g;
+  const unsigned fgrid = (unsigned)ceil_div((int64_t)pl.g.C * 32, kThreads);
+  launch_pdl(k_fold_rows<Op>, fgrid, true, st, g, op, (const double2*)w.slots, ng.nb, out);
+  return CGBN_OK;
+}
+
+// Forward statistics in mode kPartial / kRawSums / kLocalFinal / kSumSq.
+template <class T, int VEC>
+int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out, double* out2,
+              const FwdFinal* F, const WsView& w, cudaStream_t st, const double* ksum,
+              const double* kcount) {
+  const T* x = static_cast<const T*>(xv);
+  if constexpr (std::is_same<T, float>::value && VEC == 4) {
+    if (pl.tma && shift && mode == kPartial) {
+      tma::TmaStats op;
+      op.x = x;
+      op.K = 0.0;
+      return launch_tma_reduce(pl, op, out, w, st);
+    }
+  }
+  StatsOp<T, VEC> op;
+  op.x = x;
+  op.K = 0.0;
+  op.shift = shift;
+  op.ksum = ksum;
+  op.kcount = kcount;
+  op.mode = mode;
+  op.out2 = out2;
+  if (F) op.F = *F;
+  if constexpr (VEC == 1) {
+    if (pl.rows) {
+      StatsRows<T> nop;
+      nop.base = op;
+      nop.gg = pl.g;
+      return launch_rows(pl, nop, op, out, w, st);
+    }
+  }
+  return launch_reduce(pl, op, out, w, st);
+}
+
+template <class T, int VEC, bool RELU>
+int run_bwd_reduce(const Plan& pl, const void* dyv, const void* xv, const double* saved,
+                   const float* gamma, const float* beta, int mode, double* out,
+                   const BwdFinal* F, const WsView& w, cudaStream_t st) {
+  const T* dy = static_cast<const T*>(dyv);
+  const T* x = static_cast<const T*>(xv);
+  if constexpr (std::is_same<T, float>::value && VEC == 4) {
+    if (pl.tma && mode == kPartial) {
+      tma::TmaBwd<RELU> op;
+      op.dy = dy;
+      op.x = x;
+      op.saved = saved;
+      op.gamma = gamma;
+      op.beta = beta;
+      op.mean = op.P = op.Q = 0.0;
+      return launch_tma_reduce(pl, op, out, w, st);
+    }
+  }
+  BwdOp<T, VEC, RELU> op;
+  op.dy = dy;
+  op.x = x;
+  op.saved = saved;
+  op.gamma = gamma;
+  op.beta = beta;
+  op.mean = op.P = op.Q = 0.0;
+  op.mode = mode;
+  if (F) op.F = *F;
+  if constexpr (VEC == 1) {
+    if (pl.rows) {
+      BwdRows<T, RELU> nop;
+      nop.base = op;
+      nop.gg = pl.g;
+      return launch_rows(pl, nop, op, out, w, st);
+    }
+  }
+  return launch_reduce(pl, op, out, w, st);
+}
+
+// fp32: vector modes 1, 2, 4, 5 (masked float4); bf16 / fp16: 1, 2, 4, 8, 9 (masked 8).
+template <class T>
+int dispatch_stats_t(const Plan& pl, const void* x, bool shift, int mode, double* out,
+                     double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st,
+                     const double* ksum, const double* kcount) {
+  if constexpr (sizeof(T) == 4) {
+    switch (pl.vec) {
+      case 5: return run_stats<T, 5>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      case 4: return run_stats<T, 4>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      case 2: return run_stats<T, 2>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      default: return run_stats<T, 1>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+    }
+  } else {
+    switch (pl.vec) {
+      case 9: return run_stats<T, 9>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      case 8: return run_stats<T, 8>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      case 4: return run_stats<T, 4>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      case 2: return run_stats<T, 2>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+      default: return run_stats<T, 1>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+    }
+  }
+}
+
+int dispatch_stats(const Plan& pl, const void* x, bool shift, int mode, double* out,
+                   double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st,
+                   const double* ksum = nullptr, const double* kcount = nullptr) {
+  switch (pl.act) {
+    case 1:
+      return dispatch_stats_t<__nv_bfloat16>(pl, x, shift, mode, out, out2, F, w, st, ksum,
+                                             kcount);
+    case 2:
+      return dispatch_stats_t<__half>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+    default:
+      return dispatch_stats_t<float>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+  }
+}
+
+template <class T, bool RELU>
+int dispatch_bwd_t(const Plan& pl, const void* dy, const void* x, const double* saved,
+                   const float* gamma, const float* beta, int mode, double* out,
+                   const BwdFinal* F, const WsView& w, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    switch (pl.vec) {
+      case 5: return run_bwd_reduce<T, 5, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      case 4: return run_bwd_reduce<T, 4, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      case 2: return run_bwd_reduce<T, 2, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      default:
+        return run_bwd_reduce<T, 1, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+    }
+  } else {
+    switch (pl.vec) {
+      case 9: return run_bwd_reduce<T, 9, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      case 8: return run_bwd_reduce<T, 8, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      case 4: return run_bwd_reduce<T, 4, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      case 2: return run_bwd_reduce<T, 2, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+      default:
+        return run_bwd_reduce<T, 1, RELU>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+    }
+  }
+}
+
+template <class T>
+int dispatch_bwd_r(const Plan& pl, const void* dy, const void* x, const double* saved,
+                   const float* gamma, const float* beta, bool relu, int mode, double* out,
+                   const BwdFinal* F, const WsView& w, cudaStream_t st) {
+  return relu ? dispatch_bwd_t<T, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st)
+              : dispatch_bwd_t<T, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+}
+
+int dispatch_bwd_reduce(const Plan& pl, const void* dy, const void* x, const double* saved,
+                        const float* gamma, const float* beta, bool relu, int mode, double* out,
+                        const BwdFinal* F, const WsView& w, cudaStream_t st) {
+  switch (pl.act) {
+    case 1:
+      return dispatch_bwd_r<__nv_bfloat16>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w,
+                                           st);
+    case 2:
+      return dispatch_bwd_r<__half>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w, st);
+    default:
+      return dispatch_bwd_r<float>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w, st);
+  }
+}
+
+// ---- elementwise
+
+struct EwPlan {
+  EwGeom g;
+  int cm;
+  int act;
+};
+
+int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* const* ptrs,
+            int nptr, EwPlan* out) {
+  int rc = validate_shape(N, C, HW, layout);
+  if (rc) return rc;
+  uintptr_t align = 0;
+  for (int k = 0; k < nptr; ++k) align |= (uintptr_t)ptrs[k];
+  if (align % 16)
+    return set_error(CGBN_ERR_INVALID, "activation pointers must be 16-byte aligned");
+  const uint64_t E = (uint64_t)N * C * HW;
+  const uint32_t UE = 16 / act_bytes(act);  // elements per 16-byte unit
+  EwGeom& g = out->g;
+  g.C = (uint32_t)C;
+  g.HW = (uint32_t)HW;
+  g.n4 = (uint32_t)(E / UE);
+  g.tail = (uint32_t)(E % UE);
+  g.dhw.init((uint32_t)HW);
+  g.dc.init((uint32_t)C);
+  // Sweep from the end of the tensor: the preceding channel-major reduction read the
+  // high-n planes of every channel last, so they are the likeliest L2 hits (measured
+  // +1.5% on the ResNet-50 step, up to 7% on the 100 MB layers; CGBN_EW_FORWARD=1 off).
+  g.rev = getenv("CGBN_EW_FORWARD") ? 0u : 1u;
+  // channel modes work on 4-element chunks of a unit: CM 0 / 3 need HW % 4 / C % 4 only
+  (void)UE;
+  if (layout == CGBN_LAYOUT_NHWC || HW == 1) out->cm = (C % 4 == 0) ? 3 : 2;
+  else out->cm = (HW % 4 == 0) ? 0 : 1;
+  out->act = act;
+  return CGBN_OK;
+}
+
+// One round of kEwU units per thread, not a persistent grid: a copy-like kernel streams
+// faster with many short-lived CTAs than with one resident wave that loops (ResNet-50
+// step +3%, 100 MB layers 4-6 us faster; CGBN_EW_PERSISTENT=1 restores the resident
+// grid for A/B).
+template <class K>
+unsigned ew_grid(K kernel, const EwPlan& ep) {
+  int64_t grid = ceil_div((int64_t)ep.g.n4 + 1, kThreads * kEwU);
+  static const bool persistent = getenv("CGBN_EW_PERSISTENT") != nullptr;
+  if (persistent) {
+    const int64_t res = resident_ctas(kernel);
+    if (grid > res) grid = res;
+  }
+  return (unsigned)(grid < 1 ? 1 : grid);
+}
+
+// pdl: the kernel before this launch on `st` is one of ours that does not write x
+// (a reduction, finalize or coefficient kernel), so x may be prefetched before the
+// dependency wait.
+template <class T, bool RELU, int CM>
+void launch_ew_affine_t(const EwPlan& ep, const void* x, void* y, const double* P,
+                        const double* Q, bool pdl, cudaStream_t st) {
+  launch_pdl(k_ew_affine<T, RELU, CM>, ew_grid(k_ew_affine<T, RELU, CM>, ep), pdl, st, ep.g,
+             static_cast<const T*>(x), static_cast<T*>(y), P, Q);
+}
+
+template <class T, bool RELU>
+void launch_ew_affine_r(const EwPlan& ep, int cm, const void* x, void* y, const double* P,
+                        const double* Q, bool pdl, cudaStream_t st) {
+  if (cm == 0) launch_ew_affine_t<T, RELU, 0>(ep, x, y, P, Q, pdl, st);
+  else if (cm == 1) launch_ew_affine_t<T, RELU, 1>(ep, x, y, P, Q, pdl, st);
+  else if (cm == 2) launch_ew_affine_t<T, RELU, 2>(ep, x, y, P, Q, pdl, st);
+  else launch_ew_affine_t<T, RELU, 3>(ep, x, y, P, Q, pdl, st);
+}
+
+template <class T>
+void launch_ew_affine_d(const EwPlan& ep, int cm, bool relu, const void* x, void* y,
+                        const double* P, const double* Q, bool pdl, cudaStream_t st) {
+  if (relu) launch_ew_affine_r<T, true>(ep, cm, x, y, P, Q, pdl, st);
+  else launch_ew_affine_r<T, false>(ep, cm, x, y, P, Q, pdl, st);
+}
+
+void launch_ew_affine(const EwPlan& ep, bool relu, const void* x, void* y, const double* P,
+                      const double* Q, cudaStream_t st, bool pdl = true) {
+  int cm = ep.cm;
+  if (cm == 3 && (((uintptr_t)P | (uintptr_t)Q) % 16) != 0) cm = 2;  // caller's tables
+  if (ep.act == 1) launch_ew_affine_d<__nv_bfloat16>(ep, cm, relu, x, y, P, Q, pdl, st);
+  else if (ep.act == 2) launch_ew_affine_d<__half>(ep, cm, relu, x, y, P, Q, pdl, st);
+  else launch_ew_affine_d<float>(ep, cm, relu, x, y, P, Q, pdl, st);
+}
+
+template <class T, bool RELU, int CM>
+void launch_ew_dx_t(const EwPlan& ep, const void* dy, const void* x, void* dx, const WsView& w,
+                    cudaStream_t st) {
+  launch_pdl(k_ew_dx<T, RELU, CM>, ew_grid(k_ew_dx<T, RELU, CM>, ep), true, st, ep.g,
+             static_cast<const T*>(dy), static_cast<const T*>(x), static_cast<T*>(dx),
+             (const double*)w.A, (const double*)w.B, (const double*)w.Cc, (const double*)w.P,
+             (const double*)w.Q);
+}
+
+template <class T, bool RELU>
+void launch_ew_dx_r(const EwPlan& ep, const void* dy, const void* x, void* dx, const WsView& w,
+                    cudaStream_t st) {
+  if (ep.cm == 0) launch_ew_dx_t<T, RELU, 0>(ep, dy, x, dx, w, st);
+  else if (ep.cm == 1) launch_ew_dx_t<T, RELU, 1>(ep, dy, x, dx, w, st);
+  else if (ep.cm == 2) launch_ew_dx_t<T, RELU, 2>(ep, dy, x, dx, w, st);
+  else launch_ew_dx_t<T, RELU, 3>(ep, dy, x, dx, w, st);
+}
+
+template <class T>
+void launch_ew_dx_d(const EwPlan& ep, bool relu, const void* dy, const void* x, void* dx,
+                    const WsView& w, cudaStream_t st) {
+  if (relu) launch_ew_dx_r<T, true>(ep, dy, x, dx, w, st);
+  else launch_ew_dx_r<T, false>(ep, dy, x, dx, w, st);
+}
+
+void launch_ew_dx(const EwPlan& ep, bool relu, const void* dy, const void* x, void* dx,
+                  const WsView& w, cudaStream_t st) {
+  if (ep.act == 1) launch_ew_dx_d<__nv_bfloat16>(ep, relu, dy, x, dx, w, st);
+  else if (ep.act == 2) launch_ew_dx_d<__half>(ep, relu, dy, x, dx, w, st);
+  else launch_ew_dx_d<float>(ep, relu, dy, x, dx, w, st);
+}
+
+unsigned chan_blocks(int64_t C) { return (unsigned)ceil_div(C, 256); }
+
+FwdFinal make_fwd_final(int64_t C, const float* gamma, const float* beta, double eps,
+                        double momentum, float* rm, float* rv, double* saved, unsigned* status,
+                        const WsView& w) {
+  FwdFinal F;
+  F.gamma = gamma; F.beta = beta;
+  F.eps = eps; F.momentum = momentum;
+  F.rmean = rm; F.rvar = rv;
+  F.saved = saved;
+  F.P = w.P; F.Q = w.Q;
+  F.status = status;
+  F.C = (uint32_t)C;
+  return F;
+}
+
+BwdFinal make_bwd_final(int64_t C, const double* saved, const float* gamma, const float* beta,
+                        double eps, bool relu, float* dgamma, float* dbeta, unsigned* status,
+                        const WsView& w) {
+  BwdFinal F;
+  F.saved = saved; F.gamma = gamma; F.beta = beta;
+  F.eps = eps;
+  F.relu = relu ? 1 : 0;
+  F.A = w.A; F.B = w.B; F.Cc = w.Cc; F.P = w.P; F.Q = w.Q;
+  F.dgamma = dgamma; F.dbeta = dbeta;
+  F.status = status;
+  F.C = (uint32_t)C;
+  return F;
+}
+
+// ---- fused cooperative kernels (cgbn_fused.cuh)
+
+bool fused_plan(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align, int nin,
+                fused::FGeom* fg) {
+  if (path_override() == 2 || getenv("CGBN_NO_FUSED")) return false;
+  if (layout != CGBN_LAYOUT_NCHW || HW % 4 != 0 || (align % 16) != 0) return false;
+  if (validate_shape(N, C, HW, layout) != CGBN_OK) return false;
+  const int64_t L = N * HW;
+  const int64_t T4 = C * L / 4;
+  int64_t grid = ceil_div(T4, 64);
+  if (grid > num_sms_cached()) grid = num_sms_cached();
+  if (grid < 1) grid = 1;
+  const int64_t max_slice = ceil_div(T4, grid) * 4;
+  const int64_t cap = (int64_t)(fused::kDataBytes / (4 * nin));
+  if (max_slice > cap) return false;
+  if (max_slice / L + 2 > fused::kMaxSeg) return false;
+  fg->C = (uint32_t)C;
+  fg->HW = (uint32_t)HW;
+  fg->L = (uint32_t)L;
+  fg->grid = (uint32_t)grid;
+  fg->T4 = (uint64_t)T4;
+  fg->dhw.init((uint32_t)HW);
+  fg->count = (double)L;
+  return true;
+}
+
+// Cooperative grids must never interleave on one device (their grid barriers could
+// deadlock): launches from different streams of one process are chained through a
+// per-device event. Skipped under stream capture, where a graph replays in order.
+std::mutex g_coop_mu;
+cudaEvent_t g_coop_last[64] = {nullptr};
+
+template <class K, class... Args>
+int launch_cooperative(K kernel, unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  const bool chain = cap == cudaStreamCaptureStatusNone && dev >= 0 && dev < 64;
+  std::unique_lock<std::mutex> lk(g_coop_mu, std::defer_lock);
+  if (chain) {
+    lk.lock();
+    if (!g_coop_last[dev]) cudaEventCreateWithFlags(&g_coop_last[dev], cudaEventDisableTiming);
+    cudaStreamWaitEvent(st, g_coop_last[dev], 0);
+  }
+  smem_optin(kernel, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(fused::kThreadsF);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (chain) cudaEventRecord(g_coop_last[dev], st);
+  if (e != cudaSuccess)
+    return set_error(CGBN_ERR_CUDA, "cooperative launch failed: %s", cudaGetErrorString(e));
+  return CGBN_OK;
+}
+
+#define CGBN_REQUIRE(cond, ...) \
+  do { if (!(cond)) return set_error(CGBN_ERR_INVALID, __VA_ARGS__); } while (0)
+
+#define CGBN_TRY(expr) \
+  do { int rc_ = (expr); if (rc_) return rc_; } while (0)
+
+int check_fwd_args(const void* x, const void* y, const float* gamma, const float* beta,
+                   const double* saved, double eps, double momentum, const float* running_mean,
+                   const float* running_var) {
+  CGBN_REQUIRE(x && y && gamma && beta && saved, "forward: NULL pointer");
+  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
+  CGBN_REQUIRE(momentum >= 0.0 && momentum <= 1.0, "momentum must lie in [0, 1], got %g",
+               momentum);
+  CGBN_REQUIRE((running_mean == nullptr) == (running_var == nullptr),
+               "running_mean and running_var must both be set or both be NULL");
+  return CGBN_OK;
+}
+
+}  // namespace
