@@ -75,6 +75,7 @@ struct EwGeom {
   uint32_t tail;  // E % UE
   FastDiv dhw, dc;
   uint32_t rev;   // 1: sweep from the end of the tensor (LRU-friendly after a reduction)
+  uint32_t reuse; // CM 3, fp32: a thread's units share their 4 channels (UE*stride % C == 0)
 };
 
 __device__ __forceinline__ uint32_t ew_unit(const EwGeom& g, uint32_t j) {
@@ -158,6 +159,16 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
   };
   load(i);    // x is not written by the kernel we may overlap with
   pdl_wait();  // the coefficient table is
+  // channels_last: when every unit of the thread covers the same 4 channels, their
+  // coefficients are loaded once
+  constexpr bool kReuse = CM == 3 && UE == 4;
+  double pr[4], qr[4];
+  if (kReuse && g.reuse && i < g.n4) {
+    uint32_t c[4];
+    chan4<CM>(g, UE * ew_unit(g, i), c);
+    ew_coef<CM>(P, c, pr);
+    ew_coef<CM>(Q, c, qr);
+  }
   for (; i < g.n4; i += kEwU * stride) {
 #pragma unroll
     for (int u = 0; u < kEwU; ++u) {
@@ -167,11 +178,19 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
       double o[UE];
 #pragma unroll
       for (int h = 0; h < UE; h += 4) {
-        uint32_t c[4];
-        chan4<CM>(g, UE * jm + h, c);
         double p[4], q[4];
-        ew_coef<CM>(P, c, p);
-        ew_coef<CM>(Q, c, q);
+        if (kReuse && g.reuse) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            p[k] = pr[k];
+            q[k] = qr[k];
+          }
+        } else {
+          uint32_t c[4];
+          chan4<CM>(g, UE * jm + h, c);
+          ew_coef<CM>(P, c, p);
+          ew_coef<CM>(Q, c, q);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           double t = __fma_rn(p[k], (double)v[u].get(h + k), q[k]);
@@ -214,6 +233,19 @@ k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restri
   };
   load(i);    // dy and x are not written by the kernel we may overlap with
   pdl_wait();  // the coefficient tables are
+  constexpr bool kReuse = CM == 3 && UE == 4;  // see k_ew_affine
+  double ar[4], br[4], cr[4], pr[4] = {0.0, 0.0, 0.0, 0.0}, qr[4] = {0.0, 0.0, 0.0, 0.0};
+  if (kReuse && g.reuse && i < g.n4) {
+    uint32_t c[4];
+    chan4<CM>(g, UE * ew_unit(g, i), c);
+    ew_coef<CM>(A, c, ar);
+    ew_coef<CM>(B, c, br);
+    ew_coef<CM>(Cc, c, cr);
+    if (RELU) {
+      ew_coef<CM>(P, c, pr);
+      ew_coef<CM>(Q, c, qr);
+    }
+  }
   for (; i < g.n4; i += kEwU * stride) {
 #pragma unroll
     for (int u = 0; u < kEwU; ++u) {
@@ -223,15 +255,26 @@ k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restri
       double o[UE];
 #pragma unroll
       for (int h = 0; h < UE; h += 4) {
-        uint32_t c[4];
-        chan4<CM>(g, UE * jm + h, c);
         double a[4], b[4], cc[4], p[4] = {0.0, 0.0, 0.0, 0.0}, q[4] = {0.0, 0.0, 0.0, 0.0};
-        ew_coef<CM>(A, c, a);
-        ew_coef<CM>(B, c, b);
-        ew_coef<CM>(Cc, c, cc);
-        if (RELU) {
-          ew_coef<CM>(P, c, p);
-          ew_coef<CM>(Q, c, q);
+        if (kReuse && g.reuse) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            a[k] = ar[k];
+            b[k] = br[k];
+            cc[k] = cr[k];
+            p[k] = pr[k];
+            q[k] = qr[k];
+          }
+        } else {
+          uint32_t c[4];
+          chan4<CM>(g, UE * jm + h, c);
+          ew_coef<CM>(A, c, a);
+          ew_coef<CM>(B, c, b);
+          ew_coef<CM>(Cc, c, cc);
+          if (RELU) {
+            ew_coef<CM>(P, c, p);
+            ew_coef<CM>(Q, c, q);
+          }
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {

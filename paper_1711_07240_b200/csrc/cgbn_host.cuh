@@ -675,6 +675,7 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* c
   // high-n planes of every channel last, so they are the likeliest L2 hits (measured
   // +1.5% on the ResNet-50 step, up to 7% on the 100 MB layers; CGBN_EW_FORWARD=1 off).
   g.rev = getenv("CGBN_EW_FORWARD") ? 0u : 1u;
+  g.reuse = 0;
   // channel modes work on 4-element chunks of a unit: CM 0 / 3 need HW % 4 / C % 4 only
   (void)UE;
   if (layout == CGBN_LAYOUT_NHWC || HW == 1) out->cm = (C % 4 == 0) ? 3 : 2;
@@ -701,11 +702,24 @@ unsigned ew_grid(K kernel, const EwPlan& ep) {
 // pdl: the kernel before this launch on `st` is one of ours that does not write x
 // (a reduction, finalize or coefficient kernel), so x may be prefetched before the
 // dependency wait.
+// Grid plus the channels_last coefficient-reuse flag (a thread's units are gridDim*256
+// units apart; they share their channels when that distance covers whole rows).
+template <class K>
+unsigned ew_grid_geom(K kernel, const EwPlan& ep, EwGeom* g) {
+  const unsigned grid = ew_grid(kernel, ep);
+  *g = ep.g;
+  const uint64_t ue = ep.act == 0 ? 4 : 8;
+  g->reuse = (ep.cm == 3 && (ue * (uint64_t)grid * kThreads) % ep.g.C == 0) ? 1u : 0u;
+  return grid;
+}
+
 template <class T, bool RELU, int CM>
 void launch_ew_affine_t(const EwPlan& ep, const void* x, void* y, const double* P,
                         const double* Q, bool pdl, cudaStream_t st) {
-  launch_pdl(k_ew_affine<T, RELU, CM>, ew_grid(k_ew_affine<T, RELU, CM>, ep), pdl, st, ep.g,
-             static_cast<const T*>(x), static_cast<T*>(y), P, Q);
+  EwGeom g;
+  const unsigned grid = ew_grid_geom(k_ew_affine<T, RELU, CM>, ep, &g);
+  launch_pdl(k_ew_affine<T, RELU, CM>, grid, pdl, st, g, static_cast<const T*>(x),
+             static_cast<T*>(y), P, Q);
 }
 
 template <class T, bool RELU>
@@ -736,7 +750,9 @@ void launch_ew_affine(const EwPlan& ep, bool relu, const void* x, void* y, const
 template <class T, bool RELU, int CM>
 void launch_ew_dx_t(const EwPlan& ep, const void* dy, const void* x, void* dx, const WsView& w,
                     cudaStream_t st) {
-  launch_pdl(k_ew_dx<T, RELU, CM>, ew_grid(k_ew_dx<T, RELU, CM>, ep), true, st, ep.g,
+  EwGeom g;
+  const unsigned grid = ew_grid_geom(k_ew_dx<T, RELU, CM>, ep, &g);
+  launch_pdl(k_ew_dx<T, RELU, CM>, grid, true, st, g,
              static_cast<const T*>(dy), static_cast<const T*>(x), static_cast<T*>(dx),
              (const double*)w.A, (const double*)w.B, (const double*)w.Cc, (const double*)w.P,
              (const double*)w.Q);
