@@ -494,13 +494,23 @@ def run_gpu_arm(args):
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # --same-device / --dist-backend gloo: every rank on GPU 0 with host-staged
+    # exchanges, to exercise the N>1 orchestration on a single-GPU box (not a benchmark)
+    dev_index = 0 if args.same_device else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    nccl = args.dist_backend == "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if nccl:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
         def _barrier():
-            dist.barrier(device_ids=[local_rank])
+            if nccl:
+                dist.barrier(device_ids=[dev_index])
+            else:
+                dist.barrier()
 
         handle, transport_report = select_transport(cg, torch, dist, dev, world,
                                                     args.transport, _barrier)
@@ -534,7 +544,10 @@ def run_gpu_arm(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            if nccl:
+                dist.barrier(device_ids=[dev_index])
+            else:
+                dist.barrier()
 
     side = torch.cuda.Stream(device=dev)
     side.wait_stream(torch.cuda.current_stream())
@@ -569,7 +582,7 @@ def run_gpu_arm(args):
             step()
 
     # ---- timed region
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     sampler.start()
     time.sleep(0.3)
     barrier()
@@ -735,8 +748,7 @@ def run_gpu_arm(args):
                           f" via DeviceGroup(1); {res['seconds']:.1f} s"),
                **host_cpu_info()}
 
-    if world > 1:
-        dist.barrier(device_ids=[local_rank])
+    barrier()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -784,6 +796,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cgbn", "reference"], default="cgbn")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help=argparse.SUPPRESS)  # gloo: orchestration test on one GPU
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--transport", choices=["auto", "nccl", "p2p"], default="auto",
                     help="BN-group statistics exchange at N>1: NCCL all-gather, the one-shot "
                          "P2P exchange, or auto (P2P if it passes its self-test and is faster)")

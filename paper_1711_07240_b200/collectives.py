@@ -536,8 +536,12 @@ def _all_gather_rows(vec: torch.Tensor, g: int, pg) -> torch.Tensor:
     import torch.distributed as dist
     vec = vec.contiguous()
     out = torch.empty((g, vec.numel()), dtype=vec.dtype, device=vec.device)
-    if vec.is_cuda:
+    if vec.is_cuda and dist.get_backend(pg) == "nccl":
         dist.all_gather_into_tensor(out.view(-1), vec, group=pg)
+    elif vec.is_cuda:  # host-staged (gloo with CUDA tensors: tests, no NVLink path)
+        host = torch.empty((g, vec.numel()), dtype=vec.dtype)
+        dist.all_gather(list(host.unbind(0)), vec.cpu(), group=pg)
+        out.copy_(host)
     else:
         dist.all_gather(list(out.unbind(0)), vec, group=pg)
     return out
