@@ -470,6 +470,87 @@ __global__ void __launch_bounds__(kT) v9(G g, const float* __restrict__ x, doubl
   }
 }
 
+// V10: cluster-team streaming with a per-thread cp.async ring in shared memory (S stages
+// of U units): loads stay in flight continuously instead of draining per round. No tail
+// (compare with V8t4). Incremental channel-major addresses.
+template <int TLC, int U, int S>
+__global__ void __launch_bounds__(kT) v10(G g, const float* __restrict__ x, double* out) {
+  extern __shared__ float4 ring[];  // [S][U][kT]
+  constexpr uint32_t tpc = 1u << TLC;
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t KC = cl.num_blocks(), r = cl.block_rank();
+  const uint32_t q = blockIdx.x / KC;
+  const uint32_t nl = 8 - TLC;
+  const uint32_t team = threadIdx.x >> TLC, tq = threadIdx.x & (tpc - 1);
+  const uint32_t c = (q << nl) + team;
+  const uint32_t j0 = (uint32_t)((uint64_t)r * g.Lv / KC), j1 = (uint32_t)((uint64_t)(r + 1) * g.Lv / KC);
+  double a = 0, b = 0;
+  if (c < g.C) {
+    const float4* x4 = reinterpret_cast<const float4*>(x) + (size_t)c * g.HWv;
+    const uint64_t pstride = (uint64_t)g.C * g.HWv;
+    // cursor
+    uint32_t jj = j0 + tq;
+    uint32_t n = g.dhw.div(jj), o = jj - n * g.HWv;
+    const uint32_t sq = tpc / g.HWv, sr = tpc % g.HWv;
+    auto issue = [&](int stage, uint32_t jstart) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (jstart + u * tpc < j1) {
+          const float4* src = x4 + n * pstride + o;
+          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ring[(stage * U + u) * kT + threadIdx.x]);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+        n += sq; o += sr;
+        if (o >= g.HWv) { o -= g.HWv; ++n; }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const uint32_t step = U * tpc;
+    uint32_t jissue = j0 + tq;
+#pragma unroll
+    for (int s0 = 0; s0 < S - 1; ++s0) { issue(s0, jissue); jissue += step; }
+    int stage = 0;
+    for (uint32_t jc = j0 + tq; jc < j1; jc += step) {
+      issue((stage + S - 1) % S, jissue);
+      jissue += step;
+      asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (jc + u * tpc < j1) acc4(ring[(stage * U + u) * kT + threadIdx.x], 1.0, a, b);
+      stage = (stage + 1) % S;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  if (a + b == 12345.0) out[blockIdx.x] = a;
+}
+
+template <int U, int S>
+void launch_v10(const G& g, const float* x, double* out, uint32_t KC, uint32_t nl, cudaStream_t st) {
+  const uint32_t nch = 1u << nl;
+  const uint32_t Q = (g.C + nch - 1) / nch;
+  const size_t smem = (size_t)S * U * kT * sizeof(float4);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(Q * KC);
+  cfg.blockDim = dim3(kT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = KC; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  switch (nl) {
+    case 0: cudaFuncSetAttribute(v10<8, U, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaLaunchKernelEx(&cfg, v10<8, U, S>, g, x, out); break;
+    case 1: cudaFuncSetAttribute(v10<7, U, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaLaunchKernelEx(&cfg, v10<7, U, S>, g, x, out); break;
+    case 2: cudaFuncSetAttribute(v10<6, U, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaLaunchKernelEx(&cfg, v10<6, U, S>, g, x, out); break;
+    default: cudaFuncSetAttribute(v10<5, U, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+             cudaLaunchKernelEx(&cfg, v10<5, U, S>, g, x, out); break;
+  }
+}
+
 int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -611,6 +692,10 @@ int main(int argc, char** argv) {
           timeit("V8t2 block reduce only", [&](const float* p) { launch_vct<4, false, 2>(g, p, out, bestK, bestL, st, true); });
           if (bestL == 0) timeit("V8p pipelined (nch=1)", [&](const float* p) { launch_vct<4, false, 5>(g, p, out, bestK, bestL, st, true); });
           timeit("V8t3 linear addresses", [&](const float* p) { launch_vct<4, false, 3>(g, p, out, bestK, bestL, st, true); });
+          timeit("V10 cp.async ring U4 S3", [&](const float* p) { launch_v10<4, 3>(g, p, out, bestK, bestL, st); });
+          timeit("V10 cp.async ring U4 S4", [&](const float* p) { launch_v10<4, 4>(g, p, out, bestK, bestL, st); });
+          timeit("V10 cp.async ring U2 S6", [&](const float* p) { launch_v10<2, 6>(g, p, out, bestK, bestL, st); });
+          timeit("V10 cp.async ring U8 S2", [&](const float* p) { launch_v10<8, 2>(g, p, out, bestK, bestL, st); });
           {
             const uint32_t g4 = (uint32_t)((g.T + kT * 4 - 1) / (kT * 4));
             timeit("V9 nonpersistent flat UPT4", [&](const float* p) { v9<4><<<g4, kT, 0, st>>>(g, p, out, (double2*)wsd, tk); });
