@@ -632,7 +632,9 @@ def world_mean_allreduce(handle: _HandleBase, grads: dict, loss=None):
     keys = sorted(grads)
     if not keys:
         raise ValueError("world_mean_allreduce needs at least one gradient")
-    dt = grads[keys[0]].dtype
+    # fold in fp64 if any gradient is fp64, else fp32 (bf16 / fp16 gradients are widened
+    # for the sum and returned in their own dtype)
+    dt = torch.float64 if any(grads[k].dtype == torch.float64 for k in keys) else torch.float32
     dev = grads[keys[0]].device
     flat = [grads[k].reshape(-1).to(dt) for k in keys]
     if loss is not None:
@@ -641,6 +643,6 @@ def world_mean_allreduce(handle: _HandleBase, grads: dict, loss=None):
     out, off = {}, 0
     for k in keys:
         n = grads[k].numel()
-        out[k] = mean[off:off + n].view(grads[k].shape)
+        out[k] = mean[off:off + n].view(grads[k].shape).to(grads[k].dtype)
         off += n
     return out, (float(mean[-1].item()) if loss is not None else None)
