@@ -4,18 +4,28 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr
 PKG := paper_1711_07240_b200
 LIB := $(PKG)/libcgbn.so
-SRCS := $(PKG)/csrc/cgbn.cu
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/cgbn.h
+OBJS := build/cgbn.o build/cgbn_conv.o
 
 all: $(LIB)
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -Xptxas -v -shared -o $@ $(SRCS) 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
+# two translation units: the BN kernels (cgbn.cu + its .cuh parts) and the tcgen05
+# producer-fusion conv (cgbn_conv.cu)
+build/cgbn.o: $(PKG)/csrc/cgbn.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> $(PKG)/csrc/ptxas.log || (cat $(PKG)/csrc/ptxas.log; exit 1)
+
+build/cgbn_conv.o: $(PKG)/csrc/cgbn_conv.cu include/cgbn.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> $(PKG)/csrc/ptxas_conv.log || (cat $(PKG)/csrc/ptxas_conv.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 sass: $(LIB)
 	cuobjdump -sass $(LIB) > $(PKG)/csrc/cgbn.sass
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(OBJS)
 
 .PHONY: all clean sass

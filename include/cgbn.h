@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CGBN_ABI_VERSION 5
+#define CGBN_ABI_VERSION 6
 
 #define CGBN_LAYOUT_NCHW 0
 #define CGBN_LAYOUT_NHWC 1
@@ -255,6 +255,29 @@ int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
                    const double* saved, const float* gamma, const float* beta, double eps,
                    int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
                    size_t ws_bytes, void* stream);
+
+/* Producer fusion (ABI v6). The layer that feeds a BN in the
+ * reference model is a GEMM-shaped convolution (model.py:235-242, out = cols @ W^T + b)
+ * whose output _train_forward immediately re-reads for its statistics (batchnorm.py:118,
+ * channel_sum, tensor.py:143-153). cgbn_conv1x1_stats computes the pointwise (1x1) case
+ *     z[n][co][p] = sum_ci w[co][ci] * x[n][ci][p] + bias[co]          (NCHW, p = h*W + w)
+ * on the tcgen05 tensor cores (bf16 x and w, fp32 accumulation, z stored as fp32 or bf16
+ * per out_dtype = CGBN_ACT_F32 / CGBN_ACT_BF16) and, in the same kernel's epilogue, this
+ * rank's forward partial of z as stored (2C+1 doubles, [mean | M2 | count], C = Cout) —
+ * the vector cgbn_fwd_stats(z) would produce, so the exchange and cgbn_fwd_normalize
+ * follow unchanged and the BN forward no longer reads z for its statistics.
+ *  bias     : Cout floats or NULL.
+ *  ws       : cgbn_conv1x1_ws_bytes(N, Cout, HW) bytes, 16-byte aligned (per-tile
+ *             partials; need not be zeroed).
+ * Two launches (the conv, then a per-channel fold of the tile partials). Returns
+ * CGBN_ERR_UNSUPPORTED when H*W or Cin is not a multiple of 8 (TMA row strides).
+ * cgbn_conv1x1 is the same convolution without the statistics (the unfused producer). */
+size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW);
+int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                 int64_t Cout, int64_t HW, int out_dtype, void* z, void* stream);
+int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                       int64_t Cout, int64_t HW, int out_dtype, void* z, double* partial,
+                       void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,9 @@ SIGNATURES = {
                             _sz, _p]),
     "cgbn_bwd_fused": (_i, [_p, _p, _i64, _i64, _i64, _i, _p, _p, _p, _d, _i, _p, _p, _p, _p, _p,
                             _sz, _p]),
+    "cgbn_conv1x1_ws_bytes": (_sz, [_i64, _i64, _i64]),
+    "cgbn_conv1x1": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i, _p, _p]),
+    "cgbn_conv1x1_stats": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
 }
 
 _lib = None

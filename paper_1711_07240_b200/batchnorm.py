@@ -365,15 +365,21 @@ def _train_forward_reference(g, state, exchange, scope_key, one_pass, relu, what
 
 
 def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
-                   one_pass: bool, relu: bool, what: str):
+                   one_pass: bool, relu: bool, what: str, partial=None):
     """The CGBN forward (batchnorm.py:115-144) on the device.
 
     G > 1: stats kernel -> exchange of the per-rank partials -> finalize (fold + running
     update + coefficients) and elementwise normalise. G == 1: the stats kernel finalises
     each channel itself (cgbn_fwd_train_local), or one fused cooperative kernel when
     enabled (set_fused) and the activation fits on chip.
+
+    ``partial``: this rank's forward partial of ``x`` already computed by its producer
+    (producer fusion, ``producer.py``); the statistics kernel is skipped and the partial
+    goes straight to the exchange and the normalise pass (for any G).
     """
     g = _check_layout(x, state)
+    if partial is not None and _exchange_mode != "merged":
+        raise BatchNormError("a producer-computed partial needs set_forward_exchange('merged')")
     if _exchange_mode == "reference":
         if group_size == 1 and g.count < 2:
             raise BatchNormError(
@@ -390,7 +396,7 @@ def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
     nb = lib.cgbn_workspace_bytes(g.N, c, g.HW, g.layout)
     ws = workspace(dev, nb)
     rm, rv = state.running_mean.data_ptr(), state.running_var.data_ptr()
-    if group_size == 1:
+    if group_size == 1 and partial is None:
         total = g.count
         if total < 2:
             raise BatchNormError(
@@ -415,10 +421,14 @@ def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
         _raise_status(what, status, total)
         return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
                                  relu=bool(relu), one_pass=bool(one_pass), _total_count=total)
-    partial = torch.empty(2 * c + 1, dtype=torch.float64, device=dev)
-    with _Span("fwd_stats", 4 * e):
-        _lib.check(lib.cgbn_fwd_stats(g.x.data_ptr(), g.N, c, g.HW, g.layout, partial.data_ptr(),
-                                      ws.data_ptr(), ws.numel(), st), "cgbn_fwd_stats")
+    if partial is None:
+        partial = torch.empty(2 * c + 1, dtype=torch.float64, device=dev)
+        with _Span("fwd_stats", 4 * e):
+            _lib.check(lib.cgbn_fwd_stats(g.x.data_ptr(), g.N, c, g.HW, g.layout,
+                                          partial.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                       "cgbn_fwd_stats")
+    elif partial.numel() != 2 * c + 1 or partial.dtype != torch.float64:
+        raise BatchNormError(f"forward partial must be {2 * c + 1} float64 values")
     parts, infos = exchange(partial, g.count)
     total = None
     if infos is not None and all(i is not None for i in infos):

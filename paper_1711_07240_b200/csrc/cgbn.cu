@@ -89,6 +89,10 @@ constexpr size_t kTicketBytes = (kTicketWords + 64) * sizeof(unsigned);
 #include "cgbn_p2p.cuh"
 #include "cgbn_host.cuh"
 
+// Error hook for the other translation unit (cgbn_conv.cu): one thread-local message
+// behind cgbn_last_error().
+int cgbn_internal_set_error(int code, const char* msg) { return set_error(code, "%s", msg); }
+
 // ==================================================================================
 // C ABI
 

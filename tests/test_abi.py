@@ -53,7 +53,7 @@ def test_constants_match_header():
 
 def test_abi_version_and_argument_validation_without_gpu():
     lib = _lib.load()
-    assert lib.cgbn_abi_version() == 5
+    assert lib.cgbn_abi_version() == 6
     assert b"sm_100a" in lib.cgbn_build_info()
     # invalid shapes are rejected on the host before any CUDA call
     rc = lib.cgbn_fwd_stats(None, 2, 3, 4, 0, None, None, 0, None)
