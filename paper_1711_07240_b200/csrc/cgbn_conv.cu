@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -50,11 +51,13 @@ namespace {
 constexpr int BM = 128;       // output channels per tile (TMEM lanes)
 constexpr int BN = 128;       // pixels per tile (TMEM columns)
 constexpr int BK = 64;        // input channels per ring stage (128 B of bf16)
-constexpr int kConvThreads = 128;
+constexpr int kEpiWarps = 8;
+constexpr int kHalf = 64;                       // tile columns per epilogue warp
+constexpr uint32_t kWarpStage = 32 * 128;       // one warp's staged rows: 4 KB
+constexpr int kConvThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilogue warps
 constexpr uint32_t kTileA = BM * BK * 2;      // 16 KB
 constexpr uint32_t kTileB = BK * BN * 2;      // 16 KB (two 64-pixel boxes of 8 KB)
 constexpr uint32_t kStage = kTileA + kTileB;  // 32 KB
-constexpr uint32_t kStageOut = BM * 128;      // one 128-byte row per channel: 16 KB
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -196,36 +199,75 @@ struct OutTraits<__nv_bfloat16> {
   __device__ static float round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 };
 
-struct ConvArgs {
-  const float* bias;  // may be null
-  double2* slots;     // [tiles per channel][Cout] (mean, M2); null = no statistics
-  int Cout, HW, tilesP, mtiles, kblocks;
+// Pairwise (tree) sum of the first nv of 32 values (nv >= 32: all, no masking).
+__device__ __forceinline__ float masked_tree32(const float (&v)[32], int nv) {
+  float t[32];
+  if (nv >= 32) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t[i] = v[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t[i] = i < nv ? v[i] : 0.f;
+  }
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) t[i] += t[i + w];
+  return t[0];
+}
+
+// Statistics slot of one (CTA, tile half): this thread's channel over every tile the
+// CTA processed — count, mean and centred M2.
+struct Slot {
+  double n, mean, M2;
 };
 
-// One output tile. S = ring stages.
-template <int S, class OutT>
-__global__ void __launch_bounds__(kConvThreads, 2)
+struct ConvArgs {
+  const float* bias;  // may be null
+  Slot* slots;        // [2 * ceil(grid / mtiles)][Cout]; null = no statistics
+  int Cout, HW, tilesP, mtiles, kblocks, tiles;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// Persistent, warp-specialised: one CTA per SM walks the output tiles t = blockIdx.x,
+// blockIdx.x + gridDim.x, ... (tile order: channel tile fastest, then pixel tile, then
+// image, so the CTAs running together share their x tiles in L2). gridDim.x is a
+// multiple of the number of channel tiles, so every tile of a CTA has the same 128
+// output channels and each epilogue thread keeps one channel for the whole kernel.
+//   warp 0        TMA: k-blocks of successive tiles through an S-stage ring, no pause
+//                 between tiles;
+//   warp 1        MMA issue into two TMEM accumulators (2 x 128 columns), so the
+//                 epilogue of tile i overlaps the loads and MMAs of tile i+1;
+//   warps 2..9    epilogue; warp w reaches TMEM lanes [32 * (w % 4), +32) and takes one
+//                 64-column half of the tile. Per 32 columns: tcgen05.ld, + bias, round to
+//                 the output type, stage the 32 rows x 128 B in the warp's own
+//                 128B-swizzled double buffer, one lane TMA-stores them; with STATS the
+//                 same registers feed the channel statistics.
+// Statistics (STATS): the shifted sums of the stored values, d = z - K with one shift K
+// per thread (the fp32 mean of its first half-tile, from a TMEM pre-pass on that tile
+// only): N, SD = sum d (fp64 per element), SQ = sum d^2 (fp32 pairwise per 32 values,
+// fp64 above). |d| is of the order of the channel's spread whatever its mean, so
+// mean = K + SD/N and M2 = SQ - SD^2/N keep the BN tolerances also for |mean| >> std.
+// Each (CTA, half) writes one Slot per channel; k_conv_fold merges the slots.
+template <int S, class OutT, bool STATS>
+__global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1x1(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmZ, const ConvArgs a) {
   constexpr int kCols = OutTraits<OutT>::kCols;
-  constexpr int kChunks = BN / kCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* ring = smem;                        // S x [A 16 KB | B 16 KB]
-  uint8_t* stage_out = smem + S * kStage;      // 2 x 16 KB (double-buffered TMA store)
-  uint64_t* full = (uint64_t*)(stage_out + 2 * kStageOut);
+  uint8_t* stage_out = smem + S * kStage;      // 8 warps x 2 x 4 KB (TMA store staging)
+  uint64_t* full = (uint64_t*)(stage_out + kEpiWarps * 2 * kWarpStage);
   uint64_t* empty = full + S;
-  uint64_t* done = empty + S;
-  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  uint64_t* tfull = empty + S;                 // [2] accumulator ready (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2;                // [2] accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bid = blockIdx.x;
-  const int mt = bid % a.mtiles;
-  const int rest = bid / a.mtiles;
-  const int pt = rest % a.tilesP;
-  const int img = rest / a.tilesP;
-  const int m0 = mt * BM, p0 = pt * BN;
-
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
@@ -234,10 +276,13 @@ __global__ void __launch_bounds__(kConvThreads, 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 32 * kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, BN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -246,170 +291,208 @@ __global__ void __launch_bounds__(kConvThreads, 2)
   // x may be produced by the kernel before us (programmatic dependent launch).
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == 0 && lane == 0) {
-    // TMA producer
-    for (int kb = 0; kb < a.kblocks; ++kb) {
-      const int s = kb % S;
-      if (kb >= S) mbar_wait(&empty[s], ((kb / S) & 1) ^ 1);
-      uint8_t* A = ring + s * kStage;
-      uint8_t* B = A + kTileA;
-      mbar_expect_tx(&full[s], kStage);
-      tma_load_2d(A, &tmW, &full[s], kb * BK, m0);
-      tma_load_3d(B, &tmX, &full[s], p0, kb * BK, img);
-      tma_load_3d(B + kTileB / 2, &tmX, &full[s], p0 + 64, kb * BK, img);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer
-    for (int kb = 0; kb < a.kblocks; ++kb) {
-      const int s = kb % S;
-      mbar_wait(&full[s], (kb / S) & 1);
-      tc_fence_after();
-      const uint32_t A = smem_u32(ring + s * kStage);
-      const uint32_t B = A + kTileA;
-#pragma unroll
-      for (int k = 0; k < BK / 16; ++k) {
-        // A: K-major rows of 128 B, 8-row atoms 1024 B apart; K step = 32 B in the row.
-        // B: MN-major, 64-pixel halves 8 KB apart (LBO), 8-channel groups 1 KB apart
-        //    (SBO); K step = 16 rows = 2 KB.
-        const uint64_t ad = sdesc(A + k * 32, 16, 1024);
-        const uint64_t bd = sdesc(B + k * 2048, kTileB / 2, 1024);
-        mma_bf16(tmem, ad, bd, kIdesc, (kb | k) != 0);
-      }
-      mma_commit(&empty[s]);
-    }
-    mma_commit(done);
-  }
-  __syncwarp();
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
-  // ---------------- epilogue: thread t <-> TMEM lane t <-> channel m0 + t
-  mbar_wait(done, 0);
-  tc_fence_after();
-  const int row = warp * 32 + lane;
-  const int c = m0 + row;
-  const bool cvalid = c < a.Cout;
-  const float bias = (a.bias != nullptr && cvalid) ? a.bias[c] : 0.f;
-  const int nvalid = min(BN, a.HW - p0);
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  double sum = 0.0;
-  for (int j = 0; j < kChunks; ++j) {
-    uint32_t packed[32];
-#pragma unroll
-    for (int h = 0; h < kCols / 32; ++h) {
-      float v[32];
-      tmem_ld32(trow + j * kCols + h * 32, v);
-      // fp64 per element (as the BN statistics kernels): fp32 partial sums lose ~1e-6
-      // of a channel mean far from zero, which the reference's 1e-3 floor exposes in y
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float r = OutTraits<OutT>::round(v[i] + bias);
-        v[i] = r;
-        s4[i & 3] += (j * kCols + h * 32 + i < nvalid) ? (double)r : 0.0;
-      }
-      sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
-      if constexpr (sizeof(OutT) == 4) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-          packed[h * 16 + i] = *reinterpret_cast<uint32_t*>(&b2);
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+        const int mt = tile % a.mtiles, rest = tile / a.mtiles;
+        const int p0 = (rest % a.tilesP) * BN, img = rest / a.tilesP;
+        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const uint32_t s = it % S;
+          if (it >= (uint32_t)S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          uint8_t* A = ring + s * kStage;
+          uint8_t* B = A + kTileA;
+          mbar_expect_tx(&full[s], kStage);
+          tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
+          tma_load_3d(B, &tmX, &full[s], p0, kb * BK, img);
+          tma_load_3d(B + kTileB / 2, &tmX, &full[s], p0 + 64, kb * BK, img);
         }
       }
     }
-    // stage this thread's 128-byte row (128B swizzle: 16-byte chunk q -> q ^ (row & 7))
-    uint8_t* buf = stage_out + (j & 1) * kStageOut;
-    if (j >= 2) {
-      if (threadIdx.x == 0) bulk_wait_read1();
-      epi_bar();
-    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      uint32_t it = 0, li = 0;
+      for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++li) {
+        const uint32_t acc = li & 1;
+        if (li >= 2) mbar_wait(&tempty[acc], ((li >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const uint32_t s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          tc_fence_after();
+          const uint32_t A = smem_u32(ring + s * kStage);
+          const uint32_t B = A + kTileA;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      uint4 u = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-      *reinterpret_cast<uint4*>(buf + row * 128 + ((q ^ (row & 7)) << 4)) = u;
-    }
-    fence_proxy_async();
-    epi_bar();
-    if (threadIdx.x == 0) {
-      if (p0 + j * kCols < a.HW) tma_store_3d(&tmZ, buf, p0 + j * kCols, m0, img);
-      bulk_commit();  // (an empty group past the pixel tail keeps the group count uniform)
-    }
-  }
-
-  if (a.slots != nullptr) {
-    // second TMEM sweep: centred M2 of the stored values around the tile mean
-    const double mean = sum / (double)nvalid;
-    double q4[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = 0; j < BN / 32; ++j) {
-      if (j * 32 >= nvalid) break;
-      float v[32];
-      tmem_ld32(trow + j * 32, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const double d =
-            (j * 32 + i < nvalid) ? (double)OutTraits<OutT>::round(v[i] + bias) - mean : 0.0;
-        q4[i & 3] = fma(d, d, q4[i & 3]);
+          for (int k = 0; k < BK / 16; ++k) {
+            // A: K-major rows of 128 B, 8-row atoms 1024 B apart; K step = 32 B in the
+            //    row. B: MN-major, 64-pixel halves 8 KB apart (LBO), 8-channel groups
+            //    1 KB apart (SBO); K step = 16 rows = 2 KB.
+            const uint64_t ad = sdesc(A + k * 32, 16, 1024);
+            const uint64_t bd = sdesc(B + k * 2048, kTileB / 2, 1024);
+            mma_bf16(d, ad, bd, kIdesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[acc]);
       }
     }
-    const double m2 = (q4[0] + q4[1]) + (q4[2] + q4[3]);
-    if (cvalid) {
-      const int t = img * a.tilesP + pt;
-      a.slots[(size_t)t * a.Cout + c] = make_double2(mean, m2);
+    __syncwarp();
+  } else {
+    const int e = warp - 2;
+    const int sub = warp & 3, half = e >> 2;
+    const int row = sub * 32 + lane;
+    const int m0 = (blockIdx.x % a.mtiles) * BM;  // the same for every tile of this CTA
+    const int c = m0 + row;
+    const bool cvalid = c < a.Cout;
+    const bool active = m0 + sub * 32 < a.Cout;  // warp-uniform: any channel to write
+    const float bias = (a.bias != nullptr && cvalid) ? __ldg(a.bias + c) : 0.f;
+    uint8_t* wbuf = stage_out + e * 2 * kWarpStage;
+    float K = 0.f;
+    bool have_shift = false;
+    double N = 0.0, SD = 0.0, SQ = 0.0;
+    uint32_t li = 0, g = 0;
+    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++li) {
+      const int rest = tile / a.mtiles;
+      const int pt = rest % a.tilesP, img = rest / a.tilesP;
+      const int p0 = pt * BN + half * kHalf;
+      const int nvalid = max(0, min(kHalf, a.HW - p0));
+      const uint32_t acc = li & 1;
+      mbar_wait(&tfull[acc], (li >> 1) & 1);
+      tc_fence_after();
+      const uint32_t trow = tmem + acc * BN + half * kHalf + ((uint32_t)(sub * 32) << 16);
+      if (active && nvalid > 0) {
+        if (STATS && !have_shift) {
+          // the shift: fp32 mean of this first half-tile (TMEM pre-pass, once per thread)
+          float s1 = 0.f;
+          for (int j = 0; j < kHalf / 32; ++j) {
+            if (j * 32 >= nvalid) break;
+            float v[32];
+            tmem_ld32(trow + j * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = OutTraits<OutT>::round(v[i] + bias);
+            s1 += masked_tree32(v, nvalid - j * 32);
+          }
+          K = s1 / (float)nvalid;
+          have_shift = true;
+        }
+        for (int j = 0; j < kHalf / kCols; ++j, ++g) {
+          uint32_t packed[32];
+#pragma unroll
+          for (int h = 0; h < kCols / 32; ++h) {
+            float v[32];
+            tmem_ld32(trow + j * kCols + h * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = OutTraits<OutT>::round(v[i] + bias);
+            if constexpr (STATS) {
+              // SD exactly: fp64 sums of the fp32 values minus nv * K (an fp32 v - K is
+              // not exact when |v| and |K| differ, and for small channels that shows);
+              // SQ from fp32 d = v - K is only needed to relative precision
+              const int nv = max(0, min(32, nvalid - j * kCols - h * 32));
+              float q[32];
+              double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const bool ok = i < nv;
+                const float d = ok ? v[i] - K : 0.f;
+                q[i] = d * d;
+                s4[i & 3] += ok ? (double)v[i] : 0.0;
+              }
+              SD += ((s4[0] + s4[1]) + (s4[2] + s4[3])) - (double)nv * (double)K;
+              SQ += (double)masked_tree32(q, 32);
+            }
+            if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                packed[h * 16 + i] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+            }
+          }
+          // stage the row (128B swizzle: 16-byte chunk q -> q ^ (row & 7)); the slot's
+          // previous store must have finished reading it
+          uint8_t* buf = wbuf + (g & 1) * kWarpStage;
+          if (g >= 2) {
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint4 u = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
+                                 packed[4 * q + 3]);
+            *reinterpret_cast<uint4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (j * kCols < nvalid) tma_store_3d(&tmZ, buf, p0 + j * kCols, m0 + sub * 32, img);
+            bulk_commit();  // (an empty group past the pixel tail keeps the count uniform)
+          }
+        }
+        N += (double)nvalid;
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
     }
+    if constexpr (STATS) {
+      if (cvalid) {
+        const double dm = N > 0.0 ? SD / N : 0.0;
+        a.slots[(size_t)((blockIdx.x / a.mtiles) * 2 + half) * a.Cout + c] =
+            Slot{N, (double)K + dm, SQ - SD * dm};
+      }
+    }
+    if (lane == 0) bulk_wait_all();
   }
-
-  if (threadIdx.x == 0) bulk_wait_all();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, BN);
+  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
 }
 
-// Merge the per-tile (mean, M2) partials of each channel (Chan's update, fixed order:
-// warp w folds tiles w, w + 8, ...; the 8 warp partials are then folded in warp order)
-// into the rank's forward partial [mean (C) | M2 (C) | count]. Block = 32 channels x 8
-// warps; a warp reads 32 consecutive channels of one tile (512 contiguous bytes).
-__global__ void __launch_bounds__(256) k_conv_fold(const double2* __restrict__ slots, int Cout,
-                                                   int HW, int tilesP, int tiles,
-                                                   double* __restrict__ partial) {
-  __shared__ double sn[8][32], smean[8][32], sm2[8][32];
+// Slots -> this rank's forward partial [mean (C) | M2 (C) | count]. One block of 32
+// warps per 32 channels (lane = channel): warp w merges slots w, w + 32, ... against
+// one shift per channel, K0 = slot 0's mean (A = sum n_k (mean_k - K0), B = sum M2_k +
+// n_k (mean_k - K0)^2: additions only), the 32 warp sums are added in warp order, and
+// mean = K0 + A/n, M2 = B - A^2/n. Fixed order: bitwise reproducible. Slot s of channel
+// group mt exists when CTA (s / 2) * mtiles + mt ran.
+__global__ void __launch_bounds__(1024) k_conv_fold(const Slot* __restrict__ slots, int Cout,
+                                                    int mtiles, int grid, int nslots,
+                                                    double* __restrict__ partial) {
+  __shared__ double sn[32][32], sa[32][32], sb[32][32];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  double n = 0.0, mean = 0.0, M2 = 0.0;
+  const int mt = (blockIdx.x * 32) / BM;
+  double n = 0.0, A = 0.0, B = 0.0, K0 = 0.0;
   if (c < Cout) {
-    for (int t = w; t < tiles; t += 8) {
-      const double2 p = slots[(size_t)t * Cout + c];
-      const int pt = t % tilesP;
-      const double nb = (double)min(BN, HW - pt * BN);
-      const double nn = n + nb;
-      const double delta = p.x - mean;
-      mean = mean + delta * (nb / nn);
-      M2 = M2 + p.y + delta * delta * (n * nb / nn);
-      n = nn;
+    K0 = slots[c].mean;
+    for (int s = w; s < nslots; s += 32) {
+      if ((s >> 1) * mtiles + mt >= grid) break;
+      const Slot p = slots[(size_t)s * Cout + c];
+      if (p.n == 0.0) continue;
+      const double d = p.mean - K0;
+      n += p.n;
+      A = fma(p.n, d, A);
+      B += fma(p.n * d, d, p.M2);
     }
   }
   sn[w][lane] = n;
-  smean[w][lane] = mean;
-  sm2[w][lane] = M2;
+  sa[w][lane] = A;
+  sb[w][lane] = B;
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (w == 0 && c < Cout) {
-    n = sn[0][lane];
-    mean = smean[0][lane];
-    M2 = sm2[0][lane];
-    for (int r = 1; r < 8; ++r) {
-      const double nb = sn[r][lane];
-      if (nb == 0.0) continue;
-      const double nn = n + nb;
-      const double delta = smean[r][lane] - mean;
-      mean = mean + delta * (nb / nn);
-      M2 = M2 + sm2[r][lane] + delta * delta * (n * nb / nn);
-      n = nn;
+    for (int r = 1; r < 32; ++r) {
+      n += sn[r][lane];
+      A += sa[r][lane];
+      B += sb[r][lane];
     }
-    partial[c] = mean;
-    partial[Cout + c] = M2;
+    partial[c] = K0 + A / n;
+    partial[Cout + c] = B - A * A / n;
     if (c == 0) partial[2 * Cout] = n;
   }
 }
@@ -450,13 +533,46 @@ int make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
   return CGBN_OK;
 }
 
-constexpr int kStages = 2;
+constexpr int kStages = 4;
 
-size_t conv_smem_bytes() { return 1024 + kStages * kStage + 2 * kStageOut + 8 * (2 * kStages + 1) + 16; }
+size_t conv_smem_bytes() {
+  return 1024 + kStages * kStage + kEpiWarps * 2 * kWarpStage + 8 * (2 * kStages + 4) + 16;
+}
+
+int num_sms() {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (sms[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
+  }
+  return sms[dev];
+}
+
+// Conv grid: one CTA per SM, rounded down to a multiple of the channel tiles (so a CTA's
+// tiles share their channels), at most one CTA per tile.
+int conv_grid(int64_t tiles, int mtiles) {
+  const int sms = num_sms();
+  int64_t g = mtiles <= sms ? (int64_t)(sms / mtiles) * mtiles : mtiles;
+  return (int)std::min<int64_t>(g, tiles);
+}
+
+int64_t conv_tiles(int64_t N, int64_t Cout, int64_t HW) {
+  return ((Cout + BM - 1) / BM) * ((HW + BN - 1) / BN) * N;
+}
+
+int conv_nslots(int64_t N, int64_t Cout, int64_t HW) {
+  const int mtiles = (int)((Cout + BM - 1) / BM);
+  const int grid = conv_grid(conv_tiles(N, Cout, HW), mtiles);
+  return 2 * ((grid + mtiles - 1) / mtiles);
+}
 
 template <class OutT>
 int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                int64_t Cout, int64_t HW, void* z, double2* slots, cudaStream_t st) {
+                int64_t Cout, int64_t HW, void* z, Slot* slots, cudaStream_t st) {
   CUtensorMap tmW, tmX, tmZ;
   {
     const cuuint64_t dims[2] = {(cuuint64_t)Cin, (cuuint64_t)Cout};
@@ -474,7 +590,7 @@ int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int6
     constexpr int sz = sizeof(OutT);
     const cuuint64_t dims[3] = {(cuuint64_t)HW, (cuuint64_t)Cout, (cuuint64_t)N};
     const cuuint64_t strides[2] = {(cuuint64_t)HW * sz, (cuuint64_t)(Cout * HW * sz)};
-    const cuuint32_t box[3] = {(cuuint32_t)OutTraits<OutT>::kCols, BM, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)OutTraits<OutT>::kCols, 32, 1};
     const CUtensorMapDataType dt =
         sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     if (int rc = make_map(&tmZ, dt, 3, z, dims, strides, box)) return rc;
@@ -487,10 +603,11 @@ int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int6
   a.tilesP = (int)((HW + BN - 1) / BN);
   a.mtiles = (int)((Cout + BM - 1) / BM);
   a.kblocks = (int)((Cin + BK - 1) / BK);
+  a.tiles = (int)conv_tiles(N, Cout, HW);
   const size_t smem = conv_smem_bytes();
-  auto kern = k_conv1x1<kStages, OutT>;
+  auto kern = slots ? k_conv1x1<kStages, OutT, true> : k_conv1x1<kStages, OutT, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const long long grid = (long long)a.mtiles * a.tilesP * N;
+  const long long grid = conv_grid(a.tiles, a.mtiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kConvThreads);
@@ -518,14 +635,13 @@ int validate(const void* x, const void* w, const void* z, int64_t N, int64_t Cin
                 (long long)HW);
   if (Cin % 8 != 0)
     return fail(CGBN_ERR_UNSUPPORTED, "conv1x1: Cin=%lld must be a multiple of 8", (long long)Cin);
-  if (Cout > 65535 || N > 65535 || HW * N > (1ll << 31))
+  if (Cout > 65535 || N > 65535 || HW * N > (1ll << 31) ||
+      (int64_t)((Cout + BM - 1) / BM) * ((HW + BN - 1) / BN) * N > (1ll << 30))
     return fail(CGBN_ERR_INVALID, "conv1x1: extents too large");
   if (((uintptr_t)x | (uintptr_t)w | (uintptr_t)z) & 15)
     return fail(CGBN_ERR_INVALID, "conv1x1: pointers must be 16-byte aligned");
   return CGBN_OK;
 }
-
-int tiles_per_channel(int64_t N, int64_t HW) { return (int)(N * ((HW + BN - 1) / BN)); }
 
 }  // namespace
 
@@ -533,7 +649,7 @@ extern "C" {
 
 size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW) {
   if (N <= 0 || Cout <= 0 || HW <= 0) return 0;
-  return (size_t)tiles_per_channel(N, HW) * (size_t)Cout * sizeof(double2);
+  return (size_t)conv_nslots(N, Cout, HW) * (size_t)Cout * sizeof(Slot);
 }
 
 int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
@@ -557,23 +673,24 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
                 (long long)need, (long long)ws_bytes);
   if ((uintptr_t)ws & 15) return fail(CGBN_ERR_INVALID, "conv1x1_stats: workspace must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  double2* slots = (double2*)ws;
+  Slot* slots = (Slot*)ws;
   int rc = out_dtype == CGBN_ACT_F32
                ? launch_conv<float>(x, w, bias, N, Cin, Cout, HW, z, slots, st)
                : launch_conv<__nv_bfloat16>(x, w, bias, N, Cin, Cout, HW, z, slots, st);
   if (rc) return rc;
-  const int tilesP = (int)((HW + BN - 1) / BN);
+  const int mtiles = (int)((Cout + BM - 1) / BM);
+  const int grid = conv_grid(conv_tiles(N, Cout, HW), mtiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((Cout + 31) / 32));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(1024);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = getenv("CGBN_NO_PDL") ? 0 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_conv_fold, (const double2*)slots, (int)Cout, (int)HW,
-                                     tilesP, tiles_per_channel(N, HW), partial);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_conv_fold, (const Slot*)slots, (int)Cout, mtiles,
+                                     grid, conv_nslots(N, Cout, HW), partial);
   if (e != cudaSuccess) return fail(CGBN_ERR_CUDA, "conv fold launch failed: %s", cudaGetErrorString(e));
   return CGBN_OK;
 }
