@@ -248,9 +248,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 //                 same registers feed the channel statistics.
 // Statistics (STATS): the shifted sums of the stored values, d = z - K with one shift K
 // per thread (the fp32 mean of its first half-tile, from a TMEM pre-pass on that tile
-// only): N, SD = sum d (fp64 per element), SQ = sum d^2 (fp32 pairwise per 32 values,
-// fp64 above). |d| is of the order of the channel's spread whatever its mean, so
-// mean = K + SD/N and M2 = SQ - SD^2/N keep the BN tolerances also for |mean| >> std.
+// only): N, SD = sum d, SQ = sum d^2, fp64 per element (d is exact in fp64). |d| is of
+// the order of the channel's spread whatever its mean, so mean = K + SD/N and
+// M2 = SQ - SD^2/N keep the BN tolerances also for |mean| >> std.
 // Each (CTA, half) writes one Slot per channel; k_conv_fold merges the slots.
 template <int S, class OutT, bool STATS>
 __global__ void __launch_bounds__(kConvThreads, 1)
@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int c = m0 + row;
     const bool cvalid = c < a.Cout;
     const bool active = m0 + sub * 32 < a.Cout;  // warp-uniform: any channel to write
-    const float bias = (a.bias != nullptr && cvalid) ? __ldg(a.bias + c) : 0.f;
+    const bool has_bias = a.bias != nullptr;
+    const float bias = (has_bias && cvalid) ? __ldg(a.bias + c) : 0.f;
     uint8_t* wbuf = stage_out + e * 2 * kWarpStage;
     float K = 0.f;
     bool have_shift = false;
@@ -383,24 +384,38 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int h = 0; h < kCols / 32; ++h) {
             float v[32];
             tmem_ld32(trow + j * kCols + h * 32, v);
+            if (has_bias) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = OutTraits<OutT>::round(v[i] + bias);
+              for (int i = 0; i < 32; ++i) v[i] += bias;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = OutTraits<OutT>::round(v[i]);
             if constexpr (STATS) {
-              // SD exactly: fp64 sums of the fp32 values minus nv * K (an fp32 v - K is
-              // not exact when |v| and |K| differ, and for small channels that shows);
-              // SQ from fp32 d = v - K is only needed to relative precision
+              // d = z - K exactly in fp64 (both fp32), SD = sum d and SQ = sum d^2 in fp64
+              // per element, as in the BN statistics kernels: the reference's 1e-3-floor
+              // comparison of y needs var to ~1e-9, beyond fp32 sums of squares
               const int nv = max(0, min(32, nvalid - j * kCols - h * 32));
-              float q[32];
-              double s4[4] = {0.0, 0.0, 0.0, 0.0};
+              const double Kd = (double)K;
+              double s8[8], q8[8];  // 8 independent chains (fp64 latency)
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const bool ok = i < nv;
-                const float d = ok ? v[i] - K : 0.f;
-                q[i] = d * d;
-                s4[i & 3] += ok ? (double)v[i] : 0.0;
+              for (int i = 0; i < 8; ++i) s8[i] = q8[i] = 0.0;
+              if (nv == 32) {  // every chunk but the pixel tail: no masking
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const double d = (double)v[i] - Kd;
+                  s8[i & 7] += d;
+                  q8[i & 7] = fma(d, d, q8[i & 7]);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const double d = i < nv ? (double)v[i] - Kd : 0.0;
+                  s8[i & 7] += d;
+                  q8[i & 7] = fma(d, d, q8[i & 7]);
+                }
               }
-              SD += ((s4[0] + s4[1]) + (s4[2] + s4[3])) - (double)nv * (double)K;
-              SQ += (double)masked_tree32(q, 32);
+              SD += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+              SQ += ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
             }
             if constexpr (sizeof(OutT) == 4) {
 #pragma unroll
@@ -459,6 +474,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // n_k (mean_k - K0)^2: additions only), the 32 warp sums are added in warp order, and
 // mean = K0 + A/n, M2 = B - A^2/n. Fixed order: bitwise reproducible. Slot s of channel
 // group mt exists when CTA (s / 2) * mtiles + mt ran.
+constexpr int kFoldPerWarp = 10;  // slots per channel <= 2 * 148 CTAs <= 32 warps x 10
+
 __global__ void __launch_bounds__(1024) k_conv_fold(const Slot* __restrict__ slots, int Cout,
                                                     int mtiles, int grid, int nslots,
                                                     double* __restrict__ partial) {
@@ -469,15 +486,22 @@ __global__ void __launch_bounds__(1024) k_conv_fold(const Slot* __restrict__ slo
   const int mt = (blockIdx.x * 32) / BM;
   double n = 0.0, A = 0.0, B = 0.0, K0 = 0.0;
   if (c < Cout) {
+    // every load of this warp in flight at once (nslots <= 32 * kFoldPerWarp)
+    Slot p[kFoldPerWarp];
+#pragma unroll
+    for (int u = 0; u < kFoldPerWarp; ++u) {
+      const int s = w + 32 * u;
+      const bool ok = s < nslots && (s >> 1) * mtiles + mt < grid;
+      p[u] = ok ? slots[(size_t)s * Cout + c] : Slot{0.0, 0.0, 0.0};
+    }
     K0 = slots[c].mean;
-    for (int s = w; s < nslots; s += 32) {
-      if ((s >> 1) * mtiles + mt >= grid) break;
-      const Slot p = slots[(size_t)s * Cout + c];
-      if (p.n == 0.0) continue;
-      const double d = p.mean - K0;
-      n += p.n;
-      A = fma(p.n, d, A);
-      B += fma(p.n * d, d, p.M2);
+#pragma unroll
+    for (int u = 0; u < kFoldPerWarp; ++u) {
+      if (p[u].n == 0.0) continue;
+      const double d = p[u].mean - K0;
+      n += p[u].n;
+      A = fma(p[u].n, d, A);
+      B += fma(p[u].n * d, d, p[u].M2);
     }
   }
   sn[w][lane] = n;
@@ -673,6 +697,9 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
                 (long long)need, (long long)ws_bytes);
   if ((uintptr_t)ws & 15) return fail(CGBN_ERR_INVALID, "conv1x1_stats: workspace must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
+  if (conv_nslots(N, Cout, HW) > 32 * kFoldPerWarp)
+    return fail(CGBN_ERR_UNSUPPORTED, "conv1x1_stats: more than %d statistics slots per channel",
+                32 * kFoldPerWarp);
   Slot* slots = (Slot*)ws;
   int rc = out_dtype == CGBN_ACT_F32
                ? launch_conv<float>(x, w, bias, N, Cin, Cout, HW, z, slots, st)

@@ -6,12 +6,10 @@ Checks, through the C ABI:
     accumulate in fp32, so the error of an element is relative to the size of the
     products it sums, not to its own value: normwise max|z - ref| / max|ref| <= 1e-5 for
     fp32 z, plus one bf16 rounding (8e-3) for bf16 z;
-  * the fused partial against the oracle's statistics of z *as stored* (f64). The
-    epilogue uses the corrected two-pass algorithm with fp32 pairwise sums of
-    d = z - (pass-1 mean) per 32 values and fp64 above, so the bounds are relative to
-    the channel's spread: |mean error| <= 1e-8 std, M2 relative error <= 1e-6 — far
-    inside what the BN tolerances below need — also with a channel offset of 1000
-    (|mean| >> std);
+  * the fused partial against the oracle's statistics of z *as stored* (f64): the
+    epilogue accumulates the shifted sums of d = z - K in fp64 per element (d exact),
+    so |mean error| <= 1e-12 std and the M2 relative error <= 1e-12, also with a channel
+    offset of 1000 (|mean| >> std);
   * the fused BN forward against the oracle on z (the reference's tolerances: 1e-5 on
     mean / var / y / running stats) for a single rank and a 4-rank group, and the
     backward through the resulting cache (1e-4 on dx / dgamma / dbeta);
@@ -46,8 +44,8 @@ def _operands(n, cin, cout, hw, seed, loc=0.0, bias=False, bias_loc=0.0):
 def _check_partial(p, mean, m2, cnt, cout):
     assert p[2 * cout] == cnt
     std = np.sqrt(m2 / cnt)
-    assert np.max(np.abs(p[:cout] - mean) / std) <= 1e-8
-    assert np.max(np.abs(p[cout:2 * cout] - m2) / m2) <= 1e-6
+    assert np.max(np.abs(p[:cout] - mean) / std) <= 1e-12
+    assert np.max(np.abs(p[cout:2 * cout] - m2) / m2) <= 1e-12
 
 
 def _z_ref(x, wt, b):
@@ -164,7 +162,7 @@ def test_fused_equals_unfused_forward():
     y1, c1, z = P.conv1x1_bn_forward_local(x.to(DEV), wt.to(DEV), st1)
     y2, c2 = cg.bn_forward_local(z, st2)
     assert O.rel_err(y1.double().cpu().numpy(), y2.double().cpu().numpy()) <= 1e-5
-    assert O.rel_err(c1.var.cpu().numpy(), c2.var.cpu().numpy()) <= 1e-6
+    assert O.rel_err(c1.var.cpu().numpy(), c2.var.cpu().numpy()) <= 1e-12
     assert O.rel_err(st1.running_var.double().cpu().numpy(),
                      st2.running_var.double().cpu().numpy()) <= 1e-6
 
