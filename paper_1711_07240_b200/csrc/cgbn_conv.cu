@@ -53,7 +53,7 @@ constexpr int BN = 128;       // pixels per tile (TMEM columns)
 constexpr int BK = 64;        // input channels per ring stage (128 B of bf16)
 constexpr int kEpiWarps = 8;
 constexpr int kHalf = 64;                       // tile columns per epilogue warp
-constexpr uint32_t kWarpStage = 32 * 128;       // one warp's staged rows: 4 KB
+constexpr uint32_t kWarpStage = 32 * 128;       // one staged box (32 rows x 128 B): 4 KB
 constexpr int kConvThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilogue warps
 constexpr uint32_t kTileA = BM * BK * 2;      // 16 KB
 constexpr uint32_t kTileB = BK * BN * 2;      // 16 KB (two 64-pixel boxes of 8 KB)
@@ -118,6 +118,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -172,6 +175,30 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 64 consecutive fp32 columns: two 32-column loads in flight, one wait.
+__device__ __forceinline__ void tmem_ld32x2(uint32_t taddr, float (&v)[64]) {
+  uint32_t r[64];
+#define CGBN_LD32(o, base)                                                                        \
+  asm volatile(                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "     \
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "     \
+      "%28, %29, %30, %31}, [%32];"                                                               \
+      : "=r"(r[o + 0]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]),            \
+        "=r"(r[o + 5]), "=r"(r[o + 6]), "=r"(r[o + 7]), "=r"(r[o + 8]), "=r"(r[o + 9]),            \
+        "=r"(r[o + 10]), "=r"(r[o + 11]), "=r"(r[o + 12]), "=r"(r[o + 13]), "=r"(r[o + 14]),       \
+        "=r"(r[o + 15]), "=r"(r[o + 16]), "=r"(r[o + 17]), "=r"(r[o + 18]), "=r"(r[o + 19]),       \
+        "=r"(r[o + 20]), "=r"(r[o + 21]), "=r"(r[o + 22]), "=r"(r[o + 23]), "=r"(r[o + 24]),       \
+        "=r"(r[o + 25]), "=r"(r[o + 26]), "=r"(r[o + 27]), "=r"(r[o + 28]), "=r"(r[o + 29]),       \
+        "=r"(r[o + 30]), "=r"(r[o + 31])                                                           \
+      : "r"(base))
+  CGBN_LD32(0, taddr);
+  CGBN_LD32(32, taddr + 32);
+#undef CGBN_LD32
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // Shared-memory matrix descriptor (tcgen05): start >> 4 in [0,14), leading byte offset
@@ -257,6 +284,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1x1(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmZ, const ConvArgs a) {
   constexpr int kCols = OutTraits<OutT>::kCols;
+  constexpr int kBoxes = kHalf / kCols;  // staged 128-byte boxes per half-row
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* ring = smem;                        // S x [A 16 KB | B 16 KB]
@@ -364,90 +392,91 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc_fence_after();
       const uint32_t trow = tmem + acc * BN + half * kHalf + ((uint32_t)(sub * 32) << 16);
       if (active && nvalid > 0) {
-        if (STATS && !have_shift) {
-          // the shift: fp32 mean of this first half-tile (TMEM pre-pass, once per thread)
-          float s1 = 0.f;
-          for (int j = 0; j < kHalf / 32; ++j) {
-            if (j * 32 >= nvalid) break;
-            float v[32];
-            tmem_ld32(trow + j * 32, v);
+        // the half-row's 64 values: both TMEM loads in flight, one wait
+        float v[64];
+        tmem_ld32x2(trow, v);
+        if (has_bias) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = OutTraits<OutT>::round(v[i] + bias);
-            s1 += masked_tree32(v, nvalid - j * 32);
-          }
-          K = s1 / (float)nvalid;
-          have_shift = true;
+          for (int i = 0; i < 64; ++i) v[i] += bias;
         }
-        for (int j = 0; j < kHalf / kCols; ++j, ++g) {
-          uint32_t packed[32];
 #pragma unroll
-          for (int h = 0; h < kCols / 32; ++h) {
-            float v[32];
-            tmem_ld32(trow + j * kCols + h * 32, v);
-            if (has_bias) {
+        for (int i = 0; i < 64; ++i) v[i] = OutTraits<OutT>::round(v[i]);
+        if constexpr (STATS) {
+          if (!have_shift) {  // the shift: fp32 mean of this thread's first half-tile
+            float t[64];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += bias;
+            for (int i = 0; i < 64; ++i) t[i] = i < nvalid ? v[i] : 0.f;
+#pragma unroll
+            for (int w2 = 32; w2 > 0; w2 >>= 1)
+#pragma unroll
+              for (int i = 0; i < w2; ++i) t[i] += t[i + w2];
+            K = t[0] / (float)nvalid;
+            have_shift = true;
+          }
+          // d = z - K exactly in fp64 (both fp32), SD = sum d and SQ = sum d^2 in fp64 per
+          // element, as in the BN statistics kernels: the reference's 1e-3-floor
+          // comparison of y needs var to ~1e-9, beyond fp32 sums of squares
+          const double Kd = (double)K;
+          double s8[8], q8[8];  // 8 independent chains (fp64 latency)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) s8[i] = q8[i] = 0.0;
+          if (nvalid == kHalf) {  // every half-tile but the pixel tail: no masking
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+              const double d = (double)v[i] - Kd;
+              s8[i & 7] += d;
+              q8[i & 7] = fma(d, d, q8[i & 7]);
             }
+          } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = OutTraits<OutT>::round(v[i]);
-            if constexpr (STATS) {
-              // d = z - K exactly in fp64 (both fp32), SD = sum d and SQ = sum d^2 in fp64
-              // per element, as in the BN statistics kernels: the reference's 1e-3-floor
-              // comparison of y needs var to ~1e-9, beyond fp32 sums of squares
-              const int nv = max(0, min(32, nvalid - j * kCols - h * 32));
-              const double Kd = (double)K;
-              double s8[8], q8[8];  // 8 independent chains (fp64 latency)
-#pragma unroll
-              for (int i = 0; i < 8; ++i) s8[i] = q8[i] = 0.0;
-              if (nv == 32) {  // every chunk but the pixel tail: no masking
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const double d = (double)v[i] - Kd;
-                  s8[i & 7] += d;
-                  q8[i & 7] = fma(d, d, q8[i & 7]);
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const double d = i < nv ? (double)v[i] - Kd : 0.0;
-                  s8[i & 7] += d;
-                  q8[i & 7] = fma(d, d, q8[i & 7]);
-                }
-              }
-              SD += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-              SQ += ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
-            }
-            if constexpr (sizeof(OutT) == 4) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-                packed[h * 16 + i] = *reinterpret_cast<uint32_t*>(&b2);
-              }
+            for (int i = 0; i < 64; ++i) {
+              const double d = i < nvalid ? (double)v[i] - Kd : 0.0;
+              s8[i & 7] += d;
+              q8[i & 7] = fma(d, d, q8[i & 7]);
             }
           }
-          // stage the row (128B swizzle: 16-byte chunk q -> q ^ (row & 7)); the slot's
-          // previous store must have finished reading it
-          uint8_t* buf = wbuf + (g & 1) * kWarpStage;
-          if (g >= 2) {
-            if (lane == 0) bulk_wait_read1();
-            __syncwarp();
-          }
+          SD += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+          SQ += ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
+        }
+        // stage the half-row as 128-byte rows (fp32: 2 boxes of 32 columns; bf16: 1 box of
+        // 64), 128B swizzle: 16-byte chunk q of row r at q ^ (r & 7); the previous tile's
+        // stores must have finished reading the warp's buffer
+        if (g > 0) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int bx = 0; bx < kBoxes; ++bx) {
+          uint8_t* buf = wbuf + bx * kWarpStage;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            uint4 u = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
-                                 packed[4 * q + 3]);
+            uint4 u;
+            if constexpr (sizeof(OutT) == 4) {
+              const float* f = v + bx * 32 + 4 * q;
+              u = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                             __float_as_uint(f[3]));
+            } else {
+              uint32_t w4[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+                w4[k] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              u = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
             *reinterpret_cast<uint4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
           }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            if (j * kCols < nvalid) tma_store_3d(&tmZ, buf, p0 + j * kCols, m0 + sub * 32, img);
-            bulk_commit();  // (an empty group past the pixel tail keeps the count uniform)
-          }
         }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int bx = 0; bx < kBoxes; ++bx)
+            if (bx * kCols < nvalid)
+              tma_store_3d(&tmZ, wbuf + bx * kWarpStage, p0 + bx * kCols, m0 + sub * 32, img);
+          bulk_commit();
+        }
+        ++g;
         N += (double)nvalid;
       }
       tc_fence_before();
