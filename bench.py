@@ -413,6 +413,80 @@ def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
                  f"reduction; CUDA events on the replay stream, mean of {reps} replays")
 
 
+# SURVEY 8(f) row 4 (producer fusion): the ResNet-50 1x1-conv -> BN layers of stages 1-2
+# (H*W a multiple of 8), batch 32: (Cin, Cout, H, W, occurrences in the network)
+PRODUCER_LAYERS = [(64, 64, 56, 56, 1), (256, 64, 56, 56, 2), (64, 256, 56, 56, 4),
+                   (256, 128, 56, 56, 1), (512, 128, 28, 28, 3), (128, 512, 28, 28, 4)]
+
+
+def producer_profile(cg, torch, dev, hbm_peak, batch=32, sets=3, iters=10):
+    """Producer fusion on the tcgen05 1x1 conv: fused (conv epilogue emits the BN partial,
+    then normalise) vs split (conv, then the BN forward re-reads z for its statistics),
+    fp32 z, CUDA-graph timed with `sets` rotating buffer sets (no L2 reuse between
+    launches). Totals are weighted by the layers' occurrences in ResNet-50."""
+    from paper_1711_07240_b200 import producer as P
+
+    def timed(fn):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                fn()
+            g.replay()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(iters):
+                g.replay()
+            e1.record(s)
+            e1.synchronize()
+        return e0.elapsed_time(e1) / iters / sets * 1e3  # us per layer
+
+    tot = {"fused_us": 0.0, "split_us": 0.0, "conv_us": 0.0, "conv_bytes": 0}
+    layers = []
+    for cin, cout, h, w, cnt in PRODUCER_LAYERS:
+        xs = [torch.randn(batch, cin, h, w, device=dev).to(torch.bfloat16) for _ in range(sets)]
+        wt = (torch.randn(cout, cin, device=dev) / cin ** 0.5).to(torch.bfloat16)
+        sts = [cg.BNLayerState.create(cout, device=dev) for _ in range(sets)]
+
+        def conv():
+            for x in xs:
+                P.conv1x1(x, wt)
+
+        def fused():
+            for x, st in zip(xs, sts):
+                P.conv1x1_bn_forward_local(x, wt, st)
+
+        def split():
+            for x, st in zip(xs, sts):
+                cg.bn_forward_local(P.conv1x1(x, wt), st)
+
+        t_conv, t_f, t_s = timed(conv), timed(fused), timed(split)
+        cb = batch * h * w * (2 * cin + 4 * cout) + 2 * cin * cout
+        layers.append({"shape": [batch, cin, cout, h, w], "count": cnt, "conv_us": t_conv,
+                       "conv_hbm_frac": cb / t_conv / 1e3 / hbm_peak,
+                       "fused_fwd_us": t_f, "split_fwd_us": t_s})
+        tot["fused_us"] += cnt * t_f
+        tot["split_us"] += cnt * t_s
+        tot["conv_us"] += cnt * t_conv
+        tot["conv_bytes"] += cnt * cb
+        del xs, sts
+    return {
+        "what": "1x1 conv (tcgen05, bf16 x/w, fp32 z) + BN forward; fused = conv epilogue "
+                "emits the BN partial (no statistics read of z), split = conv then the BN "
+                "forward's statistics kernel re-reads z",
+        "layers": "ResNet-50 stage 1-2 1x1-conv->BN layers, batch 32, weighted by count",
+        "fused_fwd_ms": tot["fused_us"] / 1e3, "split_fwd_ms": tot["split_us"] / 1e3,
+        "speedup": tot["split_us"] / tot["fused_us"],
+        "conv_gbs": tot["conv_bytes"] / tot["conv_us"] / 1e3,
+        "conv_hbm_frac": tot["conv_bytes"] / tot["conv_us"] / 1e3 / hbm_peak,
+        "per_layer": layers,
+    }
+
+
 def select_transport(cg, torch, dist, dev, world, requested, barrier):
     """Statistics transport for N>1: NCCL all-gather, or the one-shot P2P exchange when it
     passes a self-test against NCCL (bitwise-equal rows, no timeout) and -- for "auto" --
@@ -748,6 +822,13 @@ def run_gpu_arm(args):
                           f" via DeviceGroup(1); {res['seconds']:.1f} s"),
                **host_cpu_info()}
 
+    producer = None
+    if rank == 0 and world == 1 and not args.no_producer:
+        try:
+            producer = producer_profile(cg, torch, dev, hbm_peak)
+        except Exception as exc:  # report, never fail the bench line
+            producer = {"error": f"{type(exc).__name__}: {exc}"}
+
     barrier()
     if rank == 0:
         line = {
@@ -783,6 +864,7 @@ def run_gpu_arm(args):
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "producer_fusion": producer,
         }
         print(json.dumps(line))
     if world > 1:
@@ -813,6 +895,8 @@ def main():
     ap.add_argument("--no-kprof", action="store_true", help="skip the per-kernel profile")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-producer", action="store_true",
+                    help="skip the producer-fusion (conv epilogue statistics) measurement")
     ap.add_argument("--ref-procs", type=int, default=None,
                     help="reference arm worker processes (default: one per allowed core)")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
