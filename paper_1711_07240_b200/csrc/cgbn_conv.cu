@@ -11,24 +11,13 @@
 // epilogue reduces each output channel of its tile to (mean, centred M2) of the values
 // *as stored* — the partial cgbn_fwd_stats would have computed from z.
 //
-// Kernel anatomy (one CTA per 128-channel x 128-pixel output tile of one image, 128
-// threads, 2 CTAs per SM so one tile's epilogue overlaps the other's loads):
-//   warp 0 / lane 0   TMA producer: W tile [128 co][64 ci] (K-major, 128B swizzle) and
-//                     x tile [64 ci][128 px] (two 64-pixel boxes, MN-major, 128B swizzle)
-//                     into an S-stage ring, mbarrier complete_tx;
-//   warp 1 / lane 0   MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 N=128 K=16,
-//                     accumulator in 128 TMEM columns; tcgen05.commit frees ring slots
-//                     and finally signals the epilogue;
-//   warps 0-3         epilogue: tcgen05.ld 32x32b (thread t owns TMEM lane t = output
-//                     channel m0+t, so each thread reduces its own channel with no
-//                     cross-thread traffic), + bias, round to the output type, stage
-//                     128-byte rows in 128B-swizzled shared memory and TMA-store them
-//                     (clipping the pixel / channel tails); a second TMEM sweep forms the
-//                     tile's centred M2 around the tile mean.
-// Tile partials (mean, M2) go to a tile-major slot array; k_conv_fold merges the tiles
-// of each channel with Chan's update in a fixed order into this rank's forward partial
-// [mean (C) | M2 (C) | count] (include/cgbn.h), which the unchanged exchange and
-// cgbn_fwd_normalize consume.
+// Kernel (k_conv1x1, described at its definition): persistent and warp-specialised — a
+// TMA producer warp, a single-lane tcgen05.mma issuer with two TMEM accumulators, and
+// eight epilogue warps that each own 32 output channels x 64 pixels of a tile, store z
+// with TMA and accumulate their channel's shifted sums in fp64. Each (CTA, tile half)
+// leaves one statistics slot per channel; k_conv_fold merges the slots into this rank's
+// forward partial [mean (C) | M2 (C) | count] (include/cgbn.h), which the unchanged
+// exchange and cgbn_fwd_normalize consume.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -575,14 +564,16 @@ EncodeFn encode_fn() {
 // rank-r tensor map with 128-byte swizzle; dims / strides innermost first (strides in
 // bytes, for dims 1..r-1).
 int make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
-             const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+             const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+             const char* which) {
   EncodeFn fn = encode_fn();
   if (!fn) return fail(CGBN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
-  cuuint32_t es[3] = {1, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};  // one per dimension (rank <= 5)
   CUresult r = fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(CGBN_ERR_INVALID, "tensor map encoding failed (CUresult %d)", (int)r);
+  if (r != CUDA_SUCCESS)
+    return fail(CGBN_ERR_INVALID, "tensor map encoding failed for %s (CUresult %d)", which, (int)r);
   return CGBN_OK;
 }
 
@@ -631,13 +622,13 @@ int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int6
     const cuuint64_t dims[2] = {(cuuint64_t)Cin, (cuuint64_t)Cout};
     const cuuint64_t strides[1] = {(cuuint64_t)Cin * 2};
     const cuuint32_t box[2] = {BK, BM};
-    if (int rc = make_map(&tmW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, strides, box)) return rc;
+    if (int rc = make_map(&tmW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, strides, box, "w")) return rc;
   }
   {
     const cuuint64_t dims[3] = {(cuuint64_t)HW, (cuuint64_t)Cin, (cuuint64_t)N};
     const cuuint64_t strides[2] = {(cuuint64_t)HW * 2, (cuuint64_t)(Cin * HW * 2)};
     const cuuint32_t box[3] = {64, BK, 1};
-    if (int rc = make_map(&tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, x, dims, strides, box)) return rc;
+    if (int rc = make_map(&tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, x, dims, strides, box, "x")) return rc;
   }
   {
     constexpr int sz = sizeof(OutT);
@@ -646,7 +637,7 @@ int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int6
     const cuuint32_t box[3] = {(cuuint32_t)OutTraits<OutT>::kCols, 32, 1};
     const CUtensorMapDataType dt =
         sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    if (int rc = make_map(&tmZ, dt, 3, z, dims, strides, box)) return rc;
+    if (int rc = make_map(&tmZ, dt, 3, z, dims, strides, box, "z")) return rc;
   }
   ConvArgs a;
   a.bias = bias;
