@@ -279,6 +279,22 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
                        int64_t Cout, int64_t HW, int out_dtype, void* z, double* partial,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* The producer on channels-last activations (x, z NHWC = [N][H][W][C], the layout
+ * detector training uses and the BN's native NHWC kernels read), ksize 1 or 3 (stride 1,
+ * zero padding 1 for 3x3: the reference model's conv layer, model.py:235-242). The 3x3
+ * case is an implicit GEMM on TMA im2col loads (9 taps x Cin/64 k-steps; the hardware
+ * shifts each 128-pixel window by the tap and zero-fills outside the image), so any H
+ * and W work. w: bf16 [Cout][Cin] (ksize 1) or [9][Cout][Cin] with tap = 3 * ky + kx
+ * (the reference's (Cout, Cin, 3, 3) weight permuted). Cin and Cout must be multiples of
+ * 8. Statistics contract as cgbn_conv1x1_stats; ws: cgbn_conv_nhwc_ws_bytes bytes. */
+size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W);
+int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                   int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
+                   void* stream);
+int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                         int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
+                         double* partial, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,24 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
       "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const void* src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tm),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+// im2col-mode load (NHWC): 128 output pixels x 64 channels starting at input coordinate
+// {c, w, h, n}; the filter-tap offsets (ow, oh) shift every pixel's window, and pixels
+// outside the image read as zero.
+__device__ __forceinline__ void tma_load_im2col_4d(void* dst, const CUtensorMap* tm,
+                                                   uint64_t* bar, int c, int w, int h, int n,
+                                                   uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const void* src, int c0,
                                              int c1, int c2) {
   asm volatile(
@@ -199,8 +217,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, A K-major, B MN-major, N, M.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
-                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, A K-major, B MN-major (NCHW x:
+// pixels contiguous) or K-major (NHWC x: channels contiguous), N, M.
+constexpr uint32_t kIdescBase = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) |
+                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr uint32_t kIdesc = kIdescBase | (1u << 16);
+constexpr uint32_t kIdescKB = kIdescBase;
+
+// Layout / geometry modes of the conv kernel
+constexpr int kNCHW1 = 0;  // NCHW x and z, 1x1: pixel tiles within one image
+constexpr int kNHWC1 = 1;  // NHWC x and z, 1x1: pixel tiles of the flattened N*H*W
+constexpr int kNHWC3 = 2;  // NHWC x and z, 3x3 / stride 1 / pad 1, TMA im2col
 
 template <class OutT>
 struct OutTraits;
@@ -242,6 +269,8 @@ struct ConvArgs {
   const float* bias;  // may be null
   Slot* slots;        // [2 * ceil(grid / mtiles)][Cout]; null = no statistics
   int Cout, HW, tilesP, mtiles, kblocks, tiles;
+  int W;              // NHWC 3x3: image width (pixel -> (n, h, w) for the im2col base)
+  int M;              // NHWC: output pixels N*H*W
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -268,7 +297,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 // the order of the channel's spread whatever its mean, so mean = K + SD/N and
 // M2 = SQ - SD^2/N keep the BN tolerances also for |mean| >> std.
 // Each (CTA, half) writes one Slot per channel; k_conv_fold merges the slots.
-template <int S, class OutT, bool STATS>
+template <int S, class OutT, bool STATS, int MODE>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1x1(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmZ, const ConvArgs a) {
@@ -311,18 +340,34 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       uint32_t it = 0;
+      constexpr int kTaps = MODE == kNHWC3 ? 9 : 1;
       for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
         const int mt = tile % a.mtiles, rest = tile / a.mtiles;
         const int p0 = (rest % a.tilesP) * BN, img = rest / a.tilesP;
-        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
-          const uint32_t s = it % S;
-          if (it >= (uint32_t)S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          uint8_t* A = ring + s * kStage;
-          uint8_t* B = A + kTileA;
-          mbar_expect_tx(&full[s], kStage);
-          tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
-          tma_load_3d(B, &tmX, &full[s], p0, kb * BK, img);
-          tma_load_3d(B + kTileB / 2, &tmX, &full[s], p0 + 64, kb * BK, img);
+        for (int tap = 0; tap < kTaps; ++tap) {
+          for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+            const uint32_t s = it % S;
+            if (it >= (uint32_t)S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+            uint8_t* A = ring + s * kStage;
+            uint8_t* B = A + kTileA;
+            mbar_expect_tx(&full[s], kStage);
+            if constexpr (MODE == kNCHW1) {
+              tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
+              tma_load_3d(B, &tmX, &full[s], p0, kb * BK, img);
+              tma_load_3d(B + kTileB / 2, &tmX, &full[s], p0 + 64, kb * BK, img);
+            } else if constexpr (MODE == kNHWC1) {
+              // x as [N*H*W][Cin]: 128 pixels x 64 channels, K-major like W
+              tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
+              tma_load_2d(B, &tmX, &full[s], kb * BK, p0);
+            } else {
+              // implicit GEMM: the im2col base of output pixel p0 is its input position
+              // minus the padding; tap (ky, kx) is the instruction's offset
+              const int n = p0 / a.HW, rem = p0 % a.HW;
+              tma_load_3d(A, &tmW, &full[s], kb * BK, mt * BM, tap);
+              tma_load_im2col_4d(B, &tmX, &full[s], kb * BK, rem % a.W - 1, rem / a.W - 1, n,
+                                 (uint16_t)(tap % 3), (uint16_t)(tap / 3));
+            }
+          }
         }
       }
     }
@@ -335,7 +380,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (li >= 2) mbar_wait(&tempty[acc], ((li >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+        const int ksteps = (MODE == kNHWC3 ? 9 : 1) * a.kblocks;
+        for (int kb = 0; kb < ksteps; ++kb, ++it) {
           const uint32_t s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
@@ -347,8 +393,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             //    row. B: MN-major, 64-pixel halves 8 KB apart (LBO), 8-channel groups
             //    1 KB apart (SBO); K step = 16 rows = 2 KB.
             const uint64_t ad = sdesc(A + k * 32, 16, 1024);
-            const uint64_t bd = sdesc(B + k * 2048, kTileB / 2, 1024);
-            mma_bf16(d, ad, bd, kIdesc, (kb | k) != 0);
+            if constexpr (MODE == kNCHW1) {
+              const uint64_t bd = sdesc(B + k * 2048, kTileB / 2, 1024);
+              mma_bf16(d, ad, bd, kIdesc, (kb | k) != 0);
+            } else {  // NHWC: B [128 px][64 ci] K-major, the same layout as A
+              const uint64_t bd = sdesc(B + k * 32, 16, 1024);
+              mma_bf16(d, ad, bd, kIdescKB, (kb | k) != 0);
+            }
           }
           mma_commit(&empty[s]);
         }
@@ -375,7 +426,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int rest = tile / a.mtiles;
       const int pt = rest % a.tilesP, img = rest / a.tilesP;
       const int p0 = pt * BN + half * kHalf;
-      const int nvalid = max(0, min(kHalf, a.HW - p0));
+      const int nvalid = max(0, min(kHalf, (MODE == kNCHW1 ? a.HW : a.M) - p0));
       const uint32_t acc = li & 1;
       mbar_wait(&tfull[acc], (li >> 1) & 1);
       tc_fence_after();
@@ -427,42 +478,60 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           SD += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
           SQ += ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
         }
-        // stage the half-row as 128-byte rows (fp32: 2 boxes of 32 columns; bf16: 1 box of
-        // 64), 128B swizzle: 16-byte chunk q of row r at q ^ (r & 7); the previous tile's
-        // stores must have finished reading the warp's buffer
+        // the previous tile's stores must have finished reading the warp's buffer
         if (g > 0) {
           if (lane == 0) bulk_wait_read0();
           __syncwarp();
         }
+        if constexpr (MODE == kNCHW1) {
+          // stage the half-row as 128-byte rows (fp32: 2 boxes of 32 columns; bf16: 1 box
+          // of 64), 128B swizzle: 16-byte chunk q of row r at q ^ (r & 7)
 #pragma unroll
-        for (int bx = 0; bx < kBoxes; ++bx) {
-          uint8_t* buf = wbuf + bx * kWarpStage;
+          for (int bx = 0; bx < kBoxes; ++bx) {
+            uint8_t* buf = wbuf + bx * kWarpStage;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            uint4 u;
-            if constexpr (sizeof(OutT) == 4) {
-              const float* f = v + bx * 32 + 4 * q;
-              u = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
-                             __float_as_uint(f[3]));
-            } else {
-              uint32_t w4[4];
+            for (int q = 0; q < 8; ++q) {
+              uint4 u;
+              if constexpr (sizeof(OutT) == 4) {
+                const float* f = v + bx * 32 + 4 * q;
+                u = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                               __float_as_uint(f[2]), __float_as_uint(f[3]));
+              } else {
+                uint32_t w4[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
-                w4[k] = *reinterpret_cast<uint32_t*>(&b2);
+                for (int k = 0; k < 4; ++k) {
+                  __nv_bfloat162 b2 =
+                      __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+                  w4[k] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                u = make_uint4(w4[0], w4[1], w4[2], w4[3]);
               }
-              u = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+              *reinterpret_cast<uint4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
             }
-            *reinterpret_cast<uint4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
+          }
+        } else {
+          // NHWC z: transpose through shared memory — row r = pixel p0 + r holds the
+          // warp's 32 channels (lane = channel), so each store instruction writes one
+          // contiguous row (no bank conflicts without a swizzle)
+#pragma unroll
+          for (int r = 0; r < kHalf; ++r) {
+            if constexpr (sizeof(OutT) == 4)
+              reinterpret_cast<float*>(wbuf)[r * 32 + lane] = v[r];
+            else
+              reinterpret_cast<__nv_bfloat16*>(wbuf)[r * 32 + lane] = __float2bfloat16_rn(v[r]);
           }
         }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
+          if constexpr (MODE == kNCHW1) {
 #pragma unroll
-          for (int bx = 0; bx < kBoxes; ++bx)
-            if (bx * kCols < nvalid)
-              tma_store_3d(&tmZ, wbuf + bx * kWarpStage, p0 + bx * kCols, m0 + sub * 32, img);
+            for (int bx = 0; bx < kBoxes; ++bx)
+              if (bx * kCols < nvalid)
+                tma_store_3d(&tmZ, wbuf + bx * kWarpStage, p0 + bx * kCols, m0 + sub * 32, img);
+          } else {
+            tma_store_2d(&tmZ, wbuf, m0 + sub * 32, p0);  // box {32 channels, 64 pixels}
+          }
           bulk_commit();
         }
         ++g;
@@ -565,15 +634,51 @@ EncodeFn encode_fn() {
 // bytes, for dims 1..r-1).
 int make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
              const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
-             const char* which) {
+             const char* which, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn fn = encode_fn();
   if (!fn) return fail(CGBN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
   cuuint32_t es[5] = {1, 1, 1, 1, 1};  // one per dimension (rank <= 5)
   CUresult r = fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(CGBN_ERR_INVALID, "tensor map encoding failed for %s (CUresult %d)", which, (int)r);
+  return CGBN_OK;
+}
+
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// NHWC x for the 3x3 implicit GEMM: dims {C, W, H, N}; bounding-box corners -1 / -1 in W
+// and H (zero padding 1 on both sides, output size = input size); each load is 64
+// channels x 128 output pixels.
+int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int64_t H,
+                    int64_t W) {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeIm2colFn)p;
+  });
+  if (!fn) return fail(CGBN_ERR_CUDA, "cuTensorMapEncodeIm2col is unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)(W * C * 2),
+                                 (cuuint64_t)(H * W * C * 2)};
+  const int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  lower, upper, BK, BN, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(CGBN_ERR_INVALID, "im2col tensor map encoding failed for x (CUresult %d)", (int)r);
   return CGBN_OK;
 }
 
@@ -596,64 +701,111 @@ int num_sms() {
   return sms[dev];
 }
 
+// Conv geometry: mode (kNCHW1 / kNHWC1 / kNHWC3), extents, tiles. NCHW: pixel tiles of
+// 128 within one image (tiles = channel tiles x pixel tiles x images); NHWC: pixel tiles
+// of 128 over the flattened N*H*W.
+struct Geo {
+  int mode;
+  int64_t N, Cin, Cout, H, W, HW, M;
+  int tilesP, mtiles, kblocks;
+  int64_t tiles;
+};
+
+Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t W) {
+  Geo g;
+  g.mode = mode;
+  g.N = N;
+  g.Cin = Cin;
+  g.Cout = Cout;
+  g.H = H;
+  g.W = W;
+  g.HW = H * W;
+  g.M = N * g.HW;
+  g.mtiles = (int)((Cout + BM - 1) / BM);
+  g.kblocks = (int)((Cin + BK - 1) / BK);
+  if (mode == kNCHW1) {
+    g.tilesP = (int)((g.HW + BN - 1) / BN);
+    g.tiles = (int64_t)g.mtiles * g.tilesP * N;
+  } else {
+    g.tilesP = (int)((g.M + BN - 1) / BN);
+    g.tiles = (int64_t)g.mtiles * g.tilesP;
+  }
+  return g;
+}
+
 // Conv grid: one CTA per SM, rounded down to a multiple of the channel tiles (so a CTA's
 // tiles share their channels), at most one CTA per tile.
-int conv_grid(int64_t tiles, int mtiles) {
+int conv_grid(const Geo& g) {
   const int sms = num_sms();
-  int64_t g = mtiles <= sms ? (int64_t)(sms / mtiles) * mtiles : mtiles;
-  return (int)std::min<int64_t>(g, tiles);
+  int64_t n = g.mtiles <= sms ? (int64_t)(sms / g.mtiles) * g.mtiles : g.mtiles;
+  return (int)std::min<int64_t>(n, g.tiles);
 }
 
-int64_t conv_tiles(int64_t N, int64_t Cout, int64_t HW) {
-  return ((Cout + BM - 1) / BM) * ((HW + BN - 1) / BN) * N;
+int conv_nslots(const Geo& g) { return 2 * ((conv_grid(g) + g.mtiles - 1) / g.mtiles); }
+
+size_t stats_ws_bytes(const Geo& g) {
+  return (size_t)conv_nslots(g) * (size_t)g.Cout * sizeof(Slot);
 }
 
-int conv_nslots(int64_t N, int64_t Cout, int64_t HW) {
-  const int mtiles = (int)((Cout + BM - 1) / BM);
-  const int grid = conv_grid(conv_tiles(N, Cout, HW), mtiles);
-  return 2 * ((grid + mtiles - 1) / mtiles);
-}
-
-template <class OutT>
-int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                int64_t Cout, int64_t HW, void* z, Slot* slots, cudaStream_t st) {
+template <class OutT, int MODE>
+int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, void* z,
+                Slot* slots, cudaStream_t st) {
+  constexpr int sz = sizeof(OutT);
+  const CUtensorMapDataType zdt =
+      sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const auto bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUtensorMap tmW, tmX, tmZ;
-  {
-    const cuuint64_t dims[2] = {(cuuint64_t)Cin, (cuuint64_t)Cout};
-    const cuuint64_t strides[1] = {(cuuint64_t)Cin * 2};
-    const cuuint32_t box[2] = {BK, BM};
-    if (int rc = make_map(&tmW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, strides, box, "w")) return rc;
+  if constexpr (MODE == kNHWC3) {  // w9[tap][Cout][Cin]
+    const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout, 9};
+    const cuuint64_t ws[2] = {(cuuint64_t)g.Cin * 2, (cuuint64_t)(g.Cin * g.Cout * 2)};
+    const cuuint32_t wb[3] = {BK, BM, 1};
+    if (int rc = make_map(&tmW, bf, 3, w, wd, ws, wb, "w")) return rc;
+  } else {  // w[Cout][Cin]
+    const cuuint64_t wd[2] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout};
+    const cuuint64_t ws[1] = {(cuuint64_t)g.Cin * 2};
+    const cuuint32_t wb[2] = {BK, BM};
+    if (int rc = make_map(&tmW, bf, 2, w, wd, ws, wb, "w")) return rc;
   }
-  {
-    const cuuint64_t dims[3] = {(cuuint64_t)HW, (cuuint64_t)Cin, (cuuint64_t)N};
-    const cuuint64_t strides[2] = {(cuuint64_t)HW * 2, (cuuint64_t)(Cin * HW * 2)};
-    const cuuint32_t box[3] = {64, BK, 1};
-    if (int rc = make_map(&tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, x, dims, strides, box, "x")) return rc;
-  }
-  {
-    constexpr int sz = sizeof(OutT);
-    const cuuint64_t dims[3] = {(cuuint64_t)HW, (cuuint64_t)Cout, (cuuint64_t)N};
-    const cuuint64_t strides[2] = {(cuuint64_t)HW * sz, (cuuint64_t)(Cout * HW * sz)};
-    const cuuint32_t box[3] = {(cuuint32_t)OutTraits<OutT>::kCols, 32, 1};
-    const CUtensorMapDataType dt =
-        sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    if (int rc = make_map(&tmZ, dt, 3, z, dims, strides, box, "z")) return rc;
+  if constexpr (MODE == kNCHW1) {
+    const cuuint64_t xd[3] = {(cuuint64_t)g.HW, (cuuint64_t)g.Cin, (cuuint64_t)g.N};
+    const cuuint64_t xs[2] = {(cuuint64_t)g.HW * 2, (cuuint64_t)(g.Cin * g.HW * 2)};
+    const cuuint32_t xb[3] = {64, BK, 1};
+    if (int rc = make_map(&tmX, bf, 3, x, xd, xs, xb, "x")) return rc;
+    const cuuint64_t zd[3] = {(cuuint64_t)g.HW, (cuuint64_t)g.Cout, (cuuint64_t)g.N};
+    const cuuint64_t zs[2] = {(cuuint64_t)g.HW * sz, (cuuint64_t)(g.Cout * g.HW * sz)};
+    const cuuint32_t zb[3] = {(cuuint32_t)OutTraits<OutT>::kCols, 32, 1};
+    if (int rc = make_map(&tmZ, zdt, 3, z, zd, zs, zb, "z")) return rc;
+  } else {
+    if constexpr (MODE == kNHWC1) {  // x as [M][Cin]
+      const cuuint64_t xd[2] = {(cuuint64_t)g.Cin, (cuuint64_t)g.M};
+      const cuuint64_t xs[1] = {(cuuint64_t)g.Cin * 2};
+      const cuuint32_t xb[2] = {BK, BN};
+      if (int rc = make_map(&tmX, bf, 2, x, xd, xs, xb, "x")) return rc;
+    } else {
+      if (int rc = make_im2col_map(&tmX, x, g.N, g.Cin, g.H, g.W)) return rc;
+    }
+    // z as [M][Cout], box {32 channels, 64 pixels}, unswizzled (transposed staging)
+    const cuuint64_t zd[2] = {(cuuint64_t)g.Cout, (cuuint64_t)g.M};
+    const cuuint64_t zs[1] = {(cuuint64_t)g.Cout * sz};
+    const cuuint32_t zb[2] = {32, (cuuint32_t)kHalf};
+    if (int rc = make_map(&tmZ, zdt, 2, z, zd, zs, zb, "z", CU_TENSOR_MAP_SWIZZLE_NONE)) return rc;
   }
   ConvArgs a;
   a.bias = bias;
   a.slots = slots;
-  a.Cout = (int)Cout;
-  a.HW = (int)HW;
-  a.tilesP = (int)((HW + BN - 1) / BN);
-  a.mtiles = (int)((Cout + BM - 1) / BM);
-  a.kblocks = (int)((Cin + BK - 1) / BK);
-  a.tiles = (int)conv_tiles(N, Cout, HW);
+  a.Cout = (int)g.Cout;
+  a.HW = (int)g.HW;
+  a.tilesP = g.tilesP;
+  a.mtiles = g.mtiles;
+  a.kblocks = g.kblocks;
+  a.tiles = (int)g.tiles;
+  a.W = (int)g.W;
+  a.M = (int)g.M;
   const size_t smem = conv_smem_bytes();
-  auto kern = slots ? k_conv1x1<kStages, OutT, true> : k_conv1x1<kStages, OutT, false>;
+  auto kern = slots ? k_conv1x1<kStages, OutT, true, MODE> : k_conv1x1<kStages, OutT, false, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const long long grid = conv_grid(a.tiles, a.mtiles);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
+  cfg.gridDim = dim3((unsigned)conv_grid(g));
   cfg.blockDim = dim3(kConvThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -663,72 +815,56 @@ int launch_conv(const void* x, const void* w, const float* bias, int64_t N, int6
   cfg.attrs = at;
   cfg.numAttrs = getenv("CGBN_NO_PDL") ? 0 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmZ, a);
-  if (e != cudaSuccess) return fail(CGBN_ERR_CUDA, "conv1x1 launch failed: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(CGBN_ERR_CUDA, "conv launch failed: %s", cudaGetErrorString(e));
   return CGBN_OK;
 }
 
-int validate(const void* x, const void* w, const void* z, int64_t N, int64_t Cin, int64_t Cout,
-             int64_t HW, int out_dtype) {
-  if (!x || !w || !z) return fail(CGBN_ERR_INVALID, "conv1x1: null tensor pointer");
-  if (N <= 0 || Cin <= 0 || Cout <= 0 || HW <= 0)
-    return fail(CGBN_ERR_INVALID, "conv1x1: extents must be positive");
+int validate(const char* what, const void* x, const void* w, const void* z, const Geo& g,
+             int out_dtype) {
+  if (!x || !w || !z) return fail(CGBN_ERR_INVALID, "%s: null tensor pointer", what);
+  if (g.N <= 0 || g.Cin <= 0 || g.Cout <= 0 || g.H <= 0 || g.W <= 0)
+    return fail(CGBN_ERR_INVALID, "%s: extents must be positive", what);
   if (out_dtype != CGBN_ACT_F32 && out_dtype != CGBN_ACT_BF16)
-    return fail(CGBN_ERR_INVALID, "conv1x1: output dtype must be CGBN_ACT_F32 or CGBN_ACT_BF16");
-  if (HW % 8 != 0)
-    return fail(CGBN_ERR_UNSUPPORTED, "conv1x1: H*W=%lld must be a multiple of 8 (TMA row stride)",
-                (long long)HW);
-  if (Cin % 8 != 0)
-    return fail(CGBN_ERR_UNSUPPORTED, "conv1x1: Cin=%lld must be a multiple of 8", (long long)Cin);
-  if (Cout > 65535 || N > 65535 || HW * N > (1ll << 31) ||
-      (int64_t)((Cout + BM - 1) / BM) * ((HW + BN - 1) / BN) * N > (1ll << 30))
-    return fail(CGBN_ERR_INVALID, "conv1x1: extents too large");
+    return fail(CGBN_ERR_INVALID, "%s: output dtype must be CGBN_ACT_F32 or CGBN_ACT_BF16", what);
+  if (g.mode == kNCHW1 && g.HW % 8 != 0)
+    return fail(CGBN_ERR_UNSUPPORTED, "%s: H*W=%lld must be a multiple of 8 (TMA row stride)",
+                what, (long long)g.HW);
+  if (g.Cin % 8 != 0)
+    return fail(CGBN_ERR_UNSUPPORTED, "%s: Cin=%lld must be a multiple of 8", what, (long long)g.Cin);
+  if (g.mode != kNCHW1 && g.Cout % 8 != 0)
+    return fail(CGBN_ERR_UNSUPPORTED, "%s: Cout=%lld must be a multiple of 8 (NHWC z row stride)",
+                what, (long long)g.Cout);
+  if (g.Cout > 65535 || g.N > 65535 || g.M >= (1ll << 31) || g.tiles > (1ll << 30) ||
+      g.H > 32767 || g.W > 32767)
+    return fail(CGBN_ERR_INVALID, "%s: extents too large", what);
   if (((uintptr_t)x | (uintptr_t)w | (uintptr_t)z) & 15)
-    return fail(CGBN_ERR_INVALID, "conv1x1: pointers must be 16-byte aligned");
+    return fail(CGBN_ERR_INVALID, "%s: pointers must be 16-byte aligned", what);
   return CGBN_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW) {
-  if (N <= 0 || Cout <= 0 || HW <= 0) return 0;
-  return (size_t)conv_nslots(N, Cout, HW) * (size_t)Cout * sizeof(Slot);
-}
-
-int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                 int64_t Cout, int64_t HW, int out_dtype, void* z, void* stream) {
-  if (int rc = validate(x, w, z, N, Cin, Cout, HW, out_dtype)) return rc;
+template <int MODE>
+int run_conv(const char* what, const void* x, const void* w, const float* bias, const Geo& g,
+             int out_dtype, void* z, double* partial, void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(what, x, w, z, g, out_dtype)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = out_dtype == CGBN_ACT_F32
-               ? launch_conv<float>(x, w, bias, N, Cin, Cout, HW, z, nullptr, st)
-               : launch_conv<__nv_bfloat16>(x, w, bias, N, Cin, Cout, HW, z, nullptr, st);
-  return rc;
-}
-
-int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                       int64_t Cout, int64_t HW, int out_dtype, void* z, double* partial,
-                       void* ws, size_t ws_bytes, void* stream) {
-  if (int rc = validate(x, w, z, N, Cin, Cout, HW, out_dtype)) return rc;
-  if (!partial) return fail(CGBN_ERR_INVALID, "conv1x1_stats: partial is NULL");
-  const size_t need = cgbn_conv1x1_ws_bytes(N, Cout, HW);
-  if (!ws || ws_bytes < need)
-    return fail(CGBN_ERR_INVALID, "conv1x1_stats: workspace too small (need %lld, got %lld)",
-                (long long)need, (long long)ws_bytes);
-  if ((uintptr_t)ws & 15) return fail(CGBN_ERR_INVALID, "conv1x1_stats: workspace must be 16-byte aligned");
-  cudaStream_t st = (cudaStream_t)stream;
-  if (conv_nslots(N, Cout, HW) > 32 * kFoldPerWarp)
-    return fail(CGBN_ERR_UNSUPPORTED, "conv1x1_stats: more than %d statistics slots per channel",
-                32 * kFoldPerWarp);
-  Slot* slots = (Slot*)ws;
-  int rc = out_dtype == CGBN_ACT_F32
-               ? launch_conv<float>(x, w, bias, N, Cin, Cout, HW, z, slots, st)
-               : launch_conv<__nv_bfloat16>(x, w, bias, N, Cin, Cout, HW, z, slots, st);
-  if (rc) return rc;
-  const int mtiles = (int)((Cout + BM - 1) / BM);
-  const int grid = conv_grid(conv_tiles(N, Cout, HW), mtiles);
+  Slot* slots = nullptr;
+  if (partial) {
+    const size_t need = stats_ws_bytes(g);
+    if (!ws || ws_bytes < need)
+      return fail(CGBN_ERR_INVALID, "%s: workspace too small (need %lld, got %lld)", what,
+                  (long long)need, (long long)ws_bytes);
+    if ((uintptr_t)ws & 15)
+      return fail(CGBN_ERR_INVALID, "%s: workspace must be 16-byte aligned", what);
+    if (conv_nslots(g) > 32 * kFoldPerWarp)
+      return fail(CGBN_ERR_UNSUPPORTED, "%s: more than %d statistics slots per channel", what,
+                  32 * kFoldPerWarp);
+    slots = (Slot*)ws;
+  }
+  int rc = out_dtype == CGBN_ACT_F32 ? launch_conv<float, MODE>(x, w, bias, g, z, slots, st)
+                                     : launch_conv<__nv_bfloat16, MODE>(x, w, bias, g, z, slots, st);
+  if (rc || !partial) return rc;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((Cout + 31) / 32));
+  cfg.gridDim = dim3((unsigned)((g.Cout + 31) / 32));
   cfg.blockDim = dim3(1024);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -736,10 +872,64 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = getenv("CGBN_NO_PDL") ? 0 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_conv_fold, (const Slot*)slots, (int)Cout, mtiles,
-                                     grid, conv_nslots(N, Cout, HW), partial);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_conv_fold, (const Slot*)slots, (int)g.Cout, g.mtiles,
+                                     conv_grid(g), conv_nslots(g), partial);
   if (e != cudaSuccess) return fail(CGBN_ERR_CUDA, "conv fold launch failed: %s", cudaGetErrorString(e));
   return CGBN_OK;
+}
+
+int nhwc_mode(int ksize) { return ksize == 1 ? kNHWC1 : ksize == 3 ? kNHWC3 : -1; }
+
+}  // namespace
+
+extern "C" {
+
+size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW) {
+  if (N <= 0 || Cout <= 0 || HW <= 0) return 0;
+  return stats_ws_bytes(make_geo(kNCHW1, N, 8, Cout, 1, HW));
+}
+
+int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                 int64_t Cout, int64_t HW, int out_dtype, void* z, void* stream) {
+  return run_conv<kNCHW1>("conv1x1", x, w, bias, make_geo(kNCHW1, N, Cin, Cout, 1, HW),
+                          out_dtype, z, nullptr, nullptr, 0, stream);
+}
+
+int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                       int64_t Cout, int64_t HW, int out_dtype, void* z, double* partial,
+                       void* ws, size_t ws_bytes, void* stream) {
+  if (!partial) return fail(CGBN_ERR_INVALID, "conv1x1_stats: partial is NULL");
+  return run_conv<kNCHW1>("conv1x1_stats", x, w, bias, make_geo(kNCHW1, N, Cin, Cout, 1, HW),
+                          out_dtype, z, partial, ws, ws_bytes, stream);
+}
+
+size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W) {
+  if (N <= 0 || Cout <= 0 || H <= 0 || W <= 0) return 0;
+  return stats_ws_bytes(make_geo(kNHWC1, N, 8, Cout, H, W));
+}
+
+int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                   int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
+                   void* stream) {
+  const int mode = nhwc_mode(ksize);
+  if (mode < 0) return fail(CGBN_ERR_INVALID, "conv_nhwc: ksize must be 1 or 3, got %d", ksize);
+  const Geo g = make_geo(mode, N, Cin, Cout, H, W);
+  return mode == kNHWC1
+             ? run_conv<kNHWC1>("conv_nhwc", x, w, bias, g, out_dtype, z, nullptr, nullptr, 0, stream)
+             : run_conv<kNHWC3>("conv_nhwc", x, w, bias, g, out_dtype, z, nullptr, nullptr, 0, stream);
+}
+
+int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
+                         int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
+                         double* partial, void* ws, size_t ws_bytes, void* stream) {
+  const int mode = nhwc_mode(ksize);
+  if (mode < 0) return fail(CGBN_ERR_INVALID, "conv_nhwc_stats: ksize must be 1 or 3, got %d", ksize);
+  if (!partial) return fail(CGBN_ERR_INVALID, "conv_nhwc_stats: partial is NULL");
+  const Geo g = make_geo(mode, N, Cin, Cout, H, W);
+  return mode == kNHWC1 ? run_conv<kNHWC1>("conv_nhwc_stats", x, w, bias, g, out_dtype, z,
+                                           partial, ws, ws_bytes, stream)
+                        : run_conv<kNHWC3>("conv_nhwc_stats", x, w, bias, g, out_dtype, z,
+                                           partial, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

@@ -217,3 +217,127 @@ def test_unsupported_shapes_raise():
         P.conv1x1(x, wt)
     with pytest.raises(cg.BatchNormError, match="bfloat16"):
         P.conv1x1(x.float(), wt)
+
+
+# ------------------------------------------- channels_last: 1x1 and 3x3 (TMA im2col)
+
+def _cl(t):
+    return t.contiguous(memory_format=torch.channels_last)
+
+
+def _operands3(n, cin, cout, hw, seed, loc=0.0, bias=False, bias_loc=0.0):
+    g = torch.Generator().manual_seed(seed)
+    h, w = hw
+    x = (torch.randn(n, cin, h, w, generator=g) + loc).to(torch.bfloat16)
+    wt = (torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, generator=g) * 3.0 + bias_loc if bias else None
+    return x, wt, b
+
+
+SHAPES_NHWC = [
+    # n, cin, cout, (h, w): any H, W; tiles of 128 pixels run across rows and images
+    (2, 64, 256, (56, 56)),
+    (4, 256, 64, (14, 14)),     # H*W = 196: not possible on the NCHW kernel
+    (3, 72, 136, (7, 7)),       # K tail, Cout % 128 != 0, 147 pixels
+    (1, 512, 128, (5, 9)),
+]
+
+
+@pytest.mark.parametrize("n,cin,cout,hw", SHAPES_NHWC)
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_conv1x1_channels_last(n, cin, cout, hw, out_dtype):
+    x, wt, b = _operands(n, cin, cout, hw, seed=cin * 3 + cout, bias=True)
+    z, partial = P.conv1x1_stats(_cl(x.to(DEV)), wt.to(DEV), b, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    assert z.is_contiguous(memory_format=torch.channels_last) and z.shape == (n, cout, *hw)
+    ref = _z_ref(x, wt, b)
+    tol = 1e-5 if out_dtype == torch.float32 else 8e-3
+    assert O.rel_err(z.double().cpu().numpy(), ref.numpy(), floor=float(ref.abs().max())) <= tol
+    mean, m2, cnt = _stats64(z)
+    _check_partial(partial.cpu().numpy(), mean, m2, cnt, cout)
+
+
+SHAPES3 = [
+    (2, 64, 64, (56, 56)),      # ResNet stage-1 conv2
+    (2, 128, 128, (28, 28)),    # stage-2 conv2
+    (3, 64, 256, (14, 14)),
+    (1, 72, 192, (7, 7)),       # K tail, Cout tail, tiny plane (every pixel on a border)
+    (2, 64, 64, (9, 13)),       # odd extents
+]
+
+
+def _z_ref3(x, wt, b):
+    z = torch.nn.functional.conv2d(x.double(), wt.double(), padding=1)
+    if b is not None:
+        z = z + b.double()[None, :, None, None]
+    return z
+
+
+@pytest.mark.parametrize("n,cin,cout,hw", SHAPES3)
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_conv3x3_output_and_partial(n, cin, cout, hw, out_dtype):
+    x, wt, b = _operands3(n, cin, cout, hw, seed=cin + cout + 3, bias=(cout % 128 != 0))
+    z, partial = P.conv3x3_stats(_cl(x.to(DEV)), wt.to(DEV), b, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    assert z.is_contiguous(memory_format=torch.channels_last) and z.shape == (n, cout, *hw)
+    ref = _z_ref3(x, wt, b)
+    tol = 1e-5 if out_dtype == torch.float32 else 8e-3
+    assert O.rel_err(z.double().cpu().numpy(), ref.numpy(), floor=float(ref.abs().max())) <= tol
+    mean, m2, cnt = _stats64(z)
+    _check_partial(partial.cpu().numpy(), mean, m2, cnt, cout)
+    z2 = P.conv3x3(_cl(x.to(DEV)), wt.to(DEV), b, out_dtype=out_dtype)
+    assert torch.equal(z, z2)
+
+
+@pytest.mark.parametrize("bias_loc", [0.0, 1000.0])
+def test_conv3x3_fused_bn_forward_backward_matches_oracle(bias_loc):
+    n, cin, cout, hw = 2, 64, 128, (28, 28)
+    x, wt, b = _operands3(n, cin, cout, hw, seed=31, loc=0.5, bias=True, bias_loc=bias_loc)
+    rng = np.random.default_rng(5)
+    gamma = rng.uniform(0.5, 1.5, cout).astype(np.float32)
+    beta = rng.standard_normal(cout).astype(np.float32)
+    st = cg.BNLayerState(gamma=gamma, beta=beta)
+    y, cache, z = P.conv3x3_bn_forward_local(_cl(x.to(DEV)), wt.to(DEV), st, bias=b, relu=True)
+    assert y.is_contiguous(memory_format=torch.channels_last)
+    dy = torch.randn(z.shape, generator=torch.Generator().manual_seed(6))
+    dx, dgamma, dbeta = cg.bn_backward_local(_cl(dy.to(DEV)), cache, st)
+    ref = O.cgbn_world([z.double().cpu().numpy()], gamma.astype(np.float64),
+                       beta.astype(np.float64), 1, relu=True, dys=[dy.double().numpy()])[0]
+    yref = torch.from_numpy(ref["y"]).float().double().numpy()
+    assert O.rel_err(y.double().cpu().numpy(), yref) <= 1e-5
+    assert O.rel_err(cache.mu.cpu().numpy(), ref["mu"]) <= 1e-5
+    assert O.rel_err(cache.var.cpu().numpy(), ref["var"]) <= 1e-5
+    assert O.rel_err(st.running_mean.double().cpu().numpy(), ref["running_mean"]) <= 1e-5
+    assert O.rel_err(st.running_var.double().cpu().numpy(), ref["running_var"]) <= 1e-5
+    assert O.rel_err(dx.double().cpu().numpy(), ref["dx"]) <= 1e-4
+    assert O.rel_err(dgamma.double().cpu().numpy(), ref["dgamma"]) <= 1e-4
+    assert O.rel_err(dbeta.double().cpu().numpy(), ref["dbeta"]) <= 1e-4
+
+
+def test_sync_conv3x3_group_of_two():
+    """Two ranks with unequal batches: group statistics identical on both ranks and equal
+    to the oracle on the concatenated z."""
+    world, cin, cout, hw = 2, 64, 64, (14, 14)
+    ops = [_operands3(n, cin, cout, hw, seed=200 + r) for r, n in enumerate([2, 3])]
+    wd = ops[0][1].to(DEV)
+    xs = [_cl(o[0].to(DEV)) for o in ops]
+
+    def worker(h):
+        st = cg.BNLayerState.create(cout, device=DEV)
+        y, cache, z = P.sync_conv3x3_bn_forward(h, xs[h.rank], wd, st)
+        return dict(y=y.double().cpu().numpy(), z=z.double().cpu().numpy(),
+                    mu=cache.mu.cpu().numpy(), var=cache.var.cpu().numpy())
+
+    outs = cg.DeviceGroup(world, timeout_s=60.0).run(worker)
+    ref = O.cgbn_world([o["z"] for o in outs], np.ones(cout), np.zeros(cout), world)
+    for r in range(world):
+        assert np.array_equal(outs[r]["var"], outs[0]["var"])
+        assert O.rel_err(outs[r]["var"], ref[r]["var"]) <= 1e-5
+        assert O.rel_err(outs[r]["y"], ref[r]["y"]) <= 1e-5
+
+
+def test_conv3x3_needs_channels_last():
+    x = torch.randn(1, 64, 8, 8, device=DEV).to(torch.bfloat16)
+    wt = torch.randn(64, 64, 3, 3, device=DEV).to(torch.bfloat16)
+    with pytest.raises(cg.BatchNormError, match="channels_last"):
+        P.conv3x3(x, wt)
