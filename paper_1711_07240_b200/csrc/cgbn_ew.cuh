@@ -135,6 +135,22 @@ __device__ __forceinline__ void ew_coef(const double* __restrict__ T, const uint
   }
 }
 
+// Coefficients of the UE channels of a channels_last unit starting at channel-aligned
+// element e (CM 3: c % 4 == 0), 4 at a time.
+template <int UE>
+__device__ __forceinline__ void ew_coef_unit(const EwGeom& g, const double* __restrict__ T,
+                                             uint32_t e, double* t) {
+#pragma unroll
+  for (int h = 0; h < UE; h += 4) {
+    uint32_t c[4];
+    chan4<3>(g, e + h, c);
+    double q[4];
+    ew_coef<3>(T, c, q);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[h + k] = q[k];
+  }
+}
+
 #ifndef CGBN_EWU
 #define CGBN_EWU 2
 #endif
@@ -143,7 +159,7 @@ constexpr int kEwU = CGBN_EWU;  // 16-byte units per elementwise thread (one rou
 template <class T>
 constexpr int ew_ue() { return 16 / (int)sizeof(T); }
 
-template <class T, bool RELU, int CM>
+template <class T, bool RELU, int CM, int U>
 __global__ void __launch_bounds__(kThreads)
 k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
             const double* __restrict__ P, const double* __restrict__ Q) {
@@ -151,27 +167,25 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
   pdl_trigger();  // the next reduction may launch and wait
   const uint32_t stride = gridDim.x * kThreads;
   uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  Vec<T, UE> v[kEwU];
+  Vec<T, UE> v[U];
   auto load = [&](uint32_t i0) {
 #pragma unroll
-    for (int u = 0; u < kEwU; ++u)
+    for (int u = 0; u < U; ++u)
       if (i0 + u * stride < g.n4) v[u].load(x + (size_t)UE * ew_unit(g, i0 + u * stride));
   };
   load(i);    // x is not written by the kernel we may overlap with
   pdl_wait();  // the coefficient table is
-  // channels_last: when every unit of the thread covers the same 4 channels, their
-  // coefficients are loaded once
-  constexpr bool kReuse = CM == 3 && UE == 4;
-  double pr[4], qr[4];
+  // channels_last: when every unit of the thread covers the same UE channels, their
+  // coefficients are loaded once (fp64 tables would otherwise cost 16 B per element)
+  constexpr bool kReuse = CM == 3;
+  double pr[UE], qr[UE];
   if (kReuse && g.reuse && i < g.n4) {
-    uint32_t c[4];
-    chan4<CM>(g, UE * ew_unit(g, i), c);
-    ew_coef<CM>(P, c, pr);
-    ew_coef<CM>(Q, c, qr);
+    ew_coef_unit<UE>(g, P, UE * ew_unit(g, i), pr);
+    ew_coef_unit<UE>(g, Q, UE * ew_unit(g, i), qr);
   }
-  for (; i < g.n4; i += kEwU * stride) {
+  for (; i < g.n4; i += U * stride) {
 #pragma unroll
-    for (int u = 0; u < kEwU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t j = i + u * stride;
       if (j >= g.n4) continue;
       const uint32_t jm = ew_unit(g, j);
@@ -182,8 +196,8 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
         if (kReuse && g.reuse) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            p[k] = pr[k];
-            q[k] = qr[k];
+            p[k] = pr[h + k];
+            q[k] = qr[h + k];
           }
         } else {
           uint32_t c[4];
@@ -200,7 +214,7 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
       }
       stv<T, UE>(y + (size_t)UE * jm, o);
     }
-    load(i + kEwU * stride);
+    load(i + U * stride);
   }
   if (blockIdx.x == 0 && threadIdx.x < g.tail) {
     const uint32_t e = UE * g.n4 + threadIdx.x;
@@ -211,7 +225,7 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
   }
 }
 
-template <class T, bool RELU, int CM>
+template <class T, bool RELU, int CM, int U>
 __global__ void __launch_bounds__(kThreads)
 k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restrict__ dx,
         const double* __restrict__ A, const double* __restrict__ B,
@@ -221,10 +235,10 @@ k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restri
   pdl_trigger();  // the next reduction may launch and wait
   const uint32_t stride = gridDim.x * kThreads;
   uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  Vec<T, UE> gv[kEwU], xv[kEwU];
+  Vec<T, UE> gv[U], xv[U];
   auto load = [&](uint32_t i0) {
 #pragma unroll
-    for (int u = 0; u < kEwU; ++u)
+    for (int u = 0; u < U; ++u)
       if (i0 + u * stride < g.n4) {
         const size_t off = (size_t)UE * ew_unit(g, i0 + u * stride);
         gv[u].load(dy + off);
@@ -233,22 +247,21 @@ k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restri
   };
   load(i);    // dy and x are not written by the kernel we may overlap with
   pdl_wait();  // the coefficient tables are
-  constexpr bool kReuse = CM == 3 && UE == 4;  // see k_ew_affine
-  double ar[4], br[4], cr[4], pr[4] = {0.0, 0.0, 0.0, 0.0}, qr[4] = {0.0, 0.0, 0.0, 0.0};
+  constexpr bool kReuse = CM == 3;  // see k_ew_affine
+  double ar[UE], br[UE], cr[UE], pr[UE], qr[UE];
   if (kReuse && g.reuse && i < g.n4) {
-    uint32_t c[4];
-    chan4<CM>(g, UE * ew_unit(g, i), c);
-    ew_coef<CM>(A, c, ar);
-    ew_coef<CM>(B, c, br);
-    ew_coef<CM>(Cc, c, cr);
+    const uint32_t e0 = UE * ew_unit(g, i);
+    ew_coef_unit<UE>(g, A, e0, ar);
+    ew_coef_unit<UE>(g, B, e0, br);
+    ew_coef_unit<UE>(g, Cc, e0, cr);
     if (RELU) {
-      ew_coef<CM>(P, c, pr);
-      ew_coef<CM>(Q, c, qr);
+      ew_coef_unit<UE>(g, P, e0, pr);
+      ew_coef_unit<UE>(g, Q, e0, qr);
     }
   }
-  for (; i < g.n4; i += kEwU * stride) {
+  for (; i < g.n4; i += U * stride) {
 #pragma unroll
-    for (int u = 0; u < kEwU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t j = i + u * stride;
       if (j >= g.n4) continue;
       const uint32_t jm = ew_unit(g, j);
@@ -259,11 +272,13 @@ k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restri
         if (kReuse && g.reuse) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            a[k] = ar[k];
-            b[k] = br[k];
-            cc[k] = cr[k];
-            p[k] = pr[k];
-            q[k] = qr[k];
+            a[k] = ar[h + k];
+            b[k] = br[h + k];
+            cc[k] = cr[h + k];
+            if (RELU) {
+              p[k] = pr[h + k];
+              q[k] = qr[h + k];
+            }
           }
         } else {
           uint32_t c[4];
@@ -286,7 +301,7 @@ k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restri
       }
       stv<T, UE>(dx + (size_t)UE * jm, o);
     }
-    load(i + kEwU * stride);
+    load(i + U * stride);
   }
   if (blockIdx.x == 0 && threadIdx.x < g.tail) {
     const uint32_t e = UE * g.n4 + threadIdx.x;

@@ -688,9 +688,18 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* c
 // faster with many short-lived CTAs than with one resident wave that loops (ResNet-50
 // step +3%, 100 MB layers 4-6 us faster; CGBN_EW_PERSISTENT=1 restores the resident
 // grid for A/B).
+// Units per thread per round: kEwU (2) in memory order; channels_last (CM 3) threads
+// keep their UE channels' fp64 coefficients in registers, so they take more units to
+// amortise the coefficient loads.
+#ifndef CGBN_EWU_NHWC
+#define CGBN_EWU_NHWC 4
+#endif
+template <int CM>
+constexpr int ew_units() { return CM == 3 ? CGBN_EWU_NHWC : kEwU; }
+
 template <class K>
-unsigned ew_grid(K kernel, const EwPlan& ep) {
-  int64_t grid = ceil_div((int64_t)ep.g.n4 + 1, kThreads * kEwU);
+unsigned ew_grid(K kernel, const EwPlan& ep, int units = kEwU) {
+  int64_t grid = ceil_div((int64_t)ep.g.n4 + 1, kThreads * units);
   static const bool persistent = getenv("CGBN_EW_PERSISTENT") != nullptr;
   if (persistent) {
     const int64_t res = resident_ctas(kernel);
@@ -705,8 +714,8 @@ unsigned ew_grid(K kernel, const EwPlan& ep) {
 // Grid plus the channels_last coefficient-reuse flag (a thread's units are gridDim*256
 // units apart; they share their channels when that distance covers whole rows).
 template <class K>
-unsigned ew_grid_geom(K kernel, const EwPlan& ep, EwGeom* g) {
-  const unsigned grid = ew_grid(kernel, ep);
+unsigned ew_grid_geom(K kernel, const EwPlan& ep, EwGeom* g, int units) {
+  const unsigned grid = ew_grid(kernel, ep, units);
   *g = ep.g;
   const uint64_t ue = ep.act == 0 ? 4 : 8;
   g->reuse = (ep.cm == 3 && (ue * (uint64_t)grid * kThreads) % ep.g.C == 0) ? 1u : 0u;
@@ -717,8 +726,9 @@ template <class T, bool RELU, int CM>
 void launch_ew_affine_t(const EwPlan& ep, const void* x, void* y, const double* P,
                         const double* Q, bool pdl, cudaStream_t st) {
   EwGeom g;
-  const unsigned grid = ew_grid_geom(k_ew_affine<T, RELU, CM>, ep, &g);
-  launch_pdl(k_ew_affine<T, RELU, CM>, grid, pdl, st, g, static_cast<const T*>(x),
+  constexpr int U = ew_units<CM>();
+  const unsigned grid = ew_grid_geom(k_ew_affine<T, RELU, CM, U>, ep, &g, U);
+  launch_pdl(k_ew_affine<T, RELU, CM, U>, grid, pdl, st, g, static_cast<const T*>(x),
              static_cast<T*>(y), P, Q);
 }
 
@@ -751,8 +761,9 @@ template <class T, bool RELU, int CM>
 void launch_ew_dx_t(const EwPlan& ep, const void* dy, const void* x, void* dx, const WsView& w,
                     cudaStream_t st) {
   EwGeom g;
-  const unsigned grid = ew_grid_geom(k_ew_dx<T, RELU, CM>, ep, &g);
-  launch_pdl(k_ew_dx<T, RELU, CM>, grid, true, st, g,
+  constexpr int U = ew_units<CM>();
+  const unsigned grid = ew_grid_geom(k_ew_dx<T, RELU, CM, U>, ep, &g, U);
+  launch_pdl(k_ew_dx<T, RELU, CM, U>, grid, true, st, g,
              static_cast<const T*>(dy), static_cast<const T*>(x), static_cast<T*>(dx),
              (const double*)w.A, (const double*)w.B, (const double*)w.Cc, (const double*)w.P,
              (const double*)w.Q);

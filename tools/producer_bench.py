@@ -23,6 +23,18 @@ import torch  # noqa: E402
 import paper_1711_07240_b200 as cg  # noqa: E402
 from paper_1711_07240_b200 import producer as P  # noqa: E402
 
+LAYERS_NHWC = [  # (name, k, Cin, Cout, H, W, count in ResNet-50): channels_last producers
+    ("l1.conv2", 3, 64, 64, 56, 56, 3),
+    ("l2.conv2", 3, 128, 128, 28, 28, 3),
+    ("l3.conv2", 3, 256, 256, 14, 14, 5),
+    ("l4.conv2", 3, 512, 512, 7, 7, 2),
+    ("l1.conv3", 1, 64, 256, 56, 56, 3),
+    ("l2.conv3", 1, 128, 512, 28, 28, 4),
+    ("l3.conv1", 1, 1024, 256, 14, 14, 5),
+    ("l3.conv3", 1, 256, 1024, 14, 14, 6),
+    ("l4.conv3", 1, 512, 2048, 7, 7, 3),
+]
+
 LAYERS = [  # (name, Cin, Cout, H, W, count in ResNet-50)
     ("l1.conv1.first", 64, 64, 56, 56, 1),
     ("l1.conv1", 256, 64, 56, 56, 2),
@@ -60,7 +72,10 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--sets", type=int, default=3)
     ap.add_argument("--layers", default="")
+    ap.add_argument("--layout", choices=["nchw", "nhwc"], default="nchw")
     args = ap.parse_args()
+    if args.layout == "nhwc":
+        return main_nhwc(args)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     cg.set_strict(False)
@@ -125,6 +140,49 @@ def main():
                 res["cudnn_fwd_us"] = timed(cudnn) / K
             res["speedup_fused_vs_split"] = res["split_fwd_us"] / res["fused_fwd_us"]
             print(json.dumps(res), flush=True)
+
+
+def main_nhwc(args):
+    """channels_last producers (1x1 and 3x3): fused vs split BN forward, vs cuDNN."""
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cg.set_strict(False)
+    peak = 6549.8
+    cl = torch.channels_last
+    for name, k, cin, cout, h, w, cnt in LAYERS_NHWC:
+        if args.layers and name not in args.layers.split(","):
+            continue
+        n, K = args.batch, args.sets
+        xs = [torch.randn(n, cin, h, w, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+              for _ in range(K)]
+        wt = (torch.randn(cout, cin, k, k, device=dev) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+        conv = P.conv3x3 if k == 3 else P.conv1x1
+        fused_fn = P.conv3x3_bn_forward_local if k == 3 else P.conv1x1_bn_forward_local
+        for od in (torch.float32, torch.bfloat16):
+            sts = [cg.BNLayerState.create(cout, device=dev) for _ in range(K)]
+            esz = 4 if od == torch.float32 else 2
+            e = n * cout * h * w
+            conv_bytes = n * cin * h * w * 2 + cout * cin * k * k * 2 + e * esz
+            flops = 2.0 * e * cin * k * k
+            res = {"layer": name, "k": k, "N": n, "Cin": cin, "Cout": cout, "HW": [h, w],
+                   "count": cnt, "z_dtype": str(od).replace("torch.", ""), "layout": "NHWC"}
+            res["conv_us"] = timed(lambda: [conv(x, wt, out_dtype=od) for x in xs]) / K
+            res["conv_hbm_frac"] = conv_bytes / res["conv_us"] / 1e3 / peak
+            res["conv_tflops"] = flops / res["conv_us"] / 1e6
+            res["fused_fwd_us"] = timed(lambda: [fused_fn(x, wt, st, out_dtype=od)
+                                                 for x, st in zip(xs, sts)]) / K
+            res["split_fwd_us"] = timed(lambda: [cg.bn_forward_local(conv(x, wt, out_dtype=od), st)
+                                                 for x, st in zip(xs, sts)]) / K
+            if od == torch.bfloat16:
+                pad = 1 if k == 3 else 0
+                res["cudnn_conv_us"] = timed(
+                    lambda: [torch.nn.functional.conv2d(x, wt, padding=pad) for x in xs]) / K
+                res["cudnn_fwd_us"] = timed(
+                    lambda: [cg.bn_forward_local(torch.nn.functional.conv2d(x, wt, padding=pad), st)
+                             for x, st in zip(xs, sts)]) / K
+            res["speedup_fused_vs_split"] = res["split_fwd_us"] / res["fused_fwd_us"]
+            print(json.dumps(res), flush=True)
+    return 0
 
 
 if __name__ == "__main__":
