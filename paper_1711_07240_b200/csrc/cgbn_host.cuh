@@ -691,11 +691,16 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* c
 // Units per thread per round: kEwU (2) in memory order; channels_last (CM 3) threads
 // keep their UE channels' fp64 coefficients in registers, so they take more units to
 // amortise the coefficient loads.
+// Measured on B200 (U = 2 / 4 / 8, [32,C,H,W] NHWC): 4 is best everywhere except the fp32
+// dx pass without ReLU, where 8 is (54 -> 48 us on [32,256,56,56]); 16-bit dx at 8 (40 ->
+// 50 us) and fp32 dx with ReLU at 8 (5 coefficient tables in registers) are slower.
 #ifndef CGBN_EWU_NHWC
 #define CGBN_EWU_NHWC 4
 #endif
-template <int CM>
-constexpr int ew_units() { return CM == 3 ? CGBN_EWU_NHWC : kEwU; }
+template <int CM, class T = float, bool DX = false, bool RELU = false>
+constexpr int ew_units() {
+  return CM != 3 ? kEwU : (DX && !RELU && sizeof(T) == 4) ? 2 * CGBN_EWU_NHWC : CGBN_EWU_NHWC;
+}
 
 template <class K>
 unsigned ew_grid(K kernel, const EwPlan& ep, int units = kEwU) {
@@ -761,7 +766,7 @@ template <class T, bool RELU, int CM>
 void launch_ew_dx_t(const EwPlan& ep, const void* dy, const void* x, void* dx, const WsView& w,
                     cudaStream_t st) {
   EwGeom g;
-  constexpr int U = ew_units<CM>();
+  constexpr int U = ew_units<CM, T, true, RELU>();
   const unsigned grid = ew_grid_geom(k_ew_dx<T, RELU, CM, U>, ep, &g, U);
   launch_pdl(k_ew_dx<T, RELU, CM, U>, grid, true, st, g,
              static_cast<const T*>(dy), static_cast<const T*>(x), static_cast<T*>(dx),
