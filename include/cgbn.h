@@ -280,20 +280,23 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
                        void* ws, size_t ws_bytes, void* stream);
 
 /* The producer on channels-last activations (x, z NHWC = [N][H][W][C], the layout
- * detector training uses and the BN's native NHWC kernels read), ksize 1 or 3 (stride 1,
- * zero padding 1 for 3x3: the reference model's conv layer, model.py:235-242). The 3x3
- * case is an implicit GEMM on TMA im2col loads (9 taps x Cin/64 k-steps; the hardware
- * shifts each 128-pixel window by the tap and zero-fills outside the image), so any H
- * and W work. w: bf16 [Cout][Cin] (ksize 1) or [9][Cout][Cin] with tap = 3 * ky + kx
- * (the reference's (Cout, Cin, 3, 3) weight permuted). Cin and Cout must be multiples of
- * 8. Statistics contract as cgbn_conv1x1_stats; ws: cgbn_conv_nhwc_ws_bytes bytes. */
-size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W);
+ * detector training uses and the BN's native NHWC kernels read): ksize 1 or 3 (zero
+ * padding 1 for 3x3 — the reference model's conv layer, model.py:235-242), stride 1 or
+ * 2, any H and W; z is [N][Ho][Wo][Cout] with Ho = (H + 2 pad - ksize) / stride + 1. The
+ * 3x3 and strided cases are an implicit GEMM on TMA im2col loads (taps x Cin/64 k-steps;
+ * the hardware walks the output pixels, shifts each window by the tap and zero-fills
+ * outside the image). w: bf16 [Cout][Cin] (ksize 1) or [9][Cout][Cin] with tap =
+ * 3 * ky + kx (the reference's (Cout, Cin, 3, 3) weight permuted). Cin and Cout must be
+ * multiples of 8. Statistics contract as cgbn_conv1x1_stats; ws: cgbn_conv_nhwc_ws_bytes
+ * bytes. */
+size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W, int ksize,
+                               int stride);
 int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                   int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
-                   void* stream);
+                   int64_t Cout, int64_t H, int64_t W, int ksize, int stride, int out_dtype,
+                   void* z, void* stream);
 int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                         int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
-                         double* partial, void* ws, size_t ws_bytes, void* stream);
+                         int64_t Cout, int64_t H, int64_t W, int ksize, int stride, int out_dtype,
+                         void* z, double* partial, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -227,7 +227,7 @@ constexpr uint32_t kIdescKB = kIdescBase;
 // Layout / geometry modes of the conv kernel
 constexpr int kNCHW1 = 0;  // NCHW x and z, 1x1: pixel tiles within one image
 constexpr int kNHWC1 = 1;  // NHWC x and z, 1x1: pixel tiles of the flattened N*H*W
-constexpr int kNHWC3 = 2;  // NHWC x and z, 3x3 / stride 1 / pad 1, TMA im2col
+constexpr int kNHWC3 = 2;  // NHWC x and z, TMA im2col: 3x3 (pad 1) or 1x1, stride 1 or 2
 
 template <class OutT>
 struct OutTraits;
@@ -269,8 +269,9 @@ struct ConvArgs {
   const float* bias;  // may be null
   Slot* slots;        // [2 * ceil(grid / mtiles)][Cout]; null = no statistics
   int Cout, HW, tilesP, mtiles, kblocks, tiles;
-  int W;              // NHWC 3x3: image width (pixel -> (n, h, w) for the im2col base)
-  int M;              // NHWC: output pixels N*H*W
+  int M;              // NHWC: output pixels N*Ho*Wo
+  int Wo, HWo;        // im2col: output width / plane (output pixel -> (n, ho, wo))
+  int stride, pad, ksize, taps;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       uint32_t it = 0;
-      constexpr int kTaps = MODE == kNHWC3 ? 9 : 1;
+      const int kTaps = MODE == kNHWC3 ? a.taps : 1;
       for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
         const int mt = tile % a.mtiles, rest = tile / a.mtiles;
         const int p0 = (rest % a.tilesP) * BN, img = rest / a.tilesP;
@@ -362,10 +363,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             } else {
               // implicit GEMM: the im2col base of output pixel p0 is its input position
               // minus the padding; tap (ky, kx) is the instruction's offset
-              const int n = p0 / a.HW, rem = p0 % a.HW;
+              // (stride s: the traversal walks input positions s apart)
+              const int n = p0 / a.HWo, rem = p0 % a.HWo;
               tma_load_3d(A, &tmW, &full[s], kb * BK, mt * BM, tap);
-              tma_load_im2col_4d(B, &tmX, &full[s], kb * BK, rem % a.W - 1, rem / a.W - 1, n,
-                                 (uint16_t)(tap % 3), (uint16_t)(tap / 3));
+              tma_load_im2col_4d(B, &tmX, &full[s], kb * BK, (rem % a.Wo) * a.stride - a.pad,
+                                 (rem / a.Wo) * a.stride - a.pad, n,
+                                 (uint16_t)(tap % a.ksize), (uint16_t)(tap / a.ksize));
             }
           }
         }
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (li >= 2) mbar_wait(&tempty[acc], ((li >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        const int ksteps = (MODE == kNHWC3 ? 9 : 1) * a.kblocks;
+        const int ksteps = (MODE == kNHWC3 ? a.taps : 1) * a.kblocks;
         for (int kb = 0; kb < ksteps; ++kb, ++it) {
           const uint32_t s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
@@ -652,11 +655,10 @@ using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// NHWC x for the 3x3 implicit GEMM: dims {C, W, H, N}; bounding-box corners -1 / -1 in W
-// and H (zero padding 1 on both sides, output size = input size); each load is 64
-// channels x 128 output pixels.
+// NHWC x for the implicit GEMM: dims {C, W, H, N}; each load is 64 channels x 128 output
+// pixels; the tap is the instruction's offset.
 int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int64_t H,
-                    int64_t W) {
+                    int64_t W, int ksize, int stride, int pad) {
   static EncodeIm2colFn fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -671,8 +673,11 @@ int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int6
   const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
   const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)(W * C * 2),
                                  (cuuint64_t)(H * W * C * 2)};
-  const int lower[2] = {-1, -1}, upper[2] = {-1, -1};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
+  // bounding box of the base positions: [-pad, W - 1 + pad - (ksize - 1)] per spatial
+  // dimension, walked every `stride` elements
+  const int lo = -pad, hi = pad - (ksize - 1);
+  const int lower[2] = {lo, lo}, upper[2] = {hi, hi};
+  const cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                   lower, upper, BK, BN, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -707,11 +712,14 @@ int num_sms() {
 struct Geo {
   int mode;
   int64_t N, Cin, Cout, H, W, HW, M;
+  int ksize, stride, pad;
+  int64_t Ho, Wo;
   int tilesP, mtiles, kblocks;
   int64_t tiles;
 };
 
-Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t W) {
+Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t W,
+             int ksize = 1, int stride = 1) {
   Geo g;
   g.mode = mode;
   g.N = N;
@@ -720,7 +728,12 @@ Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t 
   g.H = H;
   g.W = W;
   g.HW = H * W;
-  g.M = N * g.HW;
+  g.ksize = ksize;
+  g.stride = stride;
+  g.pad = ksize / 2;
+  g.Ho = (H + 2 * g.pad - ksize) / stride + 1;
+  g.Wo = (W + 2 * g.pad - ksize) / stride + 1;
+  g.M = N * g.Ho * g.Wo;
   g.mtiles = (int)((Cout + BM - 1) / BM);
   g.kblocks = (int)((Cin + BK - 1) / BK);
   if (mode == kNCHW1) {
@@ -755,8 +768,9 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
       sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUtensorMap tmW, tmX, tmZ;
-  if constexpr (MODE == kNHWC3) {  // w9[tap][Cout][Cin]
-    const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout, 9};
+  if constexpr (MODE == kNHWC3) {  // w[tap][Cout][Cin]
+    const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout,
+                              (cuuint64_t)(g.ksize * g.ksize)};
     const cuuint64_t ws[2] = {(cuuint64_t)g.Cin * 2, (cuuint64_t)(g.Cin * g.Cout * 2)};
     const cuuint32_t wb[3] = {BK, BM, 1};
     if (int rc = make_map(&tmW, bf, 3, w, wd, ws, wb, "w")) return rc;
@@ -782,7 +796,8 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
       const cuuint32_t xb[2] = {BK, BN};
       if (int rc = make_map(&tmX, bf, 2, x, xd, xs, xb, "x")) return rc;
     } else {
-      if (int rc = make_im2col_map(&tmX, x, g.N, g.Cin, g.H, g.W)) return rc;
+      if (int rc = make_im2col_map(&tmX, x, g.N, g.Cin, g.H, g.W, g.ksize, g.stride, g.pad))
+        return rc;
     }
     // z as [M][Cout], box {32 channels, 64 pixels}, unswizzled (transposed staging)
     const cuuint64_t zd[2] = {(cuuint64_t)g.Cout, (cuuint64_t)g.M};
@@ -799,8 +814,13 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
   a.mtiles = g.mtiles;
   a.kblocks = g.kblocks;
   a.tiles = (int)g.tiles;
-  a.W = (int)g.W;
   a.M = (int)g.M;
+  a.Wo = (int)g.Wo;
+  a.HWo = (int)(g.Ho * g.Wo);
+  a.stride = g.stride;
+  a.pad = g.pad;
+  a.ksize = g.ksize;
+  a.taps = g.ksize * g.ksize;
   const size_t smem = conv_smem_bytes();
   auto kern = slots ? k_conv1x1<kStages, OutT, true, MODE> : k_conv1x1<kStages, OutT, false, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -878,7 +898,12 @@ int run_conv(const char* what, const void* x, const void* w, const float* bias, 
   return CGBN_OK;
 }
 
-int nhwc_mode(int ksize) { return ksize == 1 ? kNHWC1 : ksize == 3 ? kNHWC3 : -1; }
+// channels_last modes: 1x1 stride 1 reads x as a plain [N*H*W][Cin] matrix; 3x3 and
+// every stride-2 case go through im2col
+int nhwc_mode(int ksize, int stride) {
+  if ((ksize != 1 && ksize != 3) || (stride != 1 && stride != 2)) return -1;
+  return ksize == 1 && stride == 1 ? kNHWC1 : kNHWC3;
+}
 
 }  // namespace
 
@@ -903,29 +928,36 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
                           out_dtype, z, partial, ws, ws_bytes, stream);
 }
 
-size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W) {
-  if (N <= 0 || Cout <= 0 || H <= 0 || W <= 0) return 0;
-  return stats_ws_bytes(make_geo(kNHWC1, N, 8, Cout, H, W));
+size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W, int ksize,
+                               int stride) {
+  const int mode = nhwc_mode(ksize, stride);
+  if (N <= 0 || Cout <= 0 || H <= 0 || W <= 0 || mode < 0) return 0;
+  return stats_ws_bytes(make_geo(mode, N, 8, Cout, H, W, ksize, stride));
 }
 
 int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                   int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
-                   void* stream) {
-  const int mode = nhwc_mode(ksize);
-  if (mode < 0) return fail(CGBN_ERR_INVALID, "conv_nhwc: ksize must be 1 or 3, got %d", ksize);
-  const Geo g = make_geo(mode, N, Cin, Cout, H, W);
+                   int64_t Cout, int64_t H, int64_t W, int ksize, int stride, int out_dtype,
+                   void* z, void* stream) {
+  const int mode = nhwc_mode(ksize, stride);
+  if (mode < 0)
+    return fail(CGBN_ERR_INVALID, "conv_nhwc: ksize must be 1 or 3 and stride 1 or 2, got %d / %d",
+                ksize, stride);
+  const Geo g = make_geo(mode, N, Cin, Cout, H, W, ksize, stride);
   return mode == kNHWC1
              ? run_conv<kNHWC1>("conv_nhwc", x, w, bias, g, out_dtype, z, nullptr, nullptr, 0, stream)
              : run_conv<kNHWC3>("conv_nhwc", x, w, bias, g, out_dtype, z, nullptr, nullptr, 0, stream);
 }
 
 int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                         int64_t Cout, int64_t H, int64_t W, int ksize, int out_dtype, void* z,
-                         double* partial, void* ws, size_t ws_bytes, void* stream) {
-  const int mode = nhwc_mode(ksize);
-  if (mode < 0) return fail(CGBN_ERR_INVALID, "conv_nhwc_stats: ksize must be 1 or 3, got %d", ksize);
+                         int64_t Cout, int64_t H, int64_t W, int ksize, int stride, int out_dtype,
+                         void* z, double* partial, void* ws, size_t ws_bytes, void* stream) {
+  const int mode = nhwc_mode(ksize, stride);
+  if (mode < 0)
+    return fail(CGBN_ERR_INVALID,
+                "conv_nhwc_stats: ksize must be 1 or 3 and stride 1 or 2, got %d / %d", ksize,
+                stride);
   if (!partial) return fail(CGBN_ERR_INVALID, "conv_nhwc_stats: partial is NULL");
-  const Geo g = make_geo(mode, N, Cin, Cout, H, W);
+  const Geo g = make_geo(mode, N, Cin, Cout, H, W, ksize, stride);
   return mode == kNHWC1 ? run_conv<kNHWC1>("conv_nhwc_stats", x, w, bias, g, out_dtype, z,
                                            partial, ws, ws_bytes, stream)
                         : run_conv<kNHWC3>("conv_nhwc_stats", x, w, bias, g, out_dtype, z,

@@ -67,7 +67,7 @@ def _tile_scratch(device, nbytes):
         return buf
 
 
-def _check(x, weight, bias, out_dtype, k):
+def _check(x, weight, bias, out_dtype, k, stride=1):
     """Validate a k x k convolution's operands (k = 1 or 3); return the device operands,
     whether x is channels_last, and (n, cin, h, w, cout). A 3x3 weight is permuted to
     the kernel's [9][Cout][Cin] tap-major layout."""
@@ -95,6 +95,10 @@ def _check(x, weight, bias, out_dtype, k):
                 "by one element in a TMA box)")
         cout = weight.shape[0]
         wt = weight.permute(2, 3, 0, 1).reshape(9, cout, cin)  # [tap = 3 ky + kx][Cout][Cin]
+    if stride not in (1, 2):
+        raise BatchNormError(f"stride must be 1 or 2, got {stride}")
+    if stride != 1 and not nhwc:
+        raise BatchNormError("strided convolutions need channels_last x (TMA im2col)")
     if cin % 8 != 0:
         raise BatchNormError(f"conv{k}x{k} needs Cin a multiple of 8, got {cin}")
     if nhwc and cout % 8 != 0:
@@ -115,11 +119,13 @@ def _check(x, weight, bias, out_dtype, k):
     return x, wt.to(x.device).contiguous(), b, nhwc, (n, cin, h, w, cout)
 
 
-def _conv(x, weight, bias, out_dtype, k, stats):
-    x, wt, b, nhwc, (n, cin, h, w, cout) = _check(x, weight, bias, out_dtype, k)
+def _conv(x, weight, bias, out_dtype, k, stats, stride=1):
+    x, wt, b, nhwc, (n, cin, h, w, cout) = _check(x, weight, bias, out_dtype, k, stride)
     lib = _lib.load()
     dev = x.device
-    z = torch.empty((n, cout, h, w), dtype=out_dtype, device=dev,
+    pad = k // 2
+    ho, wo = (h + 2 * pad - k) // stride + 1, (w + 2 * pad - k) // stride + 1
+    z = torch.empty((n, cout, ho, wo), dtype=out_dtype, device=dev,
                     memory_format=torch.channels_last if nhwc else torch.contiguous_format)
     bp = b.data_ptr() if b is not None else None
     st = stream_ptr(dev)
@@ -127,18 +133,18 @@ def _conv(x, weight, bias, out_dtype, k, stats):
     partial = None
     if stats:
         partial = torch.empty(2 * cout + 1, dtype=torch.float64, device=dev)
-        nb = (lib.cgbn_conv_nhwc_ws_bytes(n, cout, h, w) if nhwc
+        nb = (lib.cgbn_conv_nhwc_ws_bytes(n, cout, h, w, k, stride) if nhwc
               else lib.cgbn_conv1x1_ws_bytes(n, cout, h * w))
         ws = _tile_scratch(dev, nb)
     name = f"conv{k}x{k}" + ("_stats" if stats else "")
     with _Span(name, 0):
         if nhwc and stats:
             rc = lib.cgbn_conv_nhwc_stats(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h, w, k,
-                                          od, z.data_ptr(), partial.data_ptr(), ws.data_ptr(),
-                                          ws.numel(), st)
+                                          stride, od, z.data_ptr(), partial.data_ptr(),
+                                          ws.data_ptr(), ws.numel(), st)
         elif nhwc:
-            rc = lib.cgbn_conv_nhwc(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h, w, k, od,
-                                    z.data_ptr(), st)
+            rc = lib.cgbn_conv_nhwc(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h, w, k,
+                                    stride, od, z.data_ptr(), st)
         elif stats:
             rc = lib.cgbn_conv1x1_stats(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h * w, od,
                                         z.data_ptr(), partial.data_ptr(), ws.data_ptr(),
@@ -150,47 +156,48 @@ def _conv(x, weight, bias, out_dtype, k, stats):
     return z, partial
 
 
-def conv1x1(x, weight, bias=None, out_dtype=torch.float32):
-    """z = conv1x1(x, weight) + bias on the tensor cores (the unfused producer). NCHW or
-    channels_last x; z has x's memory format."""
-    return _conv(x, weight, bias, out_dtype, 1, False)[0]
+def conv1x1(x, weight, bias=None, out_dtype=torch.float32, stride=1):
+    """z = conv1x1(x, weight, stride) + bias on the tensor cores (the unfused producer).
+    NCHW or channels_last x (stride 2: channels_last); z has x's memory format."""
+    return _conv(x, weight, bias, out_dtype, 1, False, stride)[0]
 
 
-def conv1x1_stats(x, weight, bias=None, out_dtype=torch.float32):
+def conv1x1_stats(x, weight, bias=None, out_dtype=torch.float32, stride=1):
     """(z, partial): the convolution plus this rank's forward partial of z (2C+1 fp64,
     [mean | M2 | count], the cgbn_fwd_stats format)."""
-    return _conv(x, weight, bias, out_dtype, 1, True)
+    return _conv(x, weight, bias, out_dtype, 1, True, stride)
 
 
-def conv3x3(x, weight, bias=None, out_dtype=torch.float32):
-    """z = conv3x3(x, weight, padding=1) + bias on the tensor cores (implicit GEMM over TMA
-    im2col loads; channels_last x and z) — the reference model's conv layer
+def conv3x3(x, weight, bias=None, out_dtype=torch.float32, stride=1):
+    """z = conv3x3(x, weight, padding=1, stride) + bias on the tensor cores (implicit GEMM
+    over TMA im2col loads; channels_last x and z) — the reference model's conv layer
     (model.py:235-242)."""
-    return _conv(x, weight, bias, out_dtype, 3, False)[0]
+    return _conv(x, weight, bias, out_dtype, 3, False, stride)[0]
 
 
-def conv3x3_stats(x, weight, bias=None, out_dtype=torch.float32):
+def conv3x3_stats(x, weight, bias=None, out_dtype=torch.float32, stride=1):
     """(z, partial) for the 3x3 convolution, as conv1x1_stats."""
-    return _conv(x, weight, bias, out_dtype, 3, True)
+    return _conv(x, weight, bias, out_dtype, 3, True, stride)
 
 
-def _fused_local(k, x, weight, state, bias, out_dtype, relu, what):
+def _fused_local(k, x, weight, state, bias, out_dtype, relu, what, stride=1):
     if _bn._exchange_mode != "merged":
-        z = _conv(x, weight, bias, out_dtype, k, False)[0]
+        z = _conv(x, weight, bias, out_dtype, k, False, stride)[0]
         y, cache = _bn.bn_forward_local(z, state, relu=relu)
         return y, cache, z
-    z, partial = _conv(x, weight, bias, out_dtype, k, True)
+    z, partial = _conv(x, weight, bias, out_dtype, k, True, stride)
     y, cache = _train_forward(z, state, _local_exchange, 1, None, one_pass=False, relu=relu,
                               what=what, partial=partial)
     return y, cache, z
 
 
-def _fused_sync(k, handle, x, weight, state, bias, out_dtype, one_pass, relu, what):
+def _fused_sync(k, handle, x, weight, state, bias, out_dtype, one_pass, relu, what,
+                stride=1):
     if _bn._exchange_mode != "merged":
-        z = _conv(x, weight, bias, out_dtype, k, False)[0]
+        z = _conv(x, weight, bias, out_dtype, k, False, stride)[0]
         y, cache = _bn.sync_bn_forward(handle, z, state, one_pass=one_pass, relu=relu)
         return y, cache, z
-    z, partial = _conv(x, weight, bias, out_dtype, k, True)
+    z, partial = _conv(x, weight, bias, out_dtype, k, True, stride)
     scope_key = f"bn{handle.bn_group_index}"
     y, cache = _train_forward(
         z, state, lambda v, info: handle.exchange(SCOPE_BN_GROUP, "bn_forward", v, info),
@@ -200,34 +207,36 @@ def _fused_sync(k, handle, x, weight, state, bias, out_dtype, one_pass, relu, wh
 
 
 def conv3x3_bn_forward_local(x, weight, state: BNLayerState, bias=None,
-                             out_dtype=torch.float32, relu: bool = False):
+                             out_dtype=torch.float32, relu: bool = False, stride: int = 1):
     """bn_forward_local(conv3x3(x, weight) + bias, state), statistics from the conv
     epilogue (the reference model's conv -> bn pair, model.py:235-258). Returns
     (y, cache, z)."""
-    return _fused_local(3, x, weight, state, bias, out_dtype, relu, "conv3x3_bn_forward_local")
+    return _fused_local(3, x, weight, state, bias, out_dtype, relu, "conv3x3_bn_forward_local",
+                        stride)
 
 
 def sync_conv3x3_bn_forward(handle, x, weight, state: BNLayerState, bias=None,
                             out_dtype=torch.float32, one_pass: bool = False,
-                            relu: bool = False):
+                            relu: bool = False, stride: int = 1):
     """sync_bn_forward(handle, conv3x3(x, weight) + bias, state), statistics from the
     conv epilogue. Returns (y, cache, z)."""
     return _fused_sync(3, handle, x, weight, state, bias, out_dtype, one_pass, relu,
-                       "sync_conv3x3_bn_forward")
+                       "sync_conv3x3_bn_forward", stride)
 
 
 def conv1x1_bn_forward_local(x, weight, state: BNLayerState, bias=None,
-                             out_dtype=torch.float32, relu: bool = False):
+                             out_dtype=torch.float32, relu: bool = False, stride: int = 1):
     """bn_forward_local(conv1x1(x, weight) + bias, state) with the statistics taken in the
     conv epilogue. Returns (y, cache, z); cache is the BN cache over z."""
-    return _fused_local(1, x, weight, state, bias, out_dtype, relu, "conv1x1_bn_forward_local")
+    return _fused_local(1, x, weight, state, bias, out_dtype, relu, "conv1x1_bn_forward_local",
+                        stride)
 
 
 def sync_conv1x1_bn_forward(handle, x, weight, state: BNLayerState, bias=None,
                             out_dtype=torch.float32, one_pass: bool = False,
-                            relu: bool = False):
+                            relu: bool = False, stride: int = 1):
     """sync_bn_forward(handle, conv1x1(x, weight) + bias, state) with the statistics taken
     in the conv epilogue; the partial goes through the BN group's exchange unchanged.
     Returns (y, cache, z)."""
     return _fused_sync(1, handle, x, weight, state, bias, out_dtype, one_pass, relu,
-                       "sync_conv1x1_bn_forward")
+                       "sync_conv1x1_bn_forward", stride)

@@ -80,9 +80,9 @@ def test_producer_conv_argument_validation_without_gpu():
     lib = _lib.load()
     rc = lib.cgbn_conv1x1(None, None, None, 2, 64, 128, 64, 0, None, None)
     assert rc == _lib.ERR_INVALID and b"null" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 64, 128, 8, 8, 2, 0, 16, None)
+    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 64, 128, 8, 8, 2, 1, 0, 16, None)
     assert rc == _lib.ERR_INVALID and b"ksize" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 60, 128, 8, 8, 3, 0, 16, None)
+    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 60, 128, 8, 8, 3, 1, 0, 16, None)
     assert rc == _lib.ERR_UNSUPPORTED and b"Cin" in lib.cgbn_last_error()
     rc = lib.cgbn_conv1x1(16, 16, None, 2, 64, 128, 49, 0, 16, None)
     assert rc == _lib.ERR_UNSUPPORTED and b"H*W" in lib.cgbn_last_error()
@@ -90,5 +90,5 @@ def test_producer_conv_argument_validation_without_gpu():
     assert rc == _lib.ERR_INVALID and b"dtype" in lib.cgbn_last_error()
     rc = lib.cgbn_conv1x1_stats(16, 16, None, 2, 64, 128, 64, 0, 16, None, None, 0, None)
     assert rc == _lib.ERR_INVALID and b"partial" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv_nhwc_stats(16, 16, None, 2, 64, 128, 8, 8, 3, 0, 16, 16, 16, 0, None)
+    rc = lib.cgbn_conv_nhwc_stats(16, 16, None, 2, 64, 128, 8, 8, 3, 2, 0, 16, 16, 16, 0, None)
     assert rc == _lib.ERR_INVALID and b"workspace" in lib.cgbn_last_error()

@@ -341,3 +341,51 @@ def test_conv3x3_needs_channels_last():
     wt = torch.randn(64, 64, 3, 3, device=DEV).to(torch.bfloat16)
     with pytest.raises(cg.BatchNormError, match="channels_last"):
         P.conv3x3(x, wt)
+
+
+STRIDED = [
+    # k, n, cin, cout, (h, w): stride 2 (ResNet's first-block conv2 and 1x1 downsample)
+    (3, 2, 64, 128, (56, 56)),
+    (3, 3, 128, 64, (15, 9)),    # odd extents: Ho = 8, Wo = 5
+    (1, 2, 256, 512, (56, 56)),  # the 1x1 downsample
+    (1, 1, 64, 72, (7, 13)),
+]
+
+
+@pytest.mark.parametrize("k,n,cin,cout,hw", STRIDED)
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_strided_conv_channels_last(k, n, cin, cout, hw, out_dtype):
+    if k == 3:
+        x, wt, b = _operands3(n, cin, cout, hw, seed=k + cin + cout, bias=True)
+        z, partial = P.conv3x3_stats(_cl(x.to(DEV)), wt.to(DEV), b, out_dtype=out_dtype,
+                                     stride=2)
+    else:
+        x, wt, b = _operands(n, cin, cout, hw, seed=k + cin + cout, bias=True)
+        z, partial = P.conv1x1_stats(_cl(x.to(DEV)), wt.to(DEV), b, out_dtype=out_dtype,
+                                     stride=2)
+    torch.cuda.synchronize()
+    w4 = wt.double() if k == 3 else wt.double()[:, :, None, None]
+    ref = torch.nn.functional.conv2d(x.double(), w4, stride=2, padding=k // 2)
+    ref = ref + b.double()[None, :, None, None]
+    assert z.shape == ref.shape and z.is_contiguous(memory_format=torch.channels_last)
+    tol = 1e-5 if out_dtype == torch.float32 else 8e-3
+    assert O.rel_err(z.double().cpu().numpy(), ref.numpy(), floor=float(ref.abs().max())) <= tol
+    mean, m2, cnt = _stats64(z)
+    _check_partial(partial.cpu().numpy(), mean, m2, cnt, cout)
+
+
+def test_strided_fused_bn_forward_matches_oracle():
+    x, wt, b = _operands3(4, 64, 128, (28, 28), seed=77, loc=0.3, bias=True)
+    st = cg.BNLayerState.create(128, device=DEV)
+    y, cache, z = P.conv3x3_bn_forward_local(_cl(x.to(DEV)), wt.to(DEV), st, bias=b, stride=2)
+    assert z.shape == (4, 128, 14, 14)
+    ref = O.cgbn_world([z.double().cpu().numpy()], np.ones(128), np.zeros(128), 1)[0]
+    assert O.rel_err(y.double().cpu().numpy(), ref["y"]) <= 1e-5
+    assert O.rel_err(cache.var.cpu().numpy(), ref["var"]) <= 1e-5
+
+
+def test_strided_nchw_raises():
+    x = torch.randn(2, 64, 8, 8, device=DEV).to(torch.bfloat16)
+    wt = torch.randn(64, 64, device=DEV).to(torch.bfloat16)
+    with pytest.raises(cg.BatchNormError, match="channels_last"):
+        P.conv1x1(x, wt, stride=2)
