@@ -192,6 +192,38 @@ int cgbn_p2p_exchange(const double* vec, int64_t n, int rank, int G, void* const
 int cgbn_p2p_emulate(const double* vecs, int64_t n, int G, void* const* regions, int64_t max_len,
                      double* outs, unsigned* status, double timeout_s, int skip, void* stream);
 
+/* The P2P exchange fused into the kernels on either side of it (SURVEY 8(e) backend 3:
+ * "the same fused into the K1/K4a tail"); no exchange kernel of its own. Same regions and
+ * protocol as cgbn_p2p_exchange (the region layout carries a finisher counter for this):
+ *  - cgbn_fwd_stats_p2p / cgbn_bwd_reduce_p2p: the statistics reduction whose channel
+ *    finishers write the rank's partial straight into row `rank` of every region of the
+ *    group (the epoch parity comes from the own region's counter); the last finisher
+ *    advances the epoch and publishes the rank's flag in every region (release, system
+ *    scope). Replaces cgbn_fwd_stats / cgbn_bwd_reduce + cgbn_p2p_exchange.
+ *  - cgbn_fwd_normalize_p2p / cgbn_bwd_dx_p2p: the finalize kernel first waits for every
+ *    rank's flag of the current epoch in the own region (acquire; timeout_s ->
+ *    CGBN_STATUS_EXCHANGE_TIMEOUT in *status), folds the G rows read there in ascending
+ *    rank order, then the elementwise pass. Same outputs as cgbn_fwd_normalize /
+ *    cgbn_bwd_dx on the gathered partials (bitwise).
+ * G <= 8 (one NVSwitch box) for the fused variant. */
+int cgbn_fwd_stats_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank,
+                       int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes,
+                       void* stream);
+int cgbn_fwd_normalize_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                           void* region, int G, int64_t max_len, double timeout_s,
+                           const float* gamma, const float* beta, double eps, double momentum,
+                           float* running_mean, float* running_var, double* saved, int relu,
+                           void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_reduce_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
+                        int layout, const double* saved, const float* gamma, const float* beta,
+                        int relu, int rank, int G, void* const* regions, int64_t max_len,
+                        void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_dx_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                    void* region, int G, int64_t max_len, double timeout_s, const double* saved,
+                    const float* gamma, const float* beta, double eps, int relu, void* dx,
+                    float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
+                    void* stream);
+
 /* Ascending-rank fold of G device vectors of n elements (dtype CGBN_DTYPE_F32/F64):
  * out = v[0] + v[1] + ... + v[G-1], evaluated left to right. This is the arithmetic of
  * the reference's allreduce_sum at the root (collectives.py:293-295); the transport

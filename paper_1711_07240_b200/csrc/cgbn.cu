@@ -514,6 +514,146 @@ int cgbn_p2p_emulate(const double* vecs, int64_t n, int G, void* const* regions,
   return check_launch("cgbn_p2p_emulate");
 }
 
+// ---- fused exchange (SURVEY 8(e) backend 3): the reductions' finishers push the rank's
+// partial into every region and the last one publishes; the finalize kernel waits.
+
+namespace {
+int make_push(p2p::Push* P, int rank, int G, void* const* regions, int64_t max_len,
+              int64_t need, int64_t C) {
+  if (G < 1 || G > p2p::kMaxPush)
+    return set_error(CGBN_ERR_INVALID, "fused exchange: group size %d outside [1, %d]", G,
+                     p2p::kMaxPush);
+  if (rank < 0 || rank >= G) return set_error(CGBN_ERR_INVALID, "rank %d outside [0, %d)", rank, G);
+  if (!regions) return set_error(CGBN_ERR_INVALID, "regions array is NULL");
+  if (need > max_len)
+    return set_error(CGBN_ERR_INVALID, "partial of %lld values exceeds max_len %lld",
+                     (long long)need, (long long)max_len);
+  for (int q = 0; q < G; ++q) {
+    if (!regions[q]) return set_error(CGBN_ERR_INVALID, "regions[%d] is NULL", q);
+    P->base[q] = static_cast<char*>(regions[q]);
+  }
+  for (int q = G; q < p2p::kMaxPush; ++q) P->base[q] = nullptr;
+  P->rank = rank;
+  P->G = G;
+  P->max_len = max_len;
+  P->nfinish = (unsigned)C;
+  return CGBN_OK;
+}
+
+int make_pull(p2p::Pull* P, void* region, int G, int64_t max_len, int64_t need,
+              unsigned* status, double timeout_s) {
+  if (G < 1 || G > p2p::kMaxPeers)
+    return set_error(CGBN_ERR_INVALID, "group size %d outside [1, %d]", G, p2p::kMaxPeers);
+  if (!region) return set_error(CGBN_ERR_INVALID, "region is NULL");
+  if (need > max_len)
+    return set_error(CGBN_ERR_INVALID, "partial of %lld values exceeds max_len %lld",
+                     (long long)need, (long long)max_len);
+  if (!(timeout_s > 0.0)) return set_error(CGBN_ERR_INVALID, "timeout must be positive");
+  P->own = static_cast<char*>(region);
+  P->G = G;
+  P->max_len = max_len;
+  P->status = status;
+  P->timeout_ns = (uint64_t)(timeout_s * 1e9);
+  return CGBN_OK;
+}
+
+struct PushScope {  // the push applies to the reductions dispatched while it is alive
+  explicit PushScope(const p2p::Push* p) { g_push = p; }
+  ~PushScope() { g_push = nullptr; }
+};
+}  // namespace
+
+int cgbn_fwd_stats_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank,
+                       int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes,
+                       void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_REQUIRE(x, "cgbn_fwd_stats_p2p: NULL pointer");
+  const void* ptrs[] = {x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, act, ptrs, 1, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  p2p::Push push;
+  CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C + 1, C));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  pl.tma = false;
+  PushScope scope(&push);
+  CGBN_TRY(dispatch_stats(pl, x, true, kPartial, nullptr, nullptr, nullptr, w, st));
+  return check_launch("cgbn_fwd_stats_p2p");
+}
+
+int cgbn_fwd_normalize_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                           void* region, int G, int64_t max_len, double timeout_s,
+                           const float* gamma, const float* beta, double eps, double momentum,
+                           float* running_mean, float* running_var, double* saved, int relu,
+                           void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  const void* ptrs[] = {x, y};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 2, &ep));
+  p2p::Pull pull;
+  CGBN_TRY(make_pull(&pull, region, G, max_len, 2 * C + 1, status, timeout_s));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  launch_pdl(k_finalize_fwd_p2p, chan_blocks(C), true, st, pull, F);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  return check_launch("cgbn_fwd_normalize_p2p");
+}
+
+int cgbn_bwd_reduce_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
+                        int layout, const double* saved, const float* gamma, const float* beta,
+                        int relu, int rank, int G, void* const* regions, int64_t max_len,
+                        void* ws, size_t ws_bytes, void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_REQUIRE(dy && x && saved, "cgbn_bwd_reduce_p2p: NULL pointer");
+  CGBN_REQUIRE(!relu || (gamma && beta), "cgbn_bwd_reduce_p2p: relu needs gamma and beta");
+  const void* ptrs[] = {dy, x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, act, ptrs, 2, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  p2p::Push push;
+  CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C, C));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  pl.tma = false;
+  PushScope scope(&push);
+  CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, nullptr,
+                               nullptr, w, st));
+  return check_launch("cgbn_bwd_reduce_p2p");
+}
+
+int cgbn_bwd_dx_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                    void* region, int G, int64_t max_len, double timeout_s, const double* saved,
+                    const float* gamma, const float* beta, double eps, int relu, void* dx,
+                    float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
+                    void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_dx_p2p: NULL pointer");
+  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
+  CGBN_REQUIRE(!relu || beta, "cgbn_bwd_dx_p2p: relu needs beta");
+  const void* ptrs[] = {dy, x, dx};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 3, &ep));
+  p2p::Pull pull;
+  CGBN_TRY(make_pull(&pull, region, G, max_len, 2 * C, status, timeout_s));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const BwdFinal F =
+      make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
+  launch_pdl(k_finalize_bwd_p2p, chan_blocks(C), true, st, pull, F);
+  launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
+  return check_launch("cgbn_bwd_dx_p2p");
+}
+
 int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void* out,
                   void* stream) {
   CGBN_REQUIRE(vectors && out, "cgbn_fold_sum: NULL pointer");

@@ -158,6 +158,117 @@ struct Parts {
   int G;
 };
 
+}  // namespace
+
+// ----------------------------------------------------------------------------------
+// One-shot P2P exchange regions (cgbn_p2p.cuh; fused into the reductions' finishers by
+// the *_p2p entry points). Every rank of a BN group owns one region, shared with the group
+// through CUDA IPC:
+//   [ epoch counter (u64) | flags[G] (u64) | done (u32, padded) | recv[2][G][max_len] (f64) ]
+// `done` counts the channel finishers of a fused reduction; the last one publishes.
+namespace p2p {
+
+__host__ __device__ inline size_t flags_off() { return 8; }
+__host__ __device__ inline size_t done_off(int G) { return 8 + (size_t)G * 8; }
+__host__ __device__ inline size_t recv_off(int G) { return (done_off(G) + 8 + 15) / 16 * 16; }
+__host__ __device__ inline size_t region_bytes(int G, int64_t max_len) {
+  return recv_off(G) + 2 * (size_t)G * (size_t)max_len * sizeof(double);
+}
+
+__device__ __forceinline__ unsigned long long* flag_ptr(char* region, int q) {
+  return reinterpret_cast<unsigned long long*>(region + flags_off()) + q;
+}
+__device__ __forceinline__ double* recv_ptr(char* region, int G, int64_t max_len, int parity,
+                                            int q) {
+  return reinterpret_cast<double*>(region + recv_off(G)) +
+         ((size_t)parity * G + q) * (size_t)max_len;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The producer side of a fused exchange: this rank's row of every region, epoch parity
+// from the own region's counter (read by every finisher before the last one advances it).
+// At most kMaxPush ranks (one NVSwitch box): the pointers stay a small, statically
+// indexed part of every reduction Op's kernel parameters.
+constexpr int kMaxPush = 8;
+struct Push {
+  char* base[kMaxPush];  // region of every rank of the group (own at [rank])
+  int rank, G;           // G == 0: no push (the finisher writes `out`)
+  int64_t max_len;
+  unsigned nfinish;      // finisher calls per launch (one per channel)
+};
+
+__device__ __forceinline__ char* push_own(const Push& P) {
+  char* own = nullptr;
+#pragma unroll
+  for (int q = 0; q < kMaxPush; ++q)
+    if (q == P.rank) own = P.base[q];
+  return own;
+}
+__device__ __forceinline__ unsigned long long push_epoch(const Push& P) {
+  return *reinterpret_cast<volatile unsigned long long*>(push_own(P)) + 1ull;
+}
+
+// After a finisher wrote its channel into every region: fence, count, and the last
+// finisher advances the epoch and publishes this rank's flag in every region.
+__device__ __forceinline__ void push_done(const Push& P, unsigned long long e) {
+  __threadfence_system();
+  char* own = push_own(P);
+  unsigned* done = reinterpret_cast<unsigned*>(own + done_off(P.G));
+  if (atomicAdd(done, 1u) == P.nfinish - 1) {
+    *done = 0u;
+    *reinterpret_cast<volatile unsigned long long*>(own) = e;
+    __threadfence_system();
+#pragma unroll
+    for (int q = 0; q < kMaxPush; ++q)
+      if (q < P.G) st_release_sys(flag_ptr(P.base[q], P.rank), e);
+  }
+}
+
+// The consumer side: wait for every rank's flag of the current epoch (own counter), with
+// a globaltimer timeout that sets CGBN_STATUS_EXCHANGE_TIMEOUT instead of hanging.
+struct Pull {
+  char* own;
+  int G;
+  int64_t max_len;
+  unsigned* status;
+  uint64_t timeout_ns;
+};
+
+// Called by every thread of a block; returns the epoch. Threads q < G spin on flag q.
+__device__ __forceinline__ unsigned long long pull_wait(const Pull& P) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(P.own);
+  if ((int)threadIdx.x < P.G) {
+    const unsigned long long* f = flag_ptr(P.own, threadIdx.x);
+    const uint64_t t0 = now_ns();
+    while (ld_acquire_sys(f) < e) {
+      if (now_ns() - t0 > P.timeout_ns) {
+        if (P.status) atomicOr(P.status, CGBN_STATUS_EXCHANGE_TIMEOUT);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+  return e;
+}
+
+}  // namespace p2p
+
+namespace {
+
 // ----------------------------------------------------------------------------------
 // Vector load / store of activation elements (fp32, bf16 or fp16 storage; every kernel
 // computes in fp64 and rounds once on output).

@@ -32,6 +32,41 @@ __global__ void k_finalize_bwd(Parts parts, BwdFinal F) {
   finalize_bwd_channel(F, c, sdy, sdyx, true);
 }
 
+// The same after a fused exchange: every block waits for the group's flags of the current
+// epoch in its own region, then folds the G rows (ascending rank order) read there.
+__global__ void k_finalize_fwd_p2p(p2p::Pull pull, FwdFinal F) {
+  pdl_wait();
+  const unsigned long long e = p2p::pull_wait(pull);
+  pdl_trigger();
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= F.C) return;
+  Parts parts;
+  parts.G = pull.G;
+  for (int r = 0; r < pull.G; ++r)
+    parts.p[r] = p2p::recv_ptr(pull.own, pull.G, pull.max_len, (int)(e & 1ull), r);
+  double n, mean, M2, P, Q;
+  merge_fwd_partials(parts, c, F.C, n, mean, M2);
+  finalize_fwd_channel(F, c, n, mean, M2, true, P, Q);
+}
+
+__global__ void k_finalize_bwd_p2p(p2p::Pull pull, BwdFinal F) {
+  pdl_wait();
+  const unsigned long long e = p2p::pull_wait(pull);
+  pdl_trigger();
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= F.C) return;
+  const uint32_t C = F.C;
+  const int par = (int)(e & 1ull);
+  const double* r0 = p2p::recv_ptr(pull.own, pull.G, pull.max_len, par, 0);
+  double sdy = r0[c], sdyx = r0[C + c];
+  for (int r = 1; r < pull.G; ++r) {  // ascending rank fold (collectives.py:293-295)
+    const double* rr = p2p::recv_ptr(pull.own, pull.G, pull.max_len, par, r);
+    sdy += rr[c];
+    sdyx += rr[C + c];
+  }
+  finalize_bwd_channel(F, c, sdy, sdyx, true);
+}
+
 // Eval (batchnorm.py:158-166) and x_hat coefficient tables.
 // Reference-literal statistics (batchnorm.py:119-132): group sums [sum | sq | m] ->
 // mean = sum/m, var = sq/m (two-pass: sq = sum (x - mean)^2) or max(sq/m - mean^2, 0)

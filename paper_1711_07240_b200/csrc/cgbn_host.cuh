@@ -491,6 +491,20 @@ int launch_rows(const Plan& pl, const NOp& nop, const Op& op, double* out, const
   return CGBN_OK;
 }
 
+// The fused-exchange push of the *_p2p entry points (thread-local: set around one
+// dispatch by the calling thread; every other call reduces into `out`).
+thread_local const p2p::Push* g_push = nullptr;
+
+p2p::Push current_push() {
+  if (g_push) return *g_push;
+  p2p::Push none;
+  none.G = 0;
+  none.rank = 0;
+  none.max_len = 0;
+  none.nfinish = 0;
+  return none;
+}
+
 // Forward statistics in mode kPartial / kRawSums / kLocalFinal / kSumSq.
 template <class T, int VEC>
 int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out, double* out2,
@@ -498,7 +512,7 @@ int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out,
               const double* kcount) {
   const T* x = static_cast<const T*>(xv);
   if constexpr (std::is_same<T, float>::value && VEC == 4) {
-    if (pl.tma && shift && mode == kPartial) {
+    if (pl.tma && shift && mode == kPartial && !g_push) {
       tma::TmaStats op;
       op.x = x;
       op.K = 0.0;
@@ -513,6 +527,7 @@ int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out,
   op.kcount = kcount;
   op.mode = mode;
   op.out2 = out2;
+  op.push = current_push();
   if (F) op.F = *F;
   if constexpr (VEC == 1) {
     if (pl.rows) {
@@ -532,7 +547,7 @@ int run_bwd_reduce(const Plan& pl, const void* dyv, const void* xv, const double
   const T* dy = static_cast<const T*>(dyv);
   const T* x = static_cast<const T*>(xv);
   if constexpr (std::is_same<T, float>::value && VEC == 4) {
-    if (pl.tma && mode == kPartial) {
+    if (pl.tma && mode == kPartial && !g_push) {
       tma::TmaBwd<RELU> op;
       op.dy = dy;
       op.x = x;
@@ -551,6 +566,7 @@ int run_bwd_reduce(const Plan& pl, const void* dyv, const void* xv, const double
   op.beta = beta;
   op.mean = op.P = op.Q = 0.0;
   op.mode = mode;
+  op.push = current_push();
   if (F) op.F = *F;
   if constexpr (VEC == 1) {
     if (pl.rows) {

@@ -263,6 +263,7 @@ struct StatsOp {
   int mode;                   // FinishMode
   double* __restrict__ out2;  // kRawSums: sum_sq destination (may be null)
   FwdFinal F;                 // kLocalFinal
+  p2p::Push push;             // kPartial with push.G > 0: rows go to the group's regions
   struct Regs { Vec<T, VEC> v; uint32_t m; };
   struct Init { double K; };
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
@@ -310,7 +311,19 @@ struct StatsOp {
     }
     const double mean = K + S1 / n;
     const double M2 = fmax(S2 - S1 * (S1 / n), 0.0);
-    if (mode == kPartial) {
+    if (mode == kPartial && push.G > 0) {
+      // fused exchange: this channel straight into row `rank` of every rank's region
+      const unsigned long long e = p2p::push_epoch(push);
+#pragma unroll
+      for (int q = 0; q < p2p::kMaxPush; ++q) {
+        if (q >= push.G) break;
+        double* dst = p2p::recv_ptr(push.base[q], push.G, push.max_len, (int)(e & 1ull), push.rank);
+        dst[c] = mean;
+        dst[g.C + c] = M2;
+        if (c == 0) dst[2 * g.C] = n;
+      }
+      p2p::push_done(push, e);
+    } else if (mode == kPartial) {
       out[c] = mean;
       out[g.C + c] = M2;
       if (c == 0) out[2 * g.C] = n;
@@ -337,6 +350,7 @@ struct BwdOp {
   double mean, P, Q;
   int mode;    // kPartial or kLocalFinal
   BwdFinal F;  // kLocalFinal
+  p2p::Push push;  // kPartial with push.G > 0: rows go to the group's regions
   struct Regs { Vec<T, VEC> g, x; uint32_t m; };
   struct Init { double mean; };  // finish() needs no per-channel state
   __device__ __forceinline__ void init(const Geom& g, uint32_t c) {
@@ -381,7 +395,17 @@ struct BwdOp {
   }
   __device__ __forceinline__ void finish(const Geom& g, uint32_t c, double S1, double S2,
                                          double* __restrict__ out, const Pre& pre) const {
-    if (mode == kPartial) {
+    if (mode == kPartial && push.G > 0) {
+      const unsigned long long e = p2p::push_epoch(push);
+#pragma unroll
+      for (int q = 0; q < p2p::kMaxPush; ++q) {
+        if (q >= push.G) break;
+        double* dst = p2p::recv_ptr(push.base[q], push.G, push.max_len, (int)(e & 1ull), push.rank);
+        dst[c] = S1;
+        dst[g.C + c] = S2;
+      }
+      p2p::push_done(push, e);
+    } else if (mode == kPartial) {
       out[c] = S1;
       out[g.C + c] = S2;
     } else {

@@ -5,8 +5,10 @@
 // Every rank of a BN group owns one region of device memory, shared with the group
 // through CUDA IPC (cgbn_p2p_alloc / cgbn_p2p_open):
 //
-//   [ epoch counter (u64, local) | flags[G] (u64) | recv[2][G][max_len] (f64) ]
+//   [ epoch counter (u64, local) | flags[G] (u64) | done | recv[2][G][max_len] (f64) ]
 //
+// (the `done` word serves the fused variant, where the statistics kernel's finishers push
+// their channels directly and the finalize kernel waits: cgbn_*_p2p)
 // One exchange = one single-CTA kernel per rank:
 //   1. epoch = ++counter (device-side, so CUDA-graph replays advance it);
 //   2. push: the rank writes its vector into recv[epoch & 1][rank] of every region
@@ -34,37 +36,10 @@ constexpr int kThreadsP2P = 256;
 constexpr int kMaxPeers = CGBN_MAX_GROUP;
 
 struct Peers {
-  char* base[kMaxPeers];  // region of every rank of the group (own region at [rank])
+  char* base[kMaxPeers];  // region of every rank of the group (own at [rank])
 };
 
-__host__ __device__ inline size_t flags_off() { return 8; }
-__host__ __device__ inline size_t recv_off(int G) { return 8 + ((size_t)G * 8 + 15) / 16 * 16; }
-__host__ __device__ inline size_t region_bytes(int G, int64_t max_len) {
-  return recv_off(G) + 2 * (size_t)G * (size_t)max_len * sizeof(double);
-}
-
-__device__ __forceinline__ unsigned long long* flag_ptr(char* region, int q) {
-  return reinterpret_cast<unsigned long long*>(region + flags_off()) + q;
-}
-__device__ __forceinline__ double* recv_ptr(char* region, int G, int64_t max_len, int parity,
-                                            int q) {
-  return reinterpret_cast<double*>(region + recv_off(G)) +
-         ((size_t)parity * G + q) * (size_t)max_len;
-}
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t now_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
+// (region layout, flags and the acquire / release helpers: cgbn_common.cuh)
 
 // One rank's exchange, executed by one CTA (blockDim.x threads, >= G).
 __device__ void exchange_rank(const double* __restrict__ vec, int64_t n, int rank, int G,
