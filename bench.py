@@ -561,9 +561,11 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
     rep["nccl"] = {f"C{c}_us": time_exchange(hn, c) for c in (256, 2048)}
     rep["nccl"]["how"] = "all_gather_into_tensor of the fp64 partial (2C+1), eager"
     hp, ok = None, 0  # the self-test runs only if every rank set the P2P handle up
-    if requested in ("auto", "p2p"):
+    if requested in ("auto", "p2p", "p2p_fused"):
         try:
-            hp = cg.DistHandle(bn_group_size=world, transport="p2p", p2p_timeout_s=1.0)
+            hp = cg.DistHandle(bn_group_size=world,
+                               transport="p2p_fused" if requested == "p2p_fused" else "p2p",
+                               p2p_timeout_s=1.0)
             ok = 1
         except Exception as exc:  # noqa: BLE001
             rep["p2p_error"] = repr(exc)[:300]
@@ -580,6 +582,17 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
                 rp, _ = hp.exchange(cg.SCOPE_BN_GROUP, "selftest", v)
                 rn, _ = hn.exchange(cg.SCOPE_BN_GROUP, "selftest", v)
                 good = good and all(torch.equal(a, b) for a, b in zip(rp, rn))
+            if requested == "p2p_fused":
+                # the fused path (push in the reduction, wait in the finalize) through the
+                # BN API: bitwise equal to the NCCL path
+                xs = torch.randn(4, 64, 14, 14, device=dev, generator=gen)
+                st_f = cg.BNLayerState.create(64, device=dev)
+                st_n = cg.BNLayerState.create(64, device=dev)
+                y_f, c_f = cg.sync_bn_forward(hp, xs, st_f)
+                y_n, c_n = cg.sync_bn_forward(hn, xs, st_n)
+                dx_f = cg.sync_bn_backward(hp, xs, c_f, st_f)[0]
+                dx_n = cg.sync_bn_backward(hn, xs, c_n, st_n)[0]
+                good = good and torch.equal(y_f, y_n) and torch.equal(dx_f, dx_n)
             cg.check_status(dev)  # raises on an exchange timeout
             ok = int(good)
         except Exception as exc:  # noqa: BLE001 - reported; NCCL stays available
@@ -588,14 +601,20 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
         t = torch.tensor([ok], device=dev, dtype=torch.int32)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         ok = int(t.item())
-    if requested in ("auto", "p2p"):
+    if requested in ("auto", "p2p", "p2p_fused"):
         rep["p2p_selftest"] = "passed" if ok else "failed"
         if ok:
             rep["p2p"] = {f"C{c}_us": time_exchange(hp, c) for c in (256, 2048)}
             rep["p2p"]["how"] = ("one single-CTA kernel per rank: NVLink pushes into CUDA-IPC "
                                  "regions, release/acquire epoch flags, eager")
-    use_p2p = ok and (requested == "p2p" or rep["p2p"]["C256_us"] < rep["nccl"]["C256_us"])
-    rep["step_transport"] = "p2p" if use_p2p else "nccl"
+    use_p2p = ok and (requested in ("p2p", "p2p_fused")
+                      or rep["p2p"]["C256_us"] < rep["nccl"]["C256_us"])
+    rep["step_transport"] = (requested if requested == "p2p_fused" else "p2p") if use_p2p else "nccl"
+    if use_p2p and requested == "p2p_fused":
+        rep["p2p_fused_note"] = ("exchange fused into the kernels: the statistics reductions "
+                                 "push into the regions, the finalize kernels wait "
+                                 "(cgbn_*_p2p); the standalone P2P exchange latency is in "
+                                 "'p2p'")
     if hp is not None and not use_p2p:
         hp.close()
     return (hp if use_p2p else hn), rep
@@ -780,7 +799,7 @@ def run_gpu_arm(args):
     if world > 1:
         exch = dict(transport_report)
         exch["per_step_exchanges"] = 2 * len(shapes)
-        used = exch.get(exch["step_transport"], {})
+        used = exch.get({"p2p_fused": "p2p"}.get(exch["step_transport"], exch["step_transport"]), {})
         if "C256_us" in used:
             exch["est_share_of_step"] = used["C256_us"] * 2 * len(shapes) * 1e-3 / ms_step
 
@@ -927,9 +946,10 @@ def main():
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help=argparse.SUPPRESS)  # gloo: orchestration test on one GPU
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--transport", choices=["auto", "nccl", "p2p"], default="auto",
+    ap.add_argument("--transport", choices=["auto", "nccl", "p2p", "p2p_fused"], default="auto",
                     help="BN-group statistics exchange at N>1: NCCL all-gather, the one-shot "
-                         "P2P exchange, or auto (P2P if it passes its self-test and is faster)")
+                         "P2P exchange, the P2P exchange fused into the reduction / finalize "
+                         "kernels, or auto (P2P if it passes its self-test and is faster)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet50_bn_b32",
                     help="SURVEY 8(d) configuration (default: config 2, the driver's)")
     ap.add_argument("--no-graph", action="store_true")

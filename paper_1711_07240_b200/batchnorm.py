@@ -421,6 +421,24 @@ def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
         _raise_status(what, status, total)
         return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
                                  relu=bool(relu), one_pass=bool(one_pass), _total_count=total)
+    fused = getattr(exchange, "fused", None) if partial is None else None
+    if fused is not None:
+        # fused P2P exchange (cgbn_fwd_stats_p2p / cgbn_fwd_normalize_p2p): the reduction
+        # pushes the partial into every rank's region, the finalize waits for the flags
+        with _Span("fwd_stats", 4 * e):
+            _lib.check(lib.cgbn_fwd_stats_p2p(
+                g.x.data_ptr(), g.N, c, g.HW, g.layout, fused.idx, fused.G, fused.regions,
+                fused.max_len, ws.data_ptr(), ws.numel(), st), "cgbn_fwd_stats_p2p")
+        with _Span("fwd_normalize", 8 * e):
+            _lib.check(lib.cgbn_fwd_normalize_p2p(
+                g.x.data_ptr(), g.N, c, g.HW, g.layout, fused.own, fused.G, fused.max_len,
+                fused.timeout_s, state.gamma.data_ptr(), state.beta.data_ptr(),
+                float(state.eps), float(state.running_momentum), rm, rv, saved.data_ptr(),
+                int(bool(relu)), y.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                "cgbn_fwd_normalize_p2p")
+        _raise_status(what, status, None)
+        return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
+                                 relu=bool(relu), one_pass=bool(one_pass), _total_count=None)
     if partial is None:
         partial = torch.empty(2 * c + 1, dtype=torch.float64, device=dev)
         with _Span("fwd_stats", 4 * e):
@@ -482,6 +500,20 @@ def bn_forward_local(x, state: BNLayerState, mode: str = "train",
     return y, cache
 
 
+class _GroupExchange:
+    """The reduce_vec seam bound to a handle's BN-group exchange (batchnorm.py:183, 236);
+    ``fused`` is the handle's fused P2P exchange when it has one (DistHandle
+    transport="p2p_fused"), in which case the kernels do the exchange themselves."""
+
+    def __init__(self, handle, kind: str):
+        self.handle = handle
+        self.kind = kind
+        self.fused = getattr(handle, "fused_exchange", None)
+
+    def __call__(self, v, info):
+        return self.handle.exchange(SCOPE_BN_GROUP, self.kind, v, info)
+
+
 def sync_bn_forward(handle, x_local, state: BNLayerState, one_pass: bool = False,
                     relu: bool = False):
     """Training-mode batch normalization synchronized across a BN sub-group
@@ -495,8 +527,7 @@ def sync_bn_forward(handle, x_local, state: BNLayerState, one_pass: bool = False
     _check_layout(x_local, state)
     scope_key = f"bn{handle.bn_group_index}"
     return _train_forward(
-        x_local, state,
-        lambda v, info: handle.exchange(SCOPE_BN_GROUP, "bn_forward", v, info),
+        x_local, state, _GroupExchange(handle, "bn_forward"),
         handle.bn_group_size, scope_key, one_pass=one_pass, relu=relu, what="sync_bn_forward")
 
 
@@ -556,6 +587,23 @@ def _backward_core(dy, cache: BNForwardCache, state: BNLayerState, exchange, gro
                 "cgbn_bwd_local")
         _raise_status(what, status)
         return dx, dgamma, dbeta
+    fused = getattr(exchange, "fused", None)
+    if fused is not None and group_size > 1:
+        with _Span("bwd_reduce", 8 * e):
+            _lib.check(lib.cgbn_bwd_reduce_p2p(
+                gd.x.data_ptr(), gx.x.data_ptr(), gx.N, c, gx.HW, gx.layout, cache.saved.data_ptr(),
+                state.gamma.data_ptr(), state.beta.data_ptr(), int(cache.relu), fused.idx,
+                fused.G, fused.regions, fused.max_len, ws.data_ptr(), ws.numel(), st),
+                "cgbn_bwd_reduce_p2p")
+        with _Span("bwd_dx", 12 * e):
+            _lib.check(lib.cgbn_bwd_dx_p2p(
+                gd.x.data_ptr(), gx.x.data_ptr(), gx.N, c, gx.HW, gx.layout, fused.own, fused.G,
+                fused.max_len, fused.timeout_s, cache.saved.data_ptr(), state.gamma.data_ptr(),
+                state.beta.data_ptr(), float(state.eps), int(cache.relu), dx.data_ptr(),
+                dgamma.data_ptr(), dbeta.data_ptr(), status.data_ptr(), ws.data_ptr(),
+                ws.numel(), st), "cgbn_bwd_dx_p2p")
+        _raise_status(what, status)
+        return dx, dgamma, dbeta
     partial = torch.empty(2 * c, dtype=torch.float64, device=dev)
     with _Span("bwd_reduce", 8 * e):
         _lib.check(lib.cgbn_bwd_reduce(
@@ -590,10 +638,8 @@ def sync_bn_backward(handle, dy_local, cache: BNForwardCache, state: BNLayerStat
         raise BatchNormError(
             f"cache was produced under scope {cache.scope_key!r} but this device "
             f"belongs to {scope_key!r}")
-    return _backward_core(
-        dy_local, cache, state,
-        lambda v, info: handle.exchange(SCOPE_BN_GROUP, "bn_backward", v, info),
-        handle.bn_group_size, "sync_bn_backward")
+    return _backward_core(dy_local, cache, state, _GroupExchange(handle, "bn_backward"),
+                          handle.bn_group_size, "sync_bn_backward")
 
 
 def bn_update_running(state: BNLayerState, mu, var, count: int) -> BNLayerState:

@@ -422,6 +422,15 @@ class _P2PGroup:
             "cgbn_p2p_exchange")
         return [out[q * n:(q + 1) * n] for q in range(self.G)]
 
+    @property
+    def regions(self):
+        """ctypes array of the group's region pointers (own at [idx])."""
+        return self._regions
+
+    @property
+    def own(self) -> int:
+        return self._own
+
     def close(self):
         lib = _lib.load()
         with torch.cuda.device(self.device):
@@ -467,13 +476,19 @@ class DistHandle(_HandleBase):
             self._device = (torch.device("cuda", torch.cuda.current_device())
                             if backend == "nccl" else torch.device("cpu"))
         # statistics transport of the BN group: "nccl" (all-gather on the group's
-        # communicator) or "p2p" (one-shot NVLink exchange over CUDA-IPC regions,
-        # include/cgbn.h cgbn_p2p_*); world-scope collectives always use NCCL
-        if transport not in ("nccl", "p2p"):
-            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        # communicator), "p2p" (one-shot NVLink exchange over CUDA-IPC regions,
+        # include/cgbn.h cgbn_p2p_*) or "p2p_fused" (the same regions, with the push fused
+        # into the statistics reductions and the wait into the finalize kernels:
+        # cgbn_*_p2p, no exchange kernel; BN groups of at most 8); world-scope
+        # collectives always use NCCL
+        if transport not in ("nccl", "p2p", "p2p_fused"):
+            raise ValueError(
+                f"transport must be 'nccl', 'p2p' or 'p2p_fused', got {transport!r}")
+        if transport == "p2p_fused" and g > 8:
+            raise ValueError("the fused P2P exchange supports BN groups of at most 8 ranks")
         self.transport = transport
         self._p2p = None
-        if transport == "p2p" and g > 1:
+        if transport in ("p2p", "p2p_fused") and g > 1:
             if self._device.type != "cuda":
                 raise ValueError("the p2p transport needs a CUDA device")
             gi = self.rank // g
@@ -483,6 +498,16 @@ class DistHandle(_HandleBase):
 
     def __repr__(self):
         return f"DistHandle(rank={self.rank}, world={self.world_size}, g={self.bn_group_size})"
+
+    @property
+    def fused_exchange(self):
+        """The fused P2P exchange of the BN group (transport "p2p_fused", G > 1), else
+        None: the BN forward / backward then call the cgbn_*_p2p kernels instead of
+        reduction -> exchange -> finalize. With validate=True the BN layers keep the
+        unfused path, whose exchange() runs the protocol check."""
+        if self.transport != "p2p_fused" or self._p2p is None or self.validate:
+            return None
+        return self._p2p
 
     @property
     def device(self) -> torch.device:

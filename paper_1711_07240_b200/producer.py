@@ -202,7 +202,7 @@ def _fused_sync(k, handle, x, weight, state, bias, out_dtype, one_pass, relu, wh
     y, cache = _train_forward(
         z, state, lambda v, info: handle.exchange(SCOPE_BN_GROUP, "bn_forward", v, info),
         handle.bn_group_size, scope_key, one_pass=one_pass, relu=relu, what=what,
-        partial=partial)
+        partial=partial)  # (the partial comes from the conv: a fused P2P push does not apply)
     return y, cache, z
 
 
