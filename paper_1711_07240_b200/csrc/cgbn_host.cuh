@@ -495,17 +495,34 @@ int launch_rows(const Plan& pl, const NOp& nop, const Op& op, double* out, const
 // dispatch by the calling thread; every other call reduces into `out`).
 thread_local const p2p::Push* g_push = nullptr;
 
-p2p::Push current_push() {
-  if (g_push) return *g_push;
-  p2p::Push none;
-  none.G = 0;
-  none.rank = 0;
-  none.max_len = 0;
-  none.nfinish = 0;
-  return none;
+
+// Forward statistics in mode kPartial / kRawSums / kLocalFinal / kSumSq (PUSH: the
+// kPartial finisher pushes into the fused exchange's regions instead of `out`).
+template <class T, int VEC, bool PUSH>
+int run_stats_op(const Plan& pl, const T* x, bool shift, int mode, double* out, double* out2,
+                 const FwdFinal* F, const WsView& w, cudaStream_t st, const double* ksum,
+                 const double* kcount) {
+  StatsOp<T, VEC, PUSH> op;
+  op.x = x;
+  op.K = 0.0;
+  op.shift = shift;
+  op.ksum = ksum;
+  op.kcount = kcount;
+  op.mode = mode;
+  op.out2 = out2;
+  if constexpr (PUSH) op.push = *g_push;
+  if (F) op.F = *F;
+  if constexpr (VEC == 1) {
+    if (pl.rows) {
+      StatsRows<T, PUSH> nop;
+      nop.base = op;
+      nop.gg = pl.g;
+      return launch_rows(pl, nop, op, out, w, st);
+    }
+  }
+  return launch_reduce(pl, op, out, w, st);
 }
 
-// Forward statistics in mode kPartial / kRawSums / kLocalFinal / kSumSq.
 template <class T, int VEC>
 int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out, double* out2,
               const FwdFinal* F, const WsView& w, cudaStream_t st, const double* ksum,
@@ -519,19 +536,28 @@ int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out,
       return launch_tma_reduce(pl, op, out, w, st);
     }
   }
-  StatsOp<T, VEC> op;
+  if (g_push && mode == kPartial)
+    return run_stats_op<T, VEC, true>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+  return run_stats_op<T, VEC, false>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
+}
+
+template <class T, int VEC, bool RELU, bool PUSH>
+int run_bwd_op(const Plan& pl, const T* dy, const T* x, const double* saved, const float* gamma,
+               const float* beta, int mode, double* out, const BwdFinal* F, const WsView& w,
+               cudaStream_t st) {
+  BwdOp<T, VEC, RELU, PUSH> op;
+  op.dy = dy;
   op.x = x;
-  op.K = 0.0;
-  op.shift = shift;
-  op.ksum = ksum;
-  op.kcount = kcount;
+  op.saved = saved;
+  op.gamma = gamma;
+  op.beta = beta;
+  op.mean = op.P = op.Q = 0.0;
   op.mode = mode;
-  op.out2 = out2;
-  op.push = current_push();
+  if constexpr (PUSH) op.push = *g_push;
   if (F) op.F = *F;
   if constexpr (VEC == 1) {
     if (pl.rows) {
-      StatsRows<T> nop;
+      BwdRows<T, RELU, PUSH> nop;
       nop.base = op;
       nop.gg = pl.g;
       return launch_rows(pl, nop, op, out, w, st);
@@ -558,25 +584,9 @@ int run_bwd_reduce(const Plan& pl, const void* dyv, const void* xv, const double
       return launch_tma_reduce(pl, op, out, w, st);
     }
   }
-  BwdOp<T, VEC, RELU> op;
-  op.dy = dy;
-  op.x = x;
-  op.saved = saved;
-  op.gamma = gamma;
-  op.beta = beta;
-  op.mean = op.P = op.Q = 0.0;
-  op.mode = mode;
-  op.push = current_push();
-  if (F) op.F = *F;
-  if constexpr (VEC == 1) {
-    if (pl.rows) {
-      BwdRows<T, RELU> nop;
-      nop.base = op;
-      nop.gg = pl.g;
-      return launch_rows(pl, nop, op, out, w, st);
-    }
-  }
-  return launch_reduce(pl, op, out, w, st);
+  if (g_push && mode == kPartial)
+    return run_bwd_op<T, VEC, RELU, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
+  return run_bwd_op<T, VEC, RELU, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
 }
 
 // fp32: vector modes 1, 2, 4, 5 (masked float4); bf16 / fp16: 1, 2, 4, 8, 9 (masked 8).

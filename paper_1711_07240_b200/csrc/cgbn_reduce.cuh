@@ -249,18 +249,18 @@ struct NGeom {
 };
 
 // Forward statistics over rows: the shift K of every channel is the NCHW op's (row 0).
-template <class T>
+template <class T, bool PUSH = false>
 struct StatsRows {
   static constexpr int kU = 8;
   static constexpr int kIn = 1;
-  StatsOp<T, 1> base;
+  StatsOp<T, 1, PUSH> base;
   Geom gg;
   struct State { double K[4]; };
   struct Regs { Vec<T, 4> v; };
   __device__ __forceinline__ void init(uint32_t c4, State& s) const {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      StatsOp<T, 1> o = base;
+      StatsOp<T, 1, PUSH> o = base;
       o.init(gg, 4 * c4 + j);
       s.K[j] = o.K;
     }
@@ -278,18 +278,18 @@ struct StatsRows {
 };
 
 // Backward sums over rows: [sum g, sum g*(x - mean)] with the forward's ReLU mask.
-template <class T, bool RELU>
+template <class T, bool RELU, bool PUSH = false>
 struct BwdRows {
   static constexpr int kU = 4;
   static constexpr int kIn = 2;
-  BwdOp<T, 1, RELU> base;
+  BwdOp<T, 1, RELU, PUSH> base;
   Geom gg;
   struct State { double mean[4], P[4], Q[4]; };
   struct Regs { Vec<T, 4> g, x; };
   __device__ __forceinline__ void init(uint32_t c4, State& s) const {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      BwdOp<T, 1, RELU> o = base;
+      BwdOp<T, 1, RELU, PUSH> o = base;
       o.init(gg, 4 * c4 + j);
       s.mean[j] = o.mean;
       s.P[j] = RELU ? o.P : 0.0;
