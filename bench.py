@@ -563,8 +563,11 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
     hp, ok = None, 0  # the self-test runs only if every rank set the P2P handle up
     if requested in ("auto", "p2p", "p2p_fused"):
         try:
+            # auto and p2p_fused set the regions up for the fused variant too (G <= 8); a
+            # p2p_fused handle also serves plain P2P exchanges
+            fused_ok = requested in ("auto", "p2p_fused") and world <= 8
             hp = cg.DistHandle(bn_group_size=world,
-                               transport="p2p_fused" if requested == "p2p_fused" else "p2p",
+                               transport="p2p_fused" if fused_ok else "p2p",
                                p2p_timeout_s=1.0)
             ok = 1
         except Exception as exc:  # noqa: BLE001
@@ -582,19 +585,31 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
                 rp, _ = hp.exchange(cg.SCOPE_BN_GROUP, "selftest", v)
                 rn, _ = hn.exchange(cg.SCOPE_BN_GROUP, "selftest", v)
                 good = good and all(torch.equal(a, b) for a, b in zip(rp, rn))
-            if requested == "p2p_fused":
-                # the fused path (push in the reduction, wait in the finalize) through the
-                # BN API: bitwise equal to the NCCL path
-                xs = torch.randn(4, 64, 14, 14, device=dev, generator=gen)
-                st_f = cg.BNLayerState.create(64, device=dev)
-                st_n = cg.BNLayerState.create(64, device=dev)
-                y_f, c_f = cg.sync_bn_forward(hp, xs, st_f)
-                y_n, c_n = cg.sync_bn_forward(hn, xs, st_n)
-                dx_f = cg.sync_bn_backward(hp, xs, c_f, st_f)[0]
-                dx_n = cg.sync_bn_backward(hn, xs, c_n, st_n)[0]
-                good = good and torch.equal(y_f, y_n) and torch.equal(dx_f, dx_n)
             cg.check_status(dev)  # raises on an exchange timeout
             ok = int(good)
+            fgood = 0
+            if ok and hp.transport == "p2p_fused":
+                # the fused path (push in the reduction, wait in the finalize) through the
+                # BN API: bitwise equal to the NCCL path
+                try:
+                    xs = torch.randn(4, 64, 14, 14, device=dev, generator=gen)
+                    st_f = cg.BNLayerState.create(64, device=dev)
+                    st_n = cg.BNLayerState.create(64, device=dev)
+                    y_f, c_f = cg.sync_bn_forward(hp, xs, st_f)
+                    y_n, c_n = cg.sync_bn_forward(hn, xs, st_n)
+                    dx_f = cg.sync_bn_backward(hp, xs, c_f, st_f)[0]
+                    dx_n = cg.sync_bn_backward(hn, xs, c_n, st_n)[0]
+                    cg.check_status(dev)
+                    fgood = int(torch.equal(y_f, y_n) and torch.equal(dx_f, dx_n))
+                except Exception as exc:  # noqa: BLE001
+                    rep["p2p_fused_error"] = repr(exc)[:300]
+            tf = torch.tensor([fgood], device=dev, dtype=torch.int32)
+            dist.all_reduce(tf, op=dist.ReduceOp.MIN)
+            if not int(tf.item()):
+                hp.transport = "p2p"  # plain P2P exchanges; fused_exchange -> None
+                if requested == "p2p_fused":
+                    ok = 0
+            rep["p2p_fused_selftest"] = "passed" if int(tf.item()) else "failed or not run"
         except Exception as exc:  # noqa: BLE001 - reported; NCCL stays available
             rep["p2p_error"] = repr(exc)[:300]
             ok = 0
@@ -609,8 +624,8 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
                                  "regions, release/acquire epoch flags, eager")
     use_p2p = ok and (requested in ("p2p", "p2p_fused")
                       or rep["p2p"]["C256_us"] < rep["nccl"]["C256_us"])
-    rep["step_transport"] = (requested if requested == "p2p_fused" else "p2p") if use_p2p else "nccl"
-    if use_p2p and requested == "p2p_fused":
+    rep["step_transport"] = hp.transport if use_p2p else "nccl"
+    if use_p2p and hp.transport == "p2p_fused":
         rep["p2p_fused_note"] = ("exchange fused into the kernels: the statistics reductions "
                                  "push into the regions, the finalize kernels wait "
                                  "(cgbn_*_p2p); the standalone P2P exchange latency is in "
@@ -949,7 +964,8 @@ def main():
     ap.add_argument("--transport", choices=["auto", "nccl", "p2p", "p2p_fused"], default="auto",
                     help="BN-group statistics exchange at N>1: NCCL all-gather, the one-shot "
                          "P2P exchange, the P2P exchange fused into the reduction / finalize "
-                         "kernels, or auto (P2P if it passes its self-test and is faster)")
+                         "kernels, or auto (P2P if it passes its self-test and is faster than "
+                         "NCCL; fused when that also passes its BN-level self-test)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet50_bn_b32",
                     help="SURVEY 8(d) configuration (default: config 2, the driver's)")
     ap.add_argument("--no-graph", action="store_true")
