@@ -587,35 +587,36 @@ def select_transport(cg, torch, dist, dev, world, requested, barrier):
                 good = good and all(torch.equal(a, b) for a, b in zip(rp, rn))
             cg.check_status(dev)  # raises on an exchange timeout
             ok = int(good)
-            fgood = 0
-            if ok and hp.transport == "p2p_fused":
-                # the fused path (push in the reduction, wait in the finalize) through the
-                # BN API: bitwise equal to the NCCL path
-                try:
-                    xs = torch.randn(4, 64, 14, 14, device=dev, generator=gen)
-                    st_f = cg.BNLayerState.create(64, device=dev)
-                    st_n = cg.BNLayerState.create(64, device=dev)
-                    y_f, c_f = cg.sync_bn_forward(hp, xs, st_f)
-                    y_n, c_n = cg.sync_bn_forward(hn, xs, st_n)
-                    dx_f = cg.sync_bn_backward(hp, xs, c_f, st_f)[0]
-                    dx_n = cg.sync_bn_backward(hn, xs, c_n, st_n)[0]
-                    cg.check_status(dev)
-                    fgood = int(torch.equal(y_f, y_n) and torch.equal(dx_f, dx_n))
-                except Exception as exc:  # noqa: BLE001
-                    rep["p2p_fused_error"] = repr(exc)[:300]
-            tf = torch.tensor([fgood], device=dev, dtype=torch.int32)
-            dist.all_reduce(tf, op=dist.ReduceOp.MIN)
-            if not int(tf.item()):
-                hp.transport = "p2p"  # plain P2P exchanges; fused_exchange -> None
-                if requested == "p2p_fused":
-                    ok = 0
-            rep["p2p_fused_selftest"] = "passed" if int(tf.item()) else "failed or not run"
         except Exception as exc:  # noqa: BLE001 - reported; NCCL stays available
             rep["p2p_error"] = repr(exc)[:300]
             ok = 0
         t = torch.tensor([ok], device=dev, dtype=torch.int32)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         ok = int(t.item())
+    if ok and hp.transport == "p2p_fused":
+        # the fused path (push in the reduction, wait in the finalize) through the BN API:
+        # bitwise equal to the NCCL path (every rank reaches the vote below)
+        fgood = 0
+        try:
+            xs = torch.randn(4, 64, 14, 14, device=dev, generator=gen)
+            st_f = cg.BNLayerState.create(64, device=dev)
+            st_n = cg.BNLayerState.create(64, device=dev)
+            y_f, c_f = cg.sync_bn_forward(hp, xs, st_f)
+            y_n, c_n = cg.sync_bn_forward(hn, xs, st_n)
+            dx_f = cg.sync_bn_backward(hp, xs, c_f, st_f)[0]
+            dx_n = cg.sync_bn_backward(hn, xs, c_n, st_n)[0]
+            cg.check_status(dev)
+            fgood = int(torch.equal(y_f, y_n) and torch.equal(dx_f, dx_n))
+        except Exception as exc:  # noqa: BLE001
+            rep["p2p_fused_error"] = repr(exc)[:300]
+        tf = torch.tensor([fgood], device=dev, dtype=torch.int32)
+        dist.all_reduce(tf, op=dist.ReduceOp.MIN)
+        fgood = int(tf.item())
+        rep["p2p_fused_selftest"] = "passed" if fgood else "failed"
+        if not fgood:
+            hp.transport = "p2p"  # plain P2P exchanges; fused_exchange -> None
+            if requested == "p2p_fused":
+                ok = 0
     if requested in ("auto", "p2p", "p2p_fused"):
         rep["p2p_selftest"] = "passed" if ok else "failed"
         if ok:
