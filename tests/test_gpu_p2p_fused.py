@@ -215,3 +215,46 @@ def test_fused_exchange_rejects_large_groups():
     rc = lib.cgbn_fwd_stats_p2p(x.data_ptr(), 2, 8, 16, 0, 0, 9, arr, MAX_LEN, ws.data_ptr(),
                                 ws.numel(), stream_ptr(DEV))
     assert rc == _lib.ERR_INVALID and b"group size" in lib.cgbn_last_error()
+
+
+def test_fused_exchange_replays_in_a_cuda_graph():
+    """The epoch lives on the device: a captured fused step (every rank's reductions, then
+    every rank's consumers) replayed several times keeps matching the split path."""
+    lib = _lib.load()
+    G = 4
+    reg = Regions(G)
+    try:
+        fused = _make_ranks(G, (2, 128, 14, 14), seed=5)
+        split = _make_ranks(G, (2, 128, 14, 14), seed=5)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for k in fused:
+                k.outputs()  # allocate the outputs before capture
+            _fused_step(lib, fused, reg, s.cuda_stream, relu=True)  # warm-up epoch
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            keep = [(k.y, k.dx, k.saved, k.dg, k.db) for k in fused]
+
+            def no_alloc_outputs(self=None):
+                pass
+            orig = Rank.outputs
+            Rank.outputs = no_alloc_outputs  # the graph writes the buffers captured above
+            try:
+                with torch.cuda.graph(g, stream=s):
+                    _fused_step(lib, fused, reg, s.cuda_stream, relu=True)
+            finally:
+                Rank.outputs = orig
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+        st = stream_ptr(DEV)
+        for _ in range(1 + 3):  # warm-up epoch + 3 replays (the capture itself runs nothing)
+            _split_step(lib, split, st, relu=True)
+        for a, b in zip(fused, split):
+            assert int(a.status.item()) == 0
+            for name in ("y", "dx", "saved", "dg", "db", "rm", "rv"):
+                assert torch.equal(getattr(a, name), getattr(b, name)), name
+        del keep
+    finally:
+        reg.free()
