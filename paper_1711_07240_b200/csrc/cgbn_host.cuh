@@ -717,15 +717,24 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* c
 // Units per thread per round: kEwU (2) in memory order; channels_last (CM 3) threads
 // keep their UE channels' fp64 coefficients in registers, so they take more units to
 // amortise the coefficient loads.
-// Measured on B200 (U = 2 / 4 / 8, [32,C,H,W] NHWC): 4 is best everywhere except the fp32
-// dx pass without ReLU, where 8 is (54 -> 48 us on [32,256,56,56]); 16-bit dx at 8 (40 ->
-// 50 us) and fp32 dx with ReLU at 8 (5 coefficient tables in registers) are slower.
+// Measured on B200 (U = 1 / 2 / 4 / 8, [32,C,H,W] NHWC): 4 is best everywhere except the
+// fp32 dx pass without ReLU, where 8 is (54 -> 48 us on [32,256,56,56]), and the 16-bit
+// dx pass with ReLU: its five 8-wide coefficient tables take ~160 registers, so one CTA
+// per SM runs and only more units in flight hide the latency (U = 1 / 2 / 4 / 8: 170 /
+// 111 / 79 / 62 us). 16-bit dx without ReLU at 8 (40 -> 50 us) and fp32 dx with ReLU at 8
+// are slower.
 #ifndef CGBN_EWU_NHWC
 #define CGBN_EWU_NHWC 4
 #endif
+#ifndef CGBN_EWU_NHWC_RELU16
+#define CGBN_EWU_NHWC_RELU16 8
+#endif
 template <int CM, class T = float, bool DX = false, bool RELU = false>
 constexpr int ew_units() {
-  return CM != 3 ? kEwU : (DX && !RELU && sizeof(T) == 4) ? 2 * CGBN_EWU_NHWC : CGBN_EWU_NHWC;
+  return CM != 3                               ? kEwU
+         : (DX && !RELU && sizeof(T) == 4)     ? 2 * CGBN_EWU_NHWC
+         : (DX && RELU && sizeof(T) == 2)      ? CGBN_EWU_NHWC_RELU16
+                                               : CGBN_EWU_NHWC;
 }
 
 template <class K>
