@@ -299,12 +299,25 @@ int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
  * the vector cgbn_fwd_stats(z) would produce, so the exchange and cgbn_fwd_normalize
  * follow unchanged and the BN forward no longer reads z for its statistics.
  *  bias     : Cout floats or NULL.
- *  ws       : cgbn_conv1x1_ws_bytes(N, Cout, HW) bytes, 16-byte aligned (per-tile
- *             partials; need not be zeroed).
+ *  ws       : cgbn_conv1x1_ws_bytes(N, Cout, HW) bytes, 16-byte aligned (the per-CTA
+ *             statistics slot table; need not be zeroed).
+ *  partial  : may be NULL: the fold is skipped and the slot table stays in ws for
+ *             cgbn_fwd_normalize_slots (below).
  * Two launches (the conv, then a per-channel fold of the tile partials). Returns
  * CGBN_ERR_UNSUPPORTED when H*W or Cin is not a multiple of 8 (TMA row strides).
  * cgbn_conv1x1 is the same convolution without the statistics (the unfused producer). */
 size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW);
+/* Single-rank groups (bn_forward_local, or a BN group of one): call the *_stats entry
+ * point with partial = NULL, which leaves the statistics slot table in ws (a 32-byte
+ * header written by the conv kernel, then the per-CTA slots), and pass that ws here as
+ * slot_ws: one kernel merges the slots straight into the coefficients (no partial, no
+ * fold launch), then the elementwise pass — the same outputs and contract as
+ * cgbn_fwd_normalize with G == 1. */
+int cgbn_fwd_normalize_slots(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                             const void* slot_ws, const float* gamma, const float* beta,
+                             double eps, double momentum, float* running_mean,
+                             float* running_var, double* saved, int relu, void* y,
+                             unsigned* status, void* ws, size_t ws_bytes, void* stream);
 int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
                  int64_t Cout, int64_t HW, int out_dtype, void* z, void* stream);
 int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,

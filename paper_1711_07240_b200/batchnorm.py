@@ -365,7 +365,7 @@ def _train_forward_reference(g, state, exchange, scope_key, one_pass, relu, what
 
 
 def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
-                   one_pass: bool, relu: bool, what: str, partial=None):
+                   one_pass: bool, relu: bool, what: str, partial=None, slots=None):
     """The CGBN forward (batchnorm.py:115-144) on the device.
 
     G > 1: stats kernel -> exchange of the per-rank partials -> finalize (fold + running
@@ -375,7 +375,9 @@ def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
 
     ``partial``: this rank's forward partial of ``x`` already computed by its producer
     (producer fusion, ``producer.py``); the statistics kernel is skipped and the partial
-    goes straight to the exchange and the normalise pass (for any G).
+    goes straight to the exchange and the normalise pass (for any G). ``slots``: for a
+    single-rank group, the producer's statistics slot table instead
+    (cgbn_fwd_normalize_slots merges it straight into the coefficients).
     """
     g = _check_layout(x, state)
     if partial is not None and _exchange_mode != "merged":
@@ -396,6 +398,21 @@ def _train_forward(x, state: BNLayerState, exchange, group_size: int, scope_key,
     nb = lib.cgbn_workspace_bytes(g.N, c, g.HW, g.layout)
     ws = workspace(dev, nb)
     rm, rv = state.running_mean.data_ptr(), state.running_var.data_ptr()
+    if group_size == 1 and slots is not None:
+        total = g.count
+        if total < 2:
+            raise BatchNormError(
+                f"training-mode statistics need at least 2 elements per channel, got {total}")
+        with _Span("fwd_normalize", 8 * e):
+            _lib.check(lib.cgbn_fwd_normalize_slots(
+                g.x.data_ptr(), g.N, c, g.HW, g.layout, slots.data_ptr(),
+                state.gamma.data_ptr(), state.beta.data_ptr(), float(state.eps),
+                float(state.running_momentum), rm, rv, saved.data_ptr(), int(bool(relu)),
+                y.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                "cgbn_fwd_normalize_slots")
+        _raise_status(what, status, total)
+        return y, BNForwardCache(x=g.x, saved=saved, train=True, scope_key=scope_key,
+                                 relu=bool(relu), one_pass=bool(one_pass), _total_count=total)
     if group_size == 1 and partial is None:
         total = g.count
         if total < 2:

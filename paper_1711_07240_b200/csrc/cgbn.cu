@@ -65,6 +65,7 @@
 #include <utility>
 
 #include "cgbn.h"
+#include "cgbn_slots.cuh"
 
 namespace {
 
@@ -652,6 +653,56 @@ int cgbn_bwd_dx_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t
   launch_pdl(k_finalize_bwd_p2p, chan_blocks(C), true, st, pull, F);
   launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
   return check_launch("cgbn_bwd_dx_p2p");
+}
+
+// ---- producer fusion, single-rank group: the conv's statistics slots -> coefficients in
+// one kernel (merge + the forward finisher), then the elementwise pass.
+namespace {
+__global__ void __launch_bounds__(1024) k_finalize_slots(const void* slot_ws, FwdFinal F) {
+  __shared__ double sn[32][32], sa[32][32], sb[32][32];
+  pdl_wait();  // the slot table comes from the conv kernel
+  const cgbn_slots::Header h = *static_cast<const cgbn_slots::Header*>(slot_ws);
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double n, mean, M2;
+  cgbn_slots::merge(cgbn_slots::table(slot_ws), h.cout, h.mtiles, h.grid, h.nslots, c, sn, sa,
+                    sb, n, mean, M2);
+  pdl_trigger();
+  if ((threadIdx.x >> 5) == 0 && c < (int)F.C) {
+    double P, Q;
+    finalize_fwd_channel(F, (uint32_t)c, n, mean, M2, true, P, Q);
+  }
+}
+}  // namespace
+
+int cgbn_fwd_normalize_slots(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                             const void* slot_ws, const float* gamma, const float* beta,
+                             double eps, double momentum, float* running_mean,
+                             float* running_var, double* saved, int relu, void* y,
+                             unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  CGBN_REQUIRE(slot_ws, "cgbn_fwd_normalize_slots: NULL slot table");
+  const void* ptrs[] = {x, y};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 2, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((C + 31) / 32));
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_finalize_slots, slot_ws, F);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  return check_launch("cgbn_fwd_normalize_slots");
 }
 
 int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void* out,

@@ -31,6 +31,7 @@
 #include <mutex>
 
 #include "cgbn.h"
+#include "cgbn_slots.cuh"
 
 // Error reporting shared with cgbn.cu (its thread-local cgbn_last_error message).
 int cgbn_internal_set_error(int code, const char* msg);
@@ -259,15 +260,12 @@ __device__ __forceinline__ float masked_tree32(const float (&v)[32], int nv) {
   return t[0];
 }
 
-// Statistics slot of one (CTA, tile half): this thread's channel over every tile the
-// CTA processed — count, mean and centred M2.
-struct Slot {
-  double n, mean, M2;
-};
+using cgbn_slots::Slot;
 
 struct ConvArgs {
   const float* bias;  // may be null
   Slot* slots;        // [2 * ceil(grid / mtiles)][Cout]; null = no statistics
+  cgbn_slots::Header* header;  // the slot table's header (CTA 0 writes it)
   int Cout, HW, tilesP, mtiles, kblocks, tiles;
   int M;              // NHWC: output pixels N*Ho*Wo
   int Wo, HWo;        // im2col: output width / plane (output pixel -> (n, ho, wo))
@@ -330,6 +328,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (STATS && blockIdx.x == 0 && threadIdx.x == 32 && a.header != nullptr) {
+    cgbn_slots::Header h;
+    h.nslots = 2 * ((gridDim.x + a.mtiles - 1) / a.mtiles);
+    h.mtiles = a.mtiles;
+    h.grid = gridDim.x;
+    h.cout = a.Cout;
+    h.pad[0] = h.pad[1] = h.pad[2] = h.pad[3] = 0;
+    *a.header = h;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -564,49 +571,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // n_k (mean_k - K0)^2: additions only), the 32 warp sums are added in warp order, and
 // mean = K0 + A/n, M2 = B - A^2/n. Fixed order: bitwise reproducible. Slot s of channel
 // group mt exists when CTA (s / 2) * mtiles + mt ran.
-constexpr int kFoldPerWarp = 10;  // slots per channel <= 2 * 148 CTAs <= 32 warps x 10
+using cgbn_slots::kFoldPerWarp;
 
 __global__ void __launch_bounds__(1024) k_conv_fold(const Slot* __restrict__ slots, int Cout,
                                                     int mtiles, int grid, int nslots,
                                                     double* __restrict__ partial) {
   __shared__ double sn[32][32], sa[32][32], sb[32][32];
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;
-  const int mt = (blockIdx.x * 32) / BM;
-  double n = 0.0, A = 0.0, B = 0.0, K0 = 0.0;
-  if (c < Cout) {
-    // every load of this warp in flight at once (nslots <= 32 * kFoldPerWarp)
-    Slot p[kFoldPerWarp];
-#pragma unroll
-    for (int u = 0; u < kFoldPerWarp; ++u) {
-      const int s = w + 32 * u;
-      const bool ok = s < nslots && (s >> 1) * mtiles + mt < grid;
-      p[u] = ok ? slots[(size_t)s * Cout + c] : Slot{0.0, 0.0, 0.0};
-    }
-    K0 = slots[c].mean;
-#pragma unroll
-    for (int u = 0; u < kFoldPerWarp; ++u) {
-      if (p[u].n == 0.0) continue;
-      const double d = p[u].mean - K0;
-      n += p[u].n;
-      A = fma(p[u].n, d, A);
-      B += fma(p[u].n * d, d, p[u].M2);
-    }
-  }
-  sn[w][lane] = n;
-  sa[w][lane] = A;
-  sb[w][lane] = B;
-  __syncthreads();
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double n, mean, M2;
+  cgbn_slots::merge(slots, Cout, mtiles, grid, nslots, c, sn, sa, sb, n, mean, M2);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (w == 0 && c < Cout) {
-    for (int r = 1; r < 32; ++r) {
-      n += sn[r][lane];
-      A += sa[r][lane];
-      B += sb[r][lane];
-    }
-    partial[c] = K0 + A / n;
-    partial[Cout + c] = B - A * A / n;
+  if ((threadIdx.x >> 5) == 0 && c < Cout) {
+    partial[c] = mean;
+    partial[Cout + c] = M2;
     if (c == 0) partial[2 * Cout] = n;
   }
 }
@@ -757,12 +735,12 @@ int conv_grid(const Geo& g) {
 int conv_nslots(const Geo& g) { return 2 * ((conv_grid(g) + g.mtiles - 1) / g.mtiles); }
 
 size_t stats_ws_bytes(const Geo& g) {
-  return (size_t)conv_nslots(g) * (size_t)g.Cout * sizeof(Slot);
+  return sizeof(cgbn_slots::Header) + (size_t)conv_nslots(g) * (size_t)g.Cout * sizeof(Slot);
 }
 
 template <class OutT, int MODE>
 int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, void* z,
-                Slot* slots, cudaStream_t st) {
+                Slot* slots, cgbn_slots::Header* header, cudaStream_t st) {
   constexpr int sz = sizeof(OutT);
   const CUtensorMapDataType zdt =
       sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -808,6 +786,7 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
   ConvArgs a;
   a.bias = bias;
   a.slots = slots;
+  a.header = header;
   a.Cout = (int)g.Cout;
   a.HW = (int)g.HW;
   a.tilesP = g.tilesP;
@@ -864,11 +843,12 @@ int validate(const char* what, const void* x, const void* w, const void* z, cons
 
 template <int MODE>
 int run_conv(const char* what, const void* x, const void* w, const float* bias, const Geo& g,
-             int out_dtype, void* z, double* partial, void* ws, size_t ws_bytes, void* stream) {
+             int out_dtype, void* z, bool stats, double* partial, void* ws, size_t ws_bytes,
+             void* stream) {
   if (int rc = validate(what, x, w, z, g, out_dtype)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   Slot* slots = nullptr;
-  if (partial) {
+  if (stats) {
     const size_t need = stats_ws_bytes(g);
     if (!ws || ws_bytes < need)
       return fail(CGBN_ERR_INVALID, "%s: workspace too small (need %lld, got %lld)", what,
@@ -878,11 +858,14 @@ int run_conv(const char* what, const void* x, const void* w, const float* bias, 
     if (conv_nslots(g) > 32 * kFoldPerWarp)
       return fail(CGBN_ERR_UNSUPPORTED, "%s: more than %d statistics slots per channel", what,
                   32 * kFoldPerWarp);
-    slots = (Slot*)ws;
+    slots = const_cast<Slot*>(cgbn_slots::table(ws));
   }
-  int rc = out_dtype == CGBN_ACT_F32 ? launch_conv<float, MODE>(x, w, bias, g, z, slots, st)
-                                     : launch_conv<__nv_bfloat16, MODE>(x, w, bias, g, z, slots, st);
-  if (rc || !partial) return rc;
+  auto* header = static_cast<cgbn_slots::Header*>(stats ? ws : nullptr);
+  int rc = out_dtype == CGBN_ACT_F32
+               ? launch_conv<float, MODE>(x, w, bias, g, z, slots, header, st)
+               : launch_conv<__nv_bfloat16, MODE>(x, w, bias, g, z, slots, header, st);
+  if (rc || !partial) return rc;  // (statistics without a partial: the slot table stays in
+                                  // ws for cgbn_fwd_normalize_slots)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((g.Cout + 31) / 32));
   cfg.blockDim = dim3(1024);
@@ -917,15 +900,14 @@ size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW) {
 int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
                  int64_t Cout, int64_t HW, int out_dtype, void* z, void* stream) {
   return run_conv<kNCHW1>("conv1x1", x, w, bias, make_geo(kNCHW1, N, Cin, Cout, 1, HW),
-                          out_dtype, z, nullptr, nullptr, 0, stream);
+                          out_dtype, z, false, nullptr, nullptr, 0, stream);
 }
 
 int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
                        int64_t Cout, int64_t HW, int out_dtype, void* z, double* partial,
                        void* ws, size_t ws_bytes, void* stream) {
-  if (!partial) return fail(CGBN_ERR_INVALID, "conv1x1_stats: partial is NULL");
   return run_conv<kNCHW1>("conv1x1_stats", x, w, bias, make_geo(kNCHW1, N, Cin, Cout, 1, HW),
-                          out_dtype, z, partial, ws, ws_bytes, stream);
+                          out_dtype, z, true, partial, ws, ws_bytes, stream);
 }
 
 size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W, int ksize,
@@ -944,8 +926,10 @@ int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, i
                 ksize, stride);
   const Geo g = make_geo(mode, N, Cin, Cout, H, W, ksize, stride);
   return mode == kNHWC1
-             ? run_conv<kNHWC1>("conv_nhwc", x, w, bias, g, out_dtype, z, nullptr, nullptr, 0, stream)
-             : run_conv<kNHWC3>("conv_nhwc", x, w, bias, g, out_dtype, z, nullptr, nullptr, 0, stream);
+             ? run_conv<kNHWC1>("conv_nhwc", x, w, bias, g, out_dtype, z, false, nullptr, nullptr,
+                                0, stream)
+             : run_conv<kNHWC3>("conv_nhwc", x, w, bias, g, out_dtype, z, false, nullptr, nullptr,
+                                0, stream);
 }
 
 int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
@@ -956,11 +940,10 @@ int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_
     return fail(CGBN_ERR_INVALID,
                 "conv_nhwc_stats: ksize must be 1 or 3 and stride 1 or 2, got %d / %d", ksize,
                 stride);
-  if (!partial) return fail(CGBN_ERR_INVALID, "conv_nhwc_stats: partial is NULL");
   const Geo g = make_geo(mode, N, Cin, Cout, H, W, ksize, stride);
-  return mode == kNHWC1 ? run_conv<kNHWC1>("conv_nhwc_stats", x, w, bias, g, out_dtype, z,
+  return mode == kNHWC1 ? run_conv<kNHWC1>("conv_nhwc_stats", x, w, bias, g, out_dtype, z, true,
                                            partial, ws, ws_bytes, stream)
-                        : run_conv<kNHWC3>("conv_nhwc_stats", x, w, bias, g, out_dtype, z,
+                        : run_conv<kNHWC3>("conv_nhwc_stats", x, w, bias, g, out_dtype, z, true,
                                            partial, ws, ws_bytes, stream);
 }
 

@@ -119,7 +119,9 @@ def _check(x, weight, bias, out_dtype, k, stride=1):
     return x, wt.to(x.device).contiguous(), b, nhwc, (n, cin, h, w, cout)
 
 
-def _conv(x, weight, bias, out_dtype, k, stats, stride=1):
+def _conv(x, weight, bias, out_dtype, k, stats, stride=1, slots_only=False):
+    """The convolution; with ``stats``, also this rank's partial (or, ``slots_only``, the
+    statistics slot table left in the returned scratch tensor instead of the partial)."""
     x, wt, b, nhwc, (n, cin, h, w, cout) = _check(x, weight, bias, out_dtype, k, stride)
     lib = _lib.load()
     dev = x.device
@@ -132,7 +134,8 @@ def _conv(x, weight, bias, out_dtype, k, stats, stride=1):
     od = _OUT[out_dtype]
     partial = None
     if stats:
-        partial = torch.empty(2 * cout + 1, dtype=torch.float64, device=dev)
+        if not slots_only:
+            partial = torch.empty(2 * cout + 1, dtype=torch.float64, device=dev)
         nb = (lib.cgbn_conv_nhwc_ws_bytes(n, cout, h, w, k, stride) if nhwc
               else lib.cgbn_conv1x1_ws_bytes(n, cout, h * w))
         ws = _tile_scratch(dev, nb)
@@ -140,19 +143,23 @@ def _conv(x, weight, bias, out_dtype, k, stats, stride=1):
     with _Span(name, 0):
         if nhwc and stats:
             rc = lib.cgbn_conv_nhwc_stats(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h, w, k,
-                                          stride, od, z.data_ptr(), partial.data_ptr(),
+                                          stride, od, z.data_ptr(),
+                                          partial.data_ptr() if partial is not None else None,
                                           ws.data_ptr(), ws.numel(), st)
         elif nhwc:
             rc = lib.cgbn_conv_nhwc(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h, w, k,
                                     stride, od, z.data_ptr(), st)
         elif stats:
             rc = lib.cgbn_conv1x1_stats(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h * w, od,
-                                        z.data_ptr(), partial.data_ptr(), ws.data_ptr(),
-                                        ws.numel(), st)
+                                        z.data_ptr(),
+                                        partial.data_ptr() if partial is not None else None,
+                                        ws.data_ptr(), ws.numel(), st)
         else:
             rc = lib.cgbn_conv1x1(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h * w, od,
                                   z.data_ptr(), st)
         _lib.check(rc, "cgbn_" + ("conv_nhwc" if nhwc else "conv1x1") + ("_stats" if stats else ""))
+    if slots_only:
+        return z, ws
     return z, partial
 
 
@@ -185,9 +192,10 @@ def _fused_local(k, x, weight, state, bias, out_dtype, relu, what, stride=1):
         z = _conv(x, weight, bias, out_dtype, k, False, stride)[0]
         y, cache = _bn.bn_forward_local(z, state, relu=relu)
         return y, cache, z
-    z, partial = _conv(x, weight, bias, out_dtype, k, True, stride)
+    # single rank: the slot table goes straight to the finalize (no partial, no fold)
+    z, slots = _conv(x, weight, bias, out_dtype, k, True, stride, slots_only=True)
     y, cache = _train_forward(z, state, _local_exchange, 1, None, one_pass=False, relu=relu,
-                              what=what, partial=partial)
+                              what=what, slots=slots)
     return y, cache, z
 
 

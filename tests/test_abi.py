@@ -89,6 +89,9 @@ def test_producer_conv_argument_validation_without_gpu():
     rc = lib.cgbn_conv1x1(16, 16, None, 2, 64, 128, 64, 0x20, 16, None)
     assert rc == _lib.ERR_INVALID and b"dtype" in lib.cgbn_last_error()
     rc = lib.cgbn_conv1x1_stats(16, 16, None, 2, 64, 128, 64, 0, 16, None, None, 0, None)
-    assert rc == _lib.ERR_INVALID and b"partial" in lib.cgbn_last_error()
+    assert rc == _lib.ERR_INVALID and b"workspace" in lib.cgbn_last_error()
+    rc = lib.cgbn_fwd_normalize_slots(16, 2, 8, 16, 0, None, 16, 16, 1e-5, 0.1, 16, 16, 16, 0,
+                                      16, 16, 16, 1 << 20, None)
+    assert rc == _lib.ERR_INVALID and b"slot table" in lib.cgbn_last_error()
     rc = lib.cgbn_conv_nhwc_stats(16, 16, None, 2, 64, 128, 8, 8, 3, 2, 0, 16, 16, 16, 0, None)
     assert rc == _lib.ERR_INVALID and b"workspace" in lib.cgbn_last_error()
