@@ -882,11 +882,41 @@ def run_gpu_arm(args):
         torch.cuda.synchronize()
         barrier()
         ms_e = a0.elapsed_time(a1) / k_e
+        # the PCIe floor of the same step: the same H2D and D2H copies on the same two
+        # streams with no compute between them (both directions concurrently)
+        def copy_only_step():
+            comp = torch.cuda.current_stream(dev)
+            s_in.wait_stream(comp)
+            s_out.wait_stream(comp)
+            with torch.cuda.stream(s_in):
+                for i in range(n_l):
+                    dx_in[i].copy_(hx[i], non_blocking=True)
+                for i in range(n_l - 1, -1, -1):
+                    ddy_in[i].copy_(hdy[i], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for i in range(n_l):
+                    hy[i].copy_(xs[i], non_blocking=True)
+                for i in range(n_l - 1, -1, -1):
+                    hdx[i].copy_(dys[i], non_blocking=True)
+            comp.wait_stream(s_in)
+            comp.wait_stream(s_out)
+
+        copy_only_step()
+        torch.cuda.synchronize()
+        a0.record()
+        for _ in range(k_e):
+            copy_only_step()
+        a1.record()
+        torch.cuda.synchronize()
+        ms_copy = a0.elapsed_time(a1) / k_e
         if world > 1:
             tt = torch.tensor([ms_e], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms_e = float(tt.item())
         e2e = {"value": step_bytes_rank * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
+               "copy_only_ms_per_step": ms_copy,
+               "pcie_gbs_per_direction": 8 * sum(elems) / (ms_copy * 1e-3) / 1e9,
+               "frac_of_copy_bound": ms_copy / ms_e,
                "h2d_bytes_per_step": 8 * sum(elems), "d2h_bytes_per_step": 8 * sum(elems),
                "ms_per_step": ms_e, "steps": k_e,
                "path": "sync_bn_forward/sync_bn_backward per layer, eager (no graph); pinned "
