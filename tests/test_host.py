@@ -127,6 +127,20 @@ def test_sequence_numbers_keep_scopes_apart():
         assert all(out[r][i][1] == 60 + 4 * i for r in range(4))
 
 
+def test_sequence_skew_diagnosed():
+    """A rank whose sequence number runs ahead (a skipped or extra collective) is
+    diagnosed, not paired with the wrong call (test_collectives.py:216-227)."""
+    grp = cpu_group(2, timeout=2.0)
+
+    def fn(h):
+        if h.rank == 1:
+            h._next_seq("world")  # simulates a skipped / extra call
+        return h.exchange(cg.SCOPE_WORLD, "allreduce", torch.ones(1, dtype=torch.float64))
+
+    with pytest.raises(cg.CollectiveError, match="#"):
+        grp.run(fn)
+
+
 def test_return_exceptions():
     grp = cpu_group(2)
 
