@@ -36,7 +36,18 @@ NGeom rows_geom(int64_t N, int64_t C, int64_t HW, int64_t ctas) {
   g.M = (uint32_t)(N * HW);
   g.C = (uint32_t)C;
   g.C4 = (uint32_t)(C / 4);
-  g.CS4 = g.C4 < (uint32_t)kThreads ? g.C4 : (uint32_t)kThreads;
+  // Channel slice width in float4 units. Narrow slices put more rows in flight per CTA
+  // (rpp = 256 / CS4) for the same slot table (nb * C = ctas * 4 * CS4 partials), which
+  // is what wide-C layers lacked: measured on B200 in a graph (tools/rows_sweep.sh),
+  // 128 channels per slice (CS4 = 32) is best up to C = 256 and on tiny row counts, 256
+  // channels (CS4 = 64) above that; full-width 1024-channel slices were 10-70% slower
+  // on C >= 512 (e.g. [32,2048,7,7] stats 10.1 -> 7.4 us, bwd reduce 14.6 -> 9.2 us).
+  uint32_t cs_max = (g.C4 > 64 && g.M >= 256) ? 64u : 32u;
+  if (const char* e = getenv("CGBN_ROWS_CS4")) {  // A/B
+    const int v = atoi(e);
+    if (v == 32 || v == 64 || v == 128 || v == 256) cs_max = (uint32_t)v;
+  }
+  g.CS4 = g.C4 < cs_max ? g.C4 : cs_max;
   g.rpp = (uint32_t)kThreads / g.CS4;
   g.nslices = (g.C4 + g.CS4 - 1) / g.CS4;
   int64_t nb = ceil_div(ctas, (int64_t)g.nslices);
