@@ -98,6 +98,12 @@ def host_cpu_info():
     return {"cpu_model": model, "host_cpus": os.cpu_count(), "affinity_cpus": aff}
 
 
+def _lib_consts():
+    """The C ABI's layout / dtype codes (include/cgbn.h via the binding module)."""
+    from paper_1711_07240_b200 import _lib
+    return _lib
+
+
 def numel(s):
     n = 1
     for e in s:
@@ -317,7 +323,7 @@ def run_reference_arm(args):
 # ----------------------------------------------------------------------------------
 # GPU arm
 
-def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
+def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20, lay=0, esize=4):
     """Per-kernel-family device time of one step. For each family a CUDA graph holds that
     kernel's launch for every layer (the layers' own buffers, step order) made through
     the C ABI: statistics (cgbn_fwd_stats), normalise (the elementwise pass alone,
@@ -355,19 +361,19 @@ def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
 
     fams = {
         "fwd_stats": (4, lambda d, ws, st: lib.cgbn_fwd_stats(
-            d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0, d["part"].data_ptr(),
+            d["x"].data_ptr(), d["n"], d["c"], d["hw"], lay, d["part"].data_ptr(),
             ws.data_ptr(), ws.numel(), st)),
         "fwd_pair": (12, lambda d, ws, st: lib.cgbn_fwd_train_local(
-            d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0, d["st"].gamma.data_ptr(),
+            d["x"].data_ptr(), d["n"], d["c"], d["hw"], lay, d["st"].gamma.data_ptr(),
             d["st"].beta.data_ptr(), 1e-5, 0.1, d["rm"].data_ptr(), d["rv"].data_ptr(),
             d["saved2"].data_ptr(), 0, d["y"].data_ptr(), d["status"].data_ptr(),
             ws.data_ptr(), ws.numel(), st)),
         "bwd_reduce": (8, lambda d, ws, st: lib.cgbn_bwd_reduce(
-            d["dy"].data_ptr(), d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0,
+            d["dy"].data_ptr(), d["x"].data_ptr(), d["n"], d["c"], d["hw"], lay,
             d["saved"].data_ptr(), d["st"].gamma.data_ptr(), d["st"].beta.data_ptr(), 0,
             d["bpart"].data_ptr(), ws.data_ptr(), ws.numel(), st)),
         "bwd_pair": (20, lambda d, ws, st: lib.cgbn_bwd_local(
-            d["dy"].data_ptr(), d["x"].data_ptr(), d["n"], d["c"], d["hw"], 0,
+            d["dy"].data_ptr(), d["x"].data_ptr(), d["n"], d["c"], d["hw"], lay,
             d["saved"].data_ptr(), d["st"].gamma.data_ptr(), d["st"].beta.data_ptr(), 1e-5,
             0, d["dx"].data_ptr(), d["dg"].data_ptr(), d["db"].data_ptr(),
             d["status"].data_ptr(), ws.data_ptr(), ws.numel(), st)),
@@ -375,7 +381,7 @@ def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
     out, raw = {}, {}
     total_elems = sum(numel(s) for s in shapes)
     with torch.cuda.stream(side):
-        ws = workspace(dev, max(lib.cgbn_workspace_bytes(d["n"], d["c"], d["hw"], 0) for d in L))
+        ws = workspace(dev, max(lib.cgbn_workspace_bytes(d["n"], d["c"], d["hw"], lay) for d in L))
         st = side.cuda_stream
         for name, (bpe, fn) in fams.items():
             for d in L:
@@ -403,6 +409,7 @@ def kernel_profile(cg, shapes, xs, dys, states, handle, reps=20):
            "bwd_reduce": (8, raw["bwd_reduce"]),
            "bwd_dx_ew": (12, raw["bwd_pair"] - raw["bwd_reduce"])}
     for name, (bpe, ms) in fam.items():
+        bpe = bpe * esize // 4  # algorithmic bytes scale with the activation size
         out[name] = {"ms_per_step": ms, "launches_per_step": len(L), "bytes_per_elem": bpe,
                      "alg_gbs": bpe * total_elems / (ms * 1e-3) / 1e9}
     tot = sum(v["ms_per_step"] for v in out.values())
@@ -677,13 +684,21 @@ def run_gpu_arm(args):
 
     shapes = WORKLOADS[args.workload][1]()
     elems = [numel(s) for s in shapes]
-    step_bytes_rank = BYTES_PER_ELEM * sum(elems)
+    # activation layout / dtype (default the reference's fp32 NCHW; channels_last and
+    # bf16 are the SURVEY 8f row-2 widenings, reported as separate lines)
+    act = {"f32": torch.float32, "bf16": torch.bfloat16}[args.act]
+    esize = 4 if args.act == "f32" else 2
+    mf = torch.channels_last if args.layout == "nhwc" else torch.contiguous_format
+    lay = (_lib_consts().LAYOUT_NHWC if args.layout == "nhwc" else 0) | \
+        (_lib_consts().ACT_BF16 if args.act == "bf16" else 0)
+    bpe_step = BYTES_PER_ELEM * esize // 4
+    step_bytes_rank = bpe_step * sum(elems)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     xs, dys, states = [], [], []
     for s in shapes:
-        xs.append(torch.randn(s, device=dev, generator=gen))
-        dys.append(torch.randn(s, device=dev, generator=gen))
+        xs.append(torch.randn(s, device=dev, generator=gen).to(act).contiguous(memory_format=mf))
+        dys.append(torch.randn(s, device=dev, generator=gen).to(act).contiguous(memory_format=mf))
         c = s[1]
         gamma = torch.rand(c, device=dev, generator=gen) + 0.5
         beta = torch.randn(c, device=dev, generator=gen)
@@ -744,7 +759,7 @@ def run_gpu_arm(args):
     torch.cuda.synchronize()
     # Working sets under 2x L2 (the small SURVEY configs) are timed step by step with an
     # L2 flush (256 MB write) between steps, outside the timed events.
-    l2_flush = 8 * sum(elems) < 2 * L2_BYTES
+    l2_flush = 2 * esize * sum(elems) < 2 * L2_BYTES
     if l2_flush:
         flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -781,7 +796,7 @@ def run_gpu_arm(args):
     # launches of the step (same layer buffers, step order) through the C ABI; CUDA
     # events on the replay stream around `reps` replays.
     kern, timing_mode = ({}, "skipped") if args.no_kprof else \
-        kernel_profile(cg, shapes, xs, dys, states, handle, reps=20)
+        kernel_profile(cg, shapes, xs, dys, states, handle, reps=20, lay=lay, esize=esize)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -822,15 +837,21 @@ def run_gpu_arm(args):
     # ---- e2e: public API with host (pinned) buffers, H2D/D2H inside the timed region
     e2e = None
     if not args.no_e2e:
-        hx = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
-        hdy = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
-        hy = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
-        hdx = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in shapes]
+        def pinned(shape):  # pinned host buffer in the activation layout
+            stride = torch.empty(shape, device="meta").contiguous(memory_format=mf).stride()
+            return torch.empty_strided(shape, stride, dtype=act, pin_memory=True)
+
+        hx = [pinned(s) for s in shapes]
+        hdy = [pinned(s) for s in shapes]
+        hy = [pinned(s) for s in shapes]
+        hdx = [pinned(s) for s in shapes]
         for i in range(len(shapes)):
             hx[i].copy_(xs[i])
             hdy[i].copy_(dys[i])
-        dx_in = [torch.empty(s, device=dev) for s in shapes]
-        ddy_in = [torch.empty(s, device=dev) for s in shapes]
+        dx_in = [torch.empty(s, device=dev, dtype=act).contiguous(memory_format=mf)
+                 for s in shapes]
+        ddy_in = [torch.empty(s, device=dev, dtype=act).contiguous(memory_format=mf)
+                  for s in shapes]
 
         # H2D on a copy-in stream, compute on the current stream, D2H on a copy-out stream
         # (the two PCIe directions run on separate copy engines), ordered by events: what
@@ -869,7 +890,8 @@ def run_gpu_arm(args):
                 dxo.record_stream(s_out)
             comp.wait_stream(s_out)  # the step ends when y and dx are in host memory
 
-        e2e_step()
+        for _ in range(2):  # warm-up (first touches of the pinned buffers)
+            e2e_step()
         torch.cuda.synchronize()
         barrier()
         k_e = max(1, min(args.steps, args.e2e_steps))
@@ -915,9 +937,10 @@ def run_gpu_arm(args):
             ms_e = float(tt.item())
         e2e = {"value": step_bytes_rank * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
                "copy_only_ms_per_step": ms_copy,
-               "pcie_gbs_per_direction": 8 * sum(elems) / (ms_copy * 1e-3) / 1e9,
+               "pcie_gbs_per_direction": 2 * esize * sum(elems) / (ms_copy * 1e-3) / 1e9,
                "frac_of_copy_bound": ms_copy / ms_e,
-               "h2d_bytes_per_step": 8 * sum(elems), "d2h_bytes_per_step": 8 * sum(elems),
+               "h2d_bytes_per_step": 2 * esize * sum(elems),
+               "d2h_bytes_per_step": 2 * esize * sum(elems),
                "ms_per_step": ms_e, "steps": k_e,
                "path": "sync_bn_forward/sync_bn_backward per layer, eager (no graph); pinned "
                        "host x/dy copied in on a copy-in stream, y/dx copied out on a "
@@ -946,18 +969,18 @@ def run_gpu_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32 (fp64 statistics)", "data": "synthetic (torch.randn, seeded per rank)",
+            "dtype": f"{args.act} (fp64 statistics)", "data": "synthetic (torch.randn, seeded per rank)",
             "config": {"workload": args.workload, "describe": WORKLOADS[args.workload][0],
                        "layers": len(shapes),
                        "per_gpu_batch": shapes[0][0], "elements_per_gpu": sum(elems),
-                       "alg_bytes_per_elem": BYTES_PER_ELEM,
+                       "alg_bytes_per_elem": bpe_step,
                        "parallelism": f"cgbn_group{world}", "bn_group_size": world,
-                       "layout": "NCHW", "relu": False,
+                       "layout": args.layout.upper(), "relu": False,
                        "l2_policy": (("L2 flushed (256 MB write) before every timed step; "
-                                      f"x+dy = {8 * sum(elems) / 1e6:.1f} MB per step")
+                                      f"x+dy = {2 * esize * sum(elems) / 1e6:.1f} MB per step")
                                      if l2_flush else
                                      (f"inputs > L2: {len(shapes)} layers' x+dy = "
-                                      f"{8 * sum(elems) / 1e9:.2f} GB per step >> 126 MB L2; "
+                                      f"{2 * esize * sum(elems) / 1e9:.2f} GB per step >> 126 MB L2; "
                                       "intra-layer re-reads of x may hit L2")),
                        "cuda_graph": graph is not None, "launch": graph_note,
                        "exchange_transport": (transport_report or {}).get(
@@ -1000,6 +1023,10 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet50_bn_b32",
                     help="SURVEY 8(d) configuration (default: config 2, the driver's)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--layout", choices=["nchw", "nhwc"], default="nchw",
+                    help="activation layout (nhwc = channels_last; SURVEY 8f row 2)")
+    ap.add_argument("--act", choices=["f32", "bf16"], default="f32",
+                    help="activation dtype (statistics stay fp64)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes/launch of the dominant kernel (recorded as-is)")
     ap.add_argument("--fused", action="store_true",
