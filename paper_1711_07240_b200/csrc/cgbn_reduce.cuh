@@ -371,10 +371,20 @@ k_fold_rows(Geom g, Op op, const double2* __restrict__ slots, uint32_t nb,
   if (c >= g.C) return;
   double a = 0.0, b = 0.0;
   const double2* p = slots + (size_t)c * nb;
-  for (uint32_t i = l; i < nb; i += 32) {
-    const double2 t = __ldcg(p + i);
-    a += t.x;
-    b += t.y;
+  // all of a lane's slot loads are issued before the first add (a rolled loop waited
+  // out one L2 round trip per slot); the adds keep the ascending per-lane order
+  constexpr int FU = 8;
+  for (uint32_t i0 = l; i0 < nb; i0 += 32 * FU) {
+    double2 t[FU];
+#pragma unroll
+    for (int u = 0; u < FU; ++u)
+      if (i0 + 32 * u < nb) t[u] = __ldcg(p + i0 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < FU; ++u)
+      if (i0 + 32 * u < nb) {
+        a += t[u].x;
+        b += t[u].y;
+      }
   }
   a = warp_sum(a);
   b = warp_sum(b);
