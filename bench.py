@@ -897,13 +897,15 @@ def run_gpu_arm(args):
         k_e = max(1, min(args.steps, args.e2e_steps))
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for _ in range(k_e):
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(k_e + 1)]
+        marks[0].record()
+        for k in range(k_e):
             e2e_step()
-        a1.record()
+            marks[k + 1].record()
         torch.cuda.synchronize()
         barrier()
-        ms_e = a0.elapsed_time(a1) / k_e
+        ms_e = marks[0].elapsed_time(marks[-1]) / k_e
+        ms_e_steps = [marks[k].elapsed_time(marks[k + 1]) for k in range(k_e)]
         # the PCIe floor of the same step: the same H2D and D2H copies on the same two
         # streams with no compute between them (both directions concurrently)
         def copy_only_step():
@@ -941,7 +943,7 @@ def run_gpu_arm(args):
                "frac_of_copy_bound": ms_copy / ms_e,
                "h2d_bytes_per_step": 2 * esize * sum(elems),
                "d2h_bytes_per_step": 2 * esize * sum(elems),
-               "ms_per_step": ms_e, "steps": k_e,
+               "ms_per_step": ms_e, "steps": k_e, "ms_each_step": ms_e_steps,
                "path": "sync_bn_forward/sync_bn_backward per layer, eager (no graph); pinned "
                        "host x/dy copied in on a copy-in stream, y/dx copied out on a "
                        "copy-out stream, event-ordered with the compute stream"}
@@ -1033,7 +1035,7 @@ def main():
                     help="single-launch cooperative kernels for layers that fit on chip")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kprof", action="store_true", help="skip the per-kernel profile")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-producer", action="store_true",
                     help="skip the producer-fusion (conv epilogue statistics) measurement")
