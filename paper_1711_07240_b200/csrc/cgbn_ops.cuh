@@ -294,6 +294,28 @@ struct StatsOp : PushSlot<PUSH> {
     if (!masked_vm(VM) || r.m) r.v.load(x + off);
   }
   __device__ __forceinline__ void acc(const Regs& r, double& a, double& b) const {
+    if constexpr (sizeof(T) == 2 && VEC >= 4) {
+      // 16-bit activations: the unit's VEC differences and squares are summed in fp32,
+      // then added once to the fp64 accumulators (a quarter of the fp64 conversions and
+      // adds). K is the channel's first element or 0 here, so d = x - K is exact in fp32
+      // whenever x and K lie within 2^15 of each other, and the partial carries at most
+      // VEC - 1 fp32 roundings (~5e-7 relative). kSumSq shifts by the fp64 group mean
+      // and keeps the fp64 path.
+      if (ksum == nullptr) {
+        const float Kf = (float)K;
+        float s = 0.f, q = 0.f;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          if (masked_vm(VM) && !((r.m >> k) & 1u)) continue;
+          const float d = r.v.get(k) - Kf;
+          s += d;
+          q = __fmaf_rn(d, d, q);
+        }
+        a += (double)s;
+        b += (double)q;
+        return;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
       if (masked_vm(VM) && !((r.m >> k) & 1u)) continue;
@@ -393,6 +415,24 @@ struct BwdOp : PushSlot<PUSH> {
     }
   }
   __device__ __forceinline__ void acc(const Regs& r, double& a, double& b) const {
+    if constexpr (sizeof(T) == 2 && VEC >= 4 && !RELU) {
+      // 16-bit activations: fp32 partials of the unit's VEC terms, one fp64 add each
+      // (see StatsOp::acc). x - mean uses the fp32 split mean = mh + ml, so the centring
+      // keeps ~2^-24 relative accuracy even when |mean| >> the spread.
+      const float mh = (float)mean;
+      const float ml = (float)(mean - (double)mh);
+      float s = 0.f, q = 0.f;
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        if (masked_vm(VM) && !((r.m >> k) & 1u)) continue;
+        const float gk = r.g.get(k);
+        s += gk;
+        q = __fmaf_rn(gk, (r.x.get(k) - mh) - ml, q);
+      }
+      a += (double)s;
+      b += (double)q;
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
       if (masked_vm(VM) && !((r.m >> k) & 1u)) continue;
