@@ -275,6 +275,35 @@ struct StatsRows {
       b[j] = __fma_rn(d, d, b[j]);
     }
   }
+  // A thread's U rows of one round. 16-bit activations: per channel, fp32 partials over
+  // the round's rows, one fp64 add each (StatsOp::acc explains the error bound).
+  template <int U>
+  __device__ __forceinline__ void acc_round(const State& s, const Regs (&v)[U], uint32_t r,
+                                            uint32_t r1, uint32_t rpp, double (&a)[4],
+                                            double (&b)[4]) const {
+    if constexpr (sizeof(T) == 2) {
+      if (base.ksum == nullptr) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float Kf = (float)s.K[j];
+          float sj = 0.f, qj = 0.f;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (r + u * rpp < r1) {
+              const float d = v[u].v.get(j) - Kf;
+              sj += d;
+              qj = __fmaf_rn(d, d, qj);
+            }
+          a[j] += (double)sj;
+          b[j] += (double)qj;
+        }
+        return;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r + u * rpp < r1) acc(s, v[u], a, b);
+  }
 };
 
 // Backward sums over rows: [sum g, sum g*(x - mean)] with the forward's ReLU mask.
@@ -311,6 +340,34 @@ struct BwdRows {
       b[j] = __fma_rn(gk, (double)xj - s.mean[j], b[j]);
     }
   }
+  // 16-bit activations without ReLU: per channel, fp32 partials over the round's rows
+  // (BwdOp::acc: two-float split mean), one fp64 add each.
+  template <int U>
+  __device__ __forceinline__ void acc_round(const State& s, const Regs (&v)[U], uint32_t r,
+                                            uint32_t r1, uint32_t rpp, double (&a)[4],
+                                            double (&b)[4]) const {
+    if constexpr (sizeof(T) == 2 && !RELU) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float mh = (float)s.mean[j];
+        const float ml = (float)(s.mean[j] - (double)mh);
+        float sj = 0.f, qj = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (r + u * rpp < r1) {
+            const float gk = v[u].g.get(j);
+            sj += gk;
+            qj = __fmaf_rn(gk, (v[u].x.get(j) - mh) - ml, qj);
+          }
+        a[j] += (double)sj;
+        b[j] += (double)qj;
+      }
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r + u * rpp < r1) acc(s, v[u], a, b);
+  }
 };
 
 template <class NOp>
@@ -337,9 +394,7 @@ k_reduce_rows(NGeom g, NOp op, double2* __restrict__ slots) {
         const uint32_t rr = r + u * g.rpp;
         if (rr < r1) op.load((size_t)rr * g.C4 + c4, v[u]);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (r + u * g.rpp < r1) op.acc(s, v[u], a, b);
+      op.template acc_round<U>(s, v, r, r1, g.rpp, a, b);
     }
   }
 #pragma unroll
