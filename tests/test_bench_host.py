@@ -35,3 +35,28 @@ def test_port_step_counts_algorithmic_bytes():
 def test_host_cpu_info_keys():
     info = bench.host_cpu_info()
     assert {"cpu_model", "host_cpus", "affinity_cpus"} <= set(info)
+
+
+def test_reference_arm_json_line_contract():
+    """`bench.py --impl reference` prints one JSON line with the reference-arm keys
+    (CPU only: the arm times the reference's own CPU path, or the oracle port when
+    baseline/_ref is absent)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run(
+        [sys.executable, "bench.py", "--impl", "reference", "--workload", "latency_2048x7x7",
+         "--steps", "2", "--warmup", "3", "--ref-procs", "1"],
+        cwd=root, capture_output=True, text=True, timeout=300, check=True)
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 3
+    assert d["metric"] == bench.METRIC and d["unit"] == bench.UNIT and d["value"] > 0
+    assert d["higher_is_better"] is True and d["n_gpus"] == 1
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] == 1 and cb["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
