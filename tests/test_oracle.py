@@ -123,3 +123,30 @@ def test_small_count_rejected():
     # batchnorm.py:133-137 / test_batchnorm.py:110-113
     with pytest.raises(ValueError, match="at least 2"):
         O.group_train_forward([np.ones((1, 3))], [O.RankState(np.ones(3), np.zeros(3))])
+
+
+@pytest.mark.parametrize("relu,shapes", [
+    (False, [(3, 10, 4, 5), (2, 10, 4, 5)]),
+    (True, [(4, 7, 3, 3)] * 3),
+    (False, [(6, 9)] * 2),
+])
+def test_group_blocks_matches_literal_restatement(relu, shapes):
+    """The memory-bounded block oracle (used at bench sizes) agrees with the literal
+    restatement group_train_forward / group_backward to ~1e-12."""
+    rng = np.random.default_rng(5)
+    c = shapes[0][1]
+    xs = [rng.normal(loc=2.0, size=s) for s in shapes]
+    dys = [rng.normal(size=s) for s in shapes]
+    gamma, beta = rng.uniform(0.5, 1.5, c), rng.normal(size=c)
+    g = len(shapes)
+    ref = O.cgbn_world(xs, gamma, beta, g, relu=relu, dys=dys)
+    outs = list(O.group_blocks(xs, gamma, beta, dys=dys, relu=relu, block_elems=40))
+    assert len(outs) > 1  # several channel blocks
+    for b in outs:
+        c0, c1 = b["c0"], b["c1"]
+        for key in ("mu", "var", "running_mean", "running_var", "dgamma", "dbeta"):
+            assert O.rel_err(b[key], ref[0][key][c0:c1]) <= 1e-12, key
+        assert b["m"] == ref[0]["m"]
+        for r in range(g):
+            assert O.rel_err(b["y"][r], ref[r]["y"][:, c0:c1]) <= 1e-12
+            assert O.rel_err(b["dx"][r], ref[r]["dx"][:, c0:c1]) <= 1e-12
