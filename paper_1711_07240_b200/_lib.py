@@ -15,6 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CGBN_LIB", os.path.join(_HERE, "libcgbn.so"))
 
 # Keep in sync with include/cgbn.h
+ABI_VERSION = 6  # CGBN_ABI_VERSION the bindings below were written for
 LAYOUT_NCHW = 0
 LAYOUT_NHWC = 1
 ACT_F32 = 0x00   # activation dtype, OR'd into the layout argument
@@ -117,6 +118,20 @@ def load():
             lib = ctypes.CDLL(LIB_PATH)
         except OSError as exc:  # pragma: no cover - environment specific
             raise CGBNLibraryError(f"failed to load {LIB_PATH}: {exc}") from exc
+        # a stale or foreign build must not be called with these argument lists
+        missing = [n for n in SIGNATURES if not hasattr(lib, n)]
+        if missing:
+            raise CGBNLibraryError(
+                f"{LIB_PATH} lacks {len(missing)} entry point(s) of include/cgbn.h "
+                f"({', '.join(missing[:4])}{', ...' if len(missing) > 4 else ''}); rebuild "
+                "it with `make`")
+        lib.cgbn_abi_version.restype = _i
+        lib.cgbn_abi_version.argtypes = []
+        got = lib.cgbn_abi_version()
+        if got != ABI_VERSION:
+            raise CGBNLibraryError(
+                f"{LIB_PATH} implements CGBN ABI v{got}, these bindings need v{ABI_VERSION}; "
+                "rebuild it with `make`")
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -189,6 +189,14 @@ class BNForwardCache:
     relu: bool = False
     one_pass: bool = False
     _total_count: int | None = field(default=None, repr=False)
+    _x_version: int | None = field(default=None, repr=False)
+
+    def __post_init__(self):
+        # x is saved by reference (the backward recomputes x_hat and the ReLU mask from
+        # it), so an in-place change of x before the backward is detected, as autograd
+        # does for saved tensors
+        if self._x_version is None:
+            self._x_version = self.x._version
 
     @property
     def channels(self) -> int:
@@ -556,6 +564,10 @@ def _backward_core(dy, cache: BNForwardCache, state: BNLayerState, exchange, gro
     kernel when enabled (set_fused) and dy, x fit on chip."""
     if not cache.train:
         raise BatchNormError("backward requires a training-mode forward cache")
+    if cache.x._version != cache._x_version:
+        raise BatchNormError(
+            "the forward input was modified in place after the forward; the backward "
+            "recomputes x_hat from it (save a copy, or run the backward first)")
     if not isinstance(dy, torch.Tensor):
         raise BatchNormError(f"dy must be a torch.Tensor, got {type(dy).__name__}")
     if tuple(dy.shape) != tuple(cache.x.shape):

@@ -67,6 +67,35 @@
 #include "cgbn.h"
 #include "cgbn_slots.cuh"
 
+// The library is built from this file three times, once per activation dtype
+// (-DCGBN_TU_ACT=0 fp32, 1 bf16, 2 fp16), so the per-dtype kernel families compile in
+// parallel. Each unit exports its dtype's entry points with a suffix (cgbn_fwd_stats_a1,
+// ...); unit 0 also exports the dtype-independent entry points and the public names,
+// which route on the dtype bits of `layout` (include/cgbn.h).
+#ifndef CGBN_TU_ACT
+#define CGBN_TU_ACT 0
+#endif
+#define CGBN_CAT2(a, b) a##b
+#define CGBN_CAT(a, b) CGBN_CAT2(a, b)
+#define CGBN_FN(name) CGBN_CAT(name, CGBN_CAT(_a, CGBN_TU_ACT))
+
+namespace {
+#if CGBN_TU_ACT == 1
+using TuAct = __nv_bfloat16;
+#elif CGBN_TU_ACT == 2
+using TuAct = __half;
+#else
+using TuAct = float;
+#endif
+}  // namespace
+
+#define CGBN_ROUTED(act)                                                                   \
+  do {                                                                                     \
+    if ((act) != CGBN_TU_ACT)                                                              \
+      return set_error(CGBN_ERR_INVALID, "internal: activation dtype %d routed to unit %d", \
+                       (int)(act), CGBN_TU_ACT);                                           \
+  } while (0)
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -75,7 +104,7 @@ constexpr uint32_t kTeamMaxLv = 2048;  // channels up to this many units use tea
 constexpr int64_t kMinElemsPerCta = 2048;
 constexpr int kMaxCtasPerSm = 8;  // 2048 threads / 256
 // Workspace head: 65536 per-channel tickets (fixed size: independent of C), then 64
-// words of grid-barrier state for the fused cooperative kernels.
+// reserved words (kept so the workspace layout and size stay those of ABI v6).
 constexpr size_t kTicketWords = 65536;
 constexpr size_t kTicketBytes = (kTicketWords + 64) * sizeof(unsigned);
 
@@ -85,42 +114,28 @@ constexpr size_t kTicketBytes = (kTicketWords + 64) * sizeof(unsigned);
 #include "cgbn_ops.cuh"
 #include "cgbn_reduce.cuh"
 #include "cgbn_ew.cuh"
-#include "cgbn_tma.cuh"
-#include "cgbn_fused.cuh"
+#include "cgbn_onchip.cuh"
 #include "cgbn_p2p.cuh"
 #include "cgbn_host.cuh"
 
-// Error hook for the other translation unit (cgbn_conv.cu): one thread-local message
-// behind cgbn_last_error().
-int cgbn_internal_set_error(int code, const char* msg) { return set_error(code, "%s", msg); }
+#if CGBN_TU_ACT == 0
+// The one thread-local error message behind cgbn_last_error(), shared by every unit
+// (set_error forwards here; cgbn_conv.cu too).
+namespace {
+thread_local std::string g_last_error;
+}
+int cgbn_internal_set_error(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
+#endif
 
 // ==================================================================================
 // C ABI
 
 extern "C" {
 
-int cgbn_abi_version(void) { return CGBN_ABI_VERSION; }
-
-#define CGBN_STR2(x) #x
-#define CGBN_STR(x) CGBN_STR2(x)
-const char* cgbn_build_info(void) {
-  return "cgbn sm_100a; nvcc " CGBN_STR(__CUDACC_VER_MAJOR__) "." CGBN_STR(__CUDACC_VER_MINOR__)
-         "; cluster-team / row reductions (fp64) + memory-order elementwise, PDL; fp32 / bf16 / "
-         "fp16 activations; fused cooperative and TMA variants opt-in";
-}
-
-const char* cgbn_last_error(void) { return g_last_error.c_str(); }
-
-int cgbn_num_sms(void) { return num_sms_cached(); }
-
-size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout) {
-  int act = 0;
-  if (split_fmt(&layout, &act)) return 0;
-  if (validate_shape(N, C, HW, layout)) return 0;
-  return ws_bytes_for(N, C, HW, layout, num_sms_cached());
-}
-
-int cgbn_fwd_stats(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_fwd_stats)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                    double* partial, void* ws, size_t ws_bytes, void* stream) {
   int act = 0;
   CGBN_TRY(split_fmt(&layout, &act));
@@ -135,7 +150,7 @@ int cgbn_fwd_stats(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
   return check_launch("cgbn_fwd_stats");
 }
 
-int cgbn_channel_sum(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_channel_sum)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                      double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream) {
   int act = 0;
   CGBN_TRY(split_fmt(&layout, &act));
@@ -146,12 +161,11 @@ int cgbn_channel_sum(const void* x, int64_t N, int64_t C, int64_t HW, int layout
   WsView w;
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  pl.tma = false;
   CGBN_TRY(dispatch_stats(pl, x, false, kRawSums, sum, sum_sq, nullptr, w, st));
   return check_launch("cgbn_channel_sum");
 }
 
-int cgbn_centered_sumsq(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_centered_sumsq)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                         const double* sum, const double* count, double* out, void* ws,
                         size_t ws_bytes, void* stream) {
   int act = 0;
@@ -163,12 +177,11 @@ int cgbn_centered_sumsq(const void* x, int64_t N, int64_t C, int64_t HW, int lay
   WsView w;
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  pl.tma = false;
   CGBN_TRY(dispatch_stats(pl, x, false, kSumSq, out, nullptr, nullptr, w, st, sum, count));
   return check_launch("cgbn_centered_sumsq");
 }
 
-int cgbn_fwd_normalize_sums(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_fwd_normalize_sums)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                             const double* sum, const double* sq, const double* count,
                             int centered, const float* gamma, const float* beta, double eps,
                             double momentum, float* running_mean, float* running_var,
@@ -191,7 +204,7 @@ int cgbn_fwd_normalize_sums(const void* x, int64_t N, int64_t C, int64_t HW, int
   return check_launch("cgbn_fwd_normalize_sums");
 }
 
-int cgbn_fwd_normalize(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_fwd_normalize)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                        const double* const* partials, int G, const float* gamma,
                        const float* beta, double eps, double momentum, float* running_mean,
                        float* running_var, double* saved, int relu, void* y, unsigned* status,
@@ -214,7 +227,7 @@ int cgbn_fwd_normalize(const void* x, int64_t N, int64_t C, int64_t HW, int layo
   return check_launch("cgbn_fwd_normalize");
 }
 
-int cgbn_fwd_train_local(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_fwd_train_local)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                          const float* gamma, const float* beta, double eps, double momentum,
                          float* running_mean, float* running_var, double* saved, int relu,
                          void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
@@ -232,13 +245,24 @@ int cgbn_fwd_train_local(const void* x, int64_t N, int64_t C, int64_t HW, int la
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
-  pl.tma = false;  // the TMA reductions only emit partials
+  // single launch with the activation held on chip when the layer fits (cgbn_onchip.cuh)
+  onchip::Args oa;
+  oa.trace = nullptr;
+  oa.x = x;
+  oa.dy = nullptr;
+  oa.out = y;
+  oa.F = F;
+  oa.F.P = oa.F.Q = nullptr;
+  const int oc = try_onchip<false>(act, relu != 0, N, C, HW, layout,
+                                   (uintptr_t)x | (uintptr_t)y, oa, st);
+  if (oc < 0) return -oc;
+  if (oc == 1) return check_launch("cgbn_fwd_train_local");
   CGBN_TRY(dispatch_stats(pl, x, true, kLocalFinal, nullptr, nullptr, &F, w, st));
   launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
   return check_launch("cgbn_fwd_train_local");
 }
 
-int cgbn_fwd_eval(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_fwd_eval)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                   const float* gamma, const float* beta, const float* running_mean,
                   const float* running_var, double eps, int relu, void* y, void* ws,
                   size_t ws_bytes, void* stream) {
@@ -259,7 +283,7 @@ int cgbn_fwd_eval(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
   return check_launch("cgbn_fwd_eval");
 }
 
-int cgbn_xhat(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_xhat)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
               const double* saved, void* xhat, void* ws, size_t ws_bytes, void* stream) {
   int act = 0;
   CGBN_TRY(split_fmt(&layout, &act));
@@ -275,7 +299,7 @@ int cgbn_xhat(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
   return check_launch("cgbn_xhat");
 }
 
-int cgbn_channel_affine(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_channel_affine)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                         const double* scale, const double* shift, void* out, void* stream) {
   int act = 0;
   CGBN_TRY(split_fmt(&layout, &act));
@@ -288,7 +312,7 @@ int cgbn_channel_affine(const void* x, int64_t N, int64_t C, int64_t HW, int lay
   return check_launch("cgbn_channel_affine");
 }
 
-int cgbn_bwd_reduce(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
+int CGBN_FN(cgbn_bwd_reduce)(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
                     int layout, const double* saved, const float* gamma, const float* beta,
                     int relu, double* partial, void* ws, size_t ws_bytes, void* stream) {
   int act = 0;
@@ -306,7 +330,7 @@ int cgbn_bwd_reduce(const void* dy, const void* x, int64_t N, int64_t C, int64_t
   return check_launch("cgbn_bwd_reduce");
 }
 
-int cgbn_bwd_dx(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+int CGBN_FN(cgbn_bwd_dx)(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                 const double* const* partials, int G, const double* saved, const float* gamma,
                 const float* beta, double eps, int relu, void* dx, float* dgamma,
                 float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
@@ -330,7 +354,7 @@ int cgbn_bwd_dx(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
   return check_launch("cgbn_bwd_dx");
 }
 
-int cgbn_bwd_local(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
+int CGBN_FN(cgbn_bwd_local)(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
                    int layout, const double* saved, const float* gamma, const float* beta,
                    double eps, int relu, void* dx, float* dgamma, float* dbeta,
                    unsigned* status, void* ws, size_t ws_bytes, void* stream) {
@@ -350,74 +374,315 @@ int cgbn_bwd_local(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const BwdFinal F =
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
-  pl.tma = false;
+  onchip::Args oa;
+  oa.trace = nullptr;
+  oa.x = x;
+  oa.dy = dy;
+  oa.out = dx;
+  oa.B = F;
+  oa.B.A = oa.B.B = oa.B.Cc = oa.B.P = oa.B.Q = nullptr;
+  const int oc = try_onchip<true>(act, relu != 0, N, C, HW, layout,
+                                  (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, oa, st);
+  if (oc < 0) return -oc;
+  if (oc == 1) return check_launch("cgbn_bwd_local");
   CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kLocalFinal, nullptr,
                                &F, w, st));
   launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
   return check_launch("cgbn_bwd_local");
 }
 
-int cgbn_fused_supported(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
-  int act = 0;
-  if (split_fmt(&layout, &act) || act != 0) return 0;  // fp32 only
-  fused::FGeom fg;
-  return fused_plan(N, C, HW, layout, 0, backward ? 2 : 1, &fg) ? 1 : 0;
+// Debug hook (not in include/cgbn.h): record per-CTA phase timestamps of this unit's
+// on-chip launches into a device buffer of 8 u64 per CTA (NULL: off). tools/onchip_trace.py.
+int CGBN_FN(cgbn_debug_onchip_trace)(void* dev_buf) {
+  g_onchip_trace = static_cast<unsigned long long*>(dev_buf);
+  return CGBN_OK;
 }
 
-int cgbn_fwd_fused(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
-                   const float* gamma, const float* beta, double eps, double momentum,
-                   float* running_mean, float* running_var, double* saved, int relu, void* y,
-                   unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+// The single-launch on-chip passes (cgbn_onchip.cuh) on request: the *_local entry points
+// pick them by themselves whenever a layer fits; these force them (error if not eligible).
+int CGBN_FN(cgbn_fused_supported)(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
+  int act = 0;
+  if (split_fmt(&layout, &act)) return 0;
+  return (backward ? onchip_supported<true>(act, false, N, C, HW, layout)
+                   : onchip_supported<false>(act, false, N, C, HW, layout))
+             ? 1
+             : 0;
+}
+
+int CGBN_FN(cgbn_fwd_fused)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                            const float* gamma, const float* beta, double eps, double momentum,
+                            float* running_mean, float* running_var, double* saved, int relu,
+                            void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
   int act = 0;
   CGBN_TRY(split_fmt(&layout, &act));
-  if (act != 0) return set_error(CGBN_ERR_UNSUPPORTED, "%s: fp32 activations only", "cgbn_fwd_fused");
   CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
   CGBN_TRY(validate_shape(N, C, HW, layout));
-  fused::FGeom fg;
-  if (!fused_plan(N, C, HW, layout, (uintptr_t)x | (uintptr_t)y, 1, &fg))
-    return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_fwd_fused: shape/layout not eligible");
   WsView w;
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  FwdFinal F =
-      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
-  F.P = F.Q = nullptr;  // the fused kernel keeps its coefficients in shared memory
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const float* xf = static_cast<const float*>(x);
-  float* yf = static_cast<float*>(y);
-  CGBN_TRY(relu ? launch_cooperative(fused::k_fused_fwd<true>, fg.grid, fused::kSmemBytes, st, fg,
-                                     xf, yf, F, w.slots, w.bar)
-                : launch_cooperative(fused::k_fused_fwd<false>, fg.grid, fused::kSmemBytes, st,
-                                     fg, xf, yf, F, w.slots, w.bar));
+  onchip::Args oa;
+  oa.trace = nullptr;
+  oa.x = x;
+  oa.dy = nullptr;
+  oa.out = y;
+  oa.F = make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  oa.F.P = oa.F.Q = nullptr;  // the coefficients stay in shared memory
+  const int oc = try_onchip<false>(act, relu != 0, N, C, HW, layout,
+                                   (uintptr_t)x | (uintptr_t)y, oa,
+                                   reinterpret_cast<cudaStream_t>(stream));
+  if (oc < 0) return -oc;
+  if (oc == 0) return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_fwd_fused: layer does not fit on chip");
   return check_launch("cgbn_fwd_fused");
 }
 
-int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
-                   const double* saved, const float* gamma, const float* beta, double eps,
-                   int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
-                   size_t ws_bytes, void* stream) {
+int CGBN_FN(cgbn_bwd_fused)(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
+                            int layout, const double* saved, const float* gamma,
+                            const float* beta, double eps, int relu, void* dx, float* dgamma,
+                            float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
+                            void* stream) {
   int act = 0;
   CGBN_TRY(split_fmt(&layout, &act));
-  if (act != 0) return set_error(CGBN_ERR_UNSUPPORTED, "%s: fp32 activations only", "cgbn_bwd_fused");
   CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_fused: NULL pointer");
   CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
   CGBN_REQUIRE(!relu || beta, "cgbn_bwd_fused: relu needs beta");
   CGBN_TRY(validate_shape(N, C, HW, layout));
-  fused::FGeom fg;
-  if (!fused_plan(N, C, HW, layout, (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, 2, &fg))
-    return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_bwd_fused: shape/layout not eligible");
   WsView w;
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  BwdFinal F = make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
-  F.A = F.B = F.Cc = F.P = F.Q = nullptr;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const float* dyf = static_cast<const float*>(dy);
-  const float* xf = static_cast<const float*>(x);
-  float* dxf = static_cast<float*>(dx);
-  CGBN_TRY(relu ? launch_cooperative(fused::k_fused_bwd<true>, fg.grid, fused::kSmemBytes, st, fg,
-                                     dyf, xf, dxf, F, w.slots, w.bar)
-                : launch_cooperative(fused::k_fused_bwd<false>, fg.grid, fused::kSmemBytes, st,
-                                     fg, dyf, xf, dxf, F, w.slots, w.bar));
+  onchip::Args oa;
+  oa.trace = nullptr;
+  oa.x = x;
+  oa.dy = dy;
+  oa.out = dx;
+  oa.B = make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
+  oa.B.A = oa.B.B = oa.B.Cc = oa.B.P = oa.B.Q = nullptr;
+  const int oc = try_onchip<true>(act, relu != 0, N, C, HW, layout,
+                                  (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, oa,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (oc < 0) return -oc;
+  if (oc == 0) return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_bwd_fused: layer does not fit on chip");
   return check_launch("cgbn_bwd_fused");
+}
+
+
+// ---- fused exchange (SURVEY 8(e) backend 3): the reductions' finishers push the rank's
+// partial into every region and the last one publishes; the finalize kernel waits.
+
+}  // extern "C"
+
+namespace {
+int make_push(p2p::Push* P, int rank, int G, void* const* regions, int64_t max_len,
+              int64_t need, int64_t C) {
+  if (G < 1 || G > p2p::kMaxPush)
+    return set_error(CGBN_ERR_INVALID, "fused exchange: group size %d outside [1, %d]", G,
+                     p2p::kMaxPush);
+  if (rank < 0 || rank >= G) return set_error(CGBN_ERR_INVALID, "rank %d outside [0, %d)", rank, G);
+  if (!regions) return set_error(CGBN_ERR_INVALID, "regions array is NULL");
+  if (need > max_len)
+    return set_error(CGBN_ERR_INVALID, "partial of %lld values exceeds max_len %lld",
+                     (long long)need, (long long)max_len);
+  for (int q = 0; q < G; ++q) {
+    if (!regions[q]) return set_error(CGBN_ERR_INVALID, "regions[%d] is NULL", q);
+    P->base[q] = static_cast<char*>(regions[q]);
+  }
+  for (int q = G; q < p2p::kMaxPush; ++q) P->base[q] = nullptr;
+  P->rank = rank;
+  P->G = G;
+  P->max_len = max_len;
+  P->nfinish = (unsigned)C;
+  return CGBN_OK;
+}
+
+int make_pull(p2p::Pull* P, void* region, int G, int64_t max_len, int64_t need,
+              unsigned* status, double timeout_s) {
+  if (G < 1 || G > p2p::kMaxPeers)
+    return set_error(CGBN_ERR_INVALID, "group size %d outside [1, %d]", G, p2p::kMaxPeers);
+  if (!region) return set_error(CGBN_ERR_INVALID, "region is NULL");
+  if (need > max_len)
+    return set_error(CGBN_ERR_INVALID, "partial of %lld values exceeds max_len %lld",
+                     (long long)need, (long long)max_len);
+  if (!(timeout_s > 0.0)) return set_error(CGBN_ERR_INVALID, "timeout must be positive");
+  P->own = static_cast<char*>(region);
+  P->G = G;
+  P->max_len = max_len;
+  P->status = status;
+  P->timeout_ns = (uint64_t)(timeout_s * 1e9);
+  return CGBN_OK;
+}
+
+struct PushScope {  // the push applies to the reductions dispatched while it is alive
+  explicit PushScope(const p2p::Push* p) { g_push = p; }
+  ~PushScope() { g_push = nullptr; }
+};
+}  // namespace
+
+extern "C" {
+
+int CGBN_FN(cgbn_fwd_stats_p2p)(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank,
+                       int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes,
+                       void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_REQUIRE(x, "cgbn_fwd_stats_p2p: NULL pointer");
+  const void* ptrs[] = {x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, act, ptrs, 1, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  p2p::Push push;
+  CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C + 1, C));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  PushScope scope(&push);
+  CGBN_TRY(dispatch_stats(pl, x, true, kPartial, nullptr, nullptr, nullptr, w, st));
+  return check_launch("cgbn_fwd_stats_p2p");
+}
+
+int CGBN_FN(cgbn_fwd_normalize_p2p)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                           void* region, int G, int64_t max_len, double timeout_s,
+                           const float* gamma, const float* beta, double eps, double momentum,
+                           float* running_mean, float* running_var, double* saved, int relu,
+                           void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  const void* ptrs[] = {x, y};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 2, &ep));
+  p2p::Pull pull;
+  CGBN_TRY(make_pull(&pull, region, G, max_len, 2 * C + 1, status, timeout_s));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  launch_pdl(k_finalize_fwd_p2p, chan_blocks(C), true, st, pull, F);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  return check_launch("cgbn_fwd_normalize_p2p");
+}
+
+int CGBN_FN(cgbn_bwd_reduce_p2p)(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
+                        int layout, const double* saved, const float* gamma, const float* beta,
+                        int relu, int rank, int G, void* const* regions, int64_t max_len,
+                        void* ws, size_t ws_bytes, void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_REQUIRE(dy && x && saved, "cgbn_bwd_reduce_p2p: NULL pointer");
+  CGBN_REQUIRE(!relu || (gamma && beta), "cgbn_bwd_reduce_p2p: relu needs gamma and beta");
+  const void* ptrs[] = {dy, x};
+  Plan pl;
+  CGBN_TRY(make_plan(N, C, HW, layout, act, ptrs, 2, &pl));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  p2p::Push push;
+  CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C, C));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  PushScope scope(&push);
+  CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, nullptr,
+                               nullptr, w, st));
+  return check_launch("cgbn_bwd_reduce_p2p");
+}
+
+int CGBN_FN(cgbn_bwd_dx_p2p)(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                    void* region, int G, int64_t max_len, double timeout_s, const double* saved,
+                    const float* gamma, const float* beta, double eps, int relu, void* dx,
+                    float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
+                    void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_dx_p2p: NULL pointer");
+  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
+  CGBN_REQUIRE(!relu || beta, "cgbn_bwd_dx_p2p: relu needs beta");
+  const void* ptrs[] = {dy, x, dx};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 3, &ep));
+  p2p::Pull pull;
+  CGBN_TRY(make_pull(&pull, region, G, max_len, 2 * C, status, timeout_s));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const BwdFinal F =
+      make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
+  launch_pdl(k_finalize_bwd_p2p, chan_blocks(C), true, st, pull, F);
+  launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
+  return check_launch("cgbn_bwd_dx_p2p");
+}
+
+// ---- producer fusion, single-rank group: the conv's statistics slots -> coefficients in
+// one kernel (merge + the forward finisher), then the elementwise pass.
+}  // extern "C"
+
+namespace {
+__global__ void __launch_bounds__(1024) k_finalize_slots(const void* slot_ws, FwdFinal F) {
+  __shared__ double sn[32][32], sa[32][32], sb[32][32];
+  pdl_wait();  // the slot table comes from the conv kernel
+  const cgbn_slots::Header h = *static_cast<const cgbn_slots::Header*>(slot_ws);
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double n, mean, M2;
+  cgbn_slots::merge(cgbn_slots::table(slot_ws), h.cout, h.mtiles, h.grid, h.nslots, c, sn, sa,
+                    sb, n, mean, M2);
+  pdl_trigger();
+  if ((threadIdx.x >> 5) == 0 && c < (int)F.C) {
+    double P, Q;
+    finalize_fwd_channel(F, (uint32_t)c, n, mean, M2, true, P, Q);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int CGBN_FN(cgbn_fwd_normalize_slots)(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
+                             const void* slot_ws, const float* gamma, const float* beta,
+                             double eps, double momentum, float* running_mean,
+                             float* running_var, double* saved, int relu, void* y,
+                             unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  int act = 0;
+  CGBN_TRY(split_fmt(&layout, &act));
+  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
+  CGBN_REQUIRE(slot_ws, "cgbn_fwd_normalize_slots: NULL slot table");
+  const void* ptrs[] = {x, y};
+  EwPlan ep;
+  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 2, &ep));
+  WsView w;
+  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FwdFinal F =
+      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((C + 31) / 32));
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_finalize_slots, slot_ws, F);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  return check_launch("cgbn_fwd_normalize_slots");
+}
+
+
+// ---- unit 0: dtype-independent entry points
+#if CGBN_TU_ACT == 0
+
+int cgbn_abi_version(void) { return CGBN_ABI_VERSION; }
+
+#define CGBN_STR2(x) #x
+#define CGBN_STR(x) CGBN_STR2(x)
+const char* cgbn_build_info(void) {
+  return "cgbn sm_100a; nvcc " CGBN_STR(__CUDACC_VER_MAJOR__) "." CGBN_STR(__CUDACC_VER_MINOR__)
+         "; on-chip single-launch passes (cluster DSMEM, bulk copies) for layers that fit, "
+         "else cluster-team / row reductions (fp64) + memory-order elementwise; PDL; fp32 / "
+         "bf16 / fp16 activations";
+}
+
+const char* cgbn_last_error(void) { return g_last_error.c_str(); }
+
+int cgbn_num_sms(void) { return num_sms_cached(); }
+
+size_t cgbn_workspace_bytes(int64_t N, int64_t C, int64_t HW, int layout) {
+  int act = 0;
+  if (split_fmt(&layout, &act)) return 0;
+  if (validate_shape(N, C, HW, layout)) return 0;
+  return ws_bytes_for(N, C, HW, layout, num_sms_cached());
 }
 
 size_t cgbn_p2p_region_bytes(int G, int64_t max_len) {
@@ -466,6 +731,8 @@ int cgbn_p2p_free(void* region) {
   return CGBN_OK;
 }
 
+}  // extern "C"
+
 namespace {
 int fill_peers(p2p::Peers* P, void* const* regions, int G) {
   if (G < 1 || G > p2p::kMaxPeers)
@@ -479,6 +746,8 @@ int fill_peers(p2p::Peers* P, void* const* regions, int G) {
   return CGBN_OK;
 }
 }  // namespace
+
+extern "C" {
 
 int cgbn_p2p_exchange(const double* vec, int64_t n, int rank, int G, void* const* regions,
                       int64_t max_len, double* out, unsigned* status, double timeout_s,
@@ -515,196 +784,6 @@ int cgbn_p2p_emulate(const double* vecs, int64_t n, int G, void* const* regions,
   return check_launch("cgbn_p2p_emulate");
 }
 
-// ---- fused exchange (SURVEY 8(e) backend 3): the reductions' finishers push the rank's
-// partial into every region and the last one publishes; the finalize kernel waits.
-
-namespace {
-int make_push(p2p::Push* P, int rank, int G, void* const* regions, int64_t max_len,
-              int64_t need, int64_t C) {
-  if (G < 1 || G > p2p::kMaxPush)
-    return set_error(CGBN_ERR_INVALID, "fused exchange: group size %d outside [1, %d]", G,
-                     p2p::kMaxPush);
-  if (rank < 0 || rank >= G) return set_error(CGBN_ERR_INVALID, "rank %d outside [0, %d)", rank, G);
-  if (!regions) return set_error(CGBN_ERR_INVALID, "regions array is NULL");
-  if (need > max_len)
-    return set_error(CGBN_ERR_INVALID, "partial of %lld values exceeds max_len %lld",
-                     (long long)need, (long long)max_len);
-  for (int q = 0; q < G; ++q) {
-    if (!regions[q]) return set_error(CGBN_ERR_INVALID, "regions[%d] is NULL", q);
-    P->base[q] = static_cast<char*>(regions[q]);
-  }
-  for (int q = G; q < p2p::kMaxPush; ++q) P->base[q] = nullptr;
-  P->rank = rank;
-  P->G = G;
-  P->max_len = max_len;
-  P->nfinish = (unsigned)C;
-  return CGBN_OK;
-}
-
-int make_pull(p2p::Pull* P, void* region, int G, int64_t max_len, int64_t need,
-              unsigned* status, double timeout_s) {
-  if (G < 1 || G > p2p::kMaxPeers)
-    return set_error(CGBN_ERR_INVALID, "group size %d outside [1, %d]", G, p2p::kMaxPeers);
-  if (!region) return set_error(CGBN_ERR_INVALID, "region is NULL");
-  if (need > max_len)
-    return set_error(CGBN_ERR_INVALID, "partial of %lld values exceeds max_len %lld",
-                     (long long)need, (long long)max_len);
-  if (!(timeout_s > 0.0)) return set_error(CGBN_ERR_INVALID, "timeout must be positive");
-  P->own = static_cast<char*>(region);
-  P->G = G;
-  P->max_len = max_len;
-  P->status = status;
-  P->timeout_ns = (uint64_t)(timeout_s * 1e9);
-  return CGBN_OK;
-}
-
-struct PushScope {  // the push applies to the reductions dispatched while it is alive
-  explicit PushScope(const p2p::Push* p) { g_push = p; }
-  ~PushScope() { g_push = nullptr; }
-};
-}  // namespace
-
-int cgbn_fwd_stats_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank,
-                       int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes,
-                       void* stream) {
-  int act = 0;
-  CGBN_TRY(split_fmt(&layout, &act));
-  CGBN_REQUIRE(x, "cgbn_fwd_stats_p2p: NULL pointer");
-  const void* ptrs[] = {x};
-  Plan pl;
-  CGBN_TRY(make_plan(N, C, HW, layout, act, ptrs, 1, &pl));
-  WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  p2p::Push push;
-  CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C + 1, C));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  pl.tma = false;
-  PushScope scope(&push);
-  CGBN_TRY(dispatch_stats(pl, x, true, kPartial, nullptr, nullptr, nullptr, w, st));
-  return check_launch("cgbn_fwd_stats_p2p");
-}
-
-int cgbn_fwd_normalize_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
-                           void* region, int G, int64_t max_len, double timeout_s,
-                           const float* gamma, const float* beta, double eps, double momentum,
-                           float* running_mean, float* running_var, double* saved, int relu,
-                           void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
-  int act = 0;
-  CGBN_TRY(split_fmt(&layout, &act));
-  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
-  const void* ptrs[] = {x, y};
-  EwPlan ep;
-  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 2, &ep));
-  p2p::Pull pull;
-  CGBN_TRY(make_pull(&pull, region, G, max_len, 2 * C + 1, status, timeout_s));
-  WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const FwdFinal F =
-      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
-  launch_pdl(k_finalize_fwd_p2p, chan_blocks(C), true, st, pull, F);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
-  return check_launch("cgbn_fwd_normalize_p2p");
-}
-
-int cgbn_bwd_reduce_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW,
-                        int layout, const double* saved, const float* gamma, const float* beta,
-                        int relu, int rank, int G, void* const* regions, int64_t max_len,
-                        void* ws, size_t ws_bytes, void* stream) {
-  int act = 0;
-  CGBN_TRY(split_fmt(&layout, &act));
-  CGBN_REQUIRE(dy && x && saved, "cgbn_bwd_reduce_p2p: NULL pointer");
-  CGBN_REQUIRE(!relu || (gamma && beta), "cgbn_bwd_reduce_p2p: relu needs gamma and beta");
-  const void* ptrs[] = {dy, x};
-  Plan pl;
-  CGBN_TRY(make_plan(N, C, HW, layout, act, ptrs, 2, &pl));
-  WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  p2p::Push push;
-  CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C, C));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  pl.tma = false;
-  PushScope scope(&push);
-  CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, nullptr,
-                               nullptr, w, st));
-  return check_launch("cgbn_bwd_reduce_p2p");
-}
-
-int cgbn_bwd_dx_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout,
-                    void* region, int G, int64_t max_len, double timeout_s, const double* saved,
-                    const float* gamma, const float* beta, double eps, int relu, void* dx,
-                    float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes,
-                    void* stream) {
-  int act = 0;
-  CGBN_TRY(split_fmt(&layout, &act));
-  CGBN_REQUIRE(dy && x && saved && gamma && dx, "cgbn_bwd_dx_p2p: NULL pointer");
-  CGBN_REQUIRE(eps > 0.0, "eps must be positive, got %g", eps);
-  CGBN_REQUIRE(!relu || beta, "cgbn_bwd_dx_p2p: relu needs beta");
-  const void* ptrs[] = {dy, x, dx};
-  EwPlan ep;
-  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 3, &ep));
-  p2p::Pull pull;
-  CGBN_TRY(make_pull(&pull, region, G, max_len, 2 * C, status, timeout_s));
-  WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const BwdFinal F =
-      make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
-  launch_pdl(k_finalize_bwd_p2p, chan_blocks(C), true, st, pull, F);
-  launch_ew_dx(ep, relu != 0, dy, x, dx, w, st);
-  return check_launch("cgbn_bwd_dx_p2p");
-}
-
-// ---- producer fusion, single-rank group: the conv's statistics slots -> coefficients in
-// one kernel (merge + the forward finisher), then the elementwise pass.
-namespace {
-__global__ void __launch_bounds__(1024) k_finalize_slots(const void* slot_ws, FwdFinal F) {
-  __shared__ double sn[32][32], sa[32][32], sb[32][32];
-  pdl_wait();  // the slot table comes from the conv kernel
-  const cgbn_slots::Header h = *static_cast<const cgbn_slots::Header*>(slot_ws);
-  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
-  double n, mean, M2;
-  cgbn_slots::merge(cgbn_slots::table(slot_ws), h.cout, h.mtiles, h.grid, h.nslots, c, sn, sa,
-                    sb, n, mean, M2);
-  pdl_trigger();
-  if ((threadIdx.x >> 5) == 0 && c < (int)F.C) {
-    double P, Q;
-    finalize_fwd_channel(F, (uint32_t)c, n, mean, M2, true, P, Q);
-  }
-}
-}  // namespace
-
-int cgbn_fwd_normalize_slots(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
-                             const void* slot_ws, const float* gamma, const float* beta,
-                             double eps, double momentum, float* running_mean,
-                             float* running_var, double* saved, int relu, void* y,
-                             unsigned* status, void* ws, size_t ws_bytes, void* stream) {
-  int act = 0;
-  CGBN_TRY(split_fmt(&layout, &act));
-  CGBN_TRY(check_fwd_args(x, y, gamma, beta, saved, eps, momentum, running_mean, running_var));
-  CGBN_REQUIRE(slot_ws, "cgbn_fwd_normalize_slots: NULL slot table");
-  const void* ptrs[] = {x, y};
-  EwPlan ep;
-  CGBN_TRY(make_ew(N, C, HW, layout, act, ptrs, 2, &ep));
-  WsView w;
-  CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const FwdFinal F =
-      make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((C + 31) / 32));
-  cfg.blockDim = dim3(1024);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k_finalize_slots, slot_ws, F);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
-  return check_launch("cgbn_fwd_normalize_slots");
-}
-
 int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void* out,
                   void* stream) {
   CGBN_REQUIRE(vectors && out, "cgbn_fold_sum: NULL pointer");
@@ -722,5 +801,210 @@ int cgbn_fold_sum(const void* const* vectors, int G, int64_t n, int dtype, void*
     k_fold_sum<float><<<(unsigned)blocks, threads, 0, st>>>(P, n, reinterpret_cast<float*>(out));
   return check_launch("cgbn_fold_sum");
 }
+
+
+// Public names: route on the activation dtype in bits 4..7 of `layout` (an unknown
+// dtype goes to unit 0, which reports it).
+int cgbn_fwd_stats_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, double* partial, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_stats_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, double* partial, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_stats(const void* x, int64_t N, int64_t C, int64_t HW, int layout, double* partial, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_stats_a1(x, N, C, HW, layout, partial, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_stats_a2(x, N, C, HW, layout, partial, ws, ws_bytes, stream);
+    default: return cgbn_fwd_stats_a0(x, N, C, HW, layout, partial, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_channel_sum_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream);
+int cgbn_channel_sum_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream);
+int cgbn_channel_sum(const void* x, int64_t N, int64_t C, int64_t HW, int layout, double* sum, double* sum_sq, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_channel_sum_a1(x, N, C, HW, layout, sum, sum_sq, ws, ws_bytes, stream);
+    case 2: return cgbn_channel_sum_a2(x, N, C, HW, layout, sum, sum_sq, ws, ws_bytes, stream);
+    default: return cgbn_channel_sum_a0(x, N, C, HW, layout, sum, sum_sq, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_centered_sumsq_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* sum, const double* count, double* out, void* ws, size_t ws_bytes, void* stream);
+int cgbn_centered_sumsq_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* sum, const double* count, double* out, void* ws, size_t ws_bytes, void* stream);
+int cgbn_centered_sumsq(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* sum, const double* count, double* out, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_centered_sumsq_a1(x, N, C, HW, layout, sum, count, out, ws, ws_bytes, stream);
+    case 2: return cgbn_centered_sumsq_a2(x, N, C, HW, layout, sum, count, out, ws, ws_bytes, stream);
+    default: return cgbn_centered_sumsq_a0(x, N, C, HW, layout, sum, count, out, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_normalize_sums_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* sum, const double* sq, const double* count, int centered, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_sums_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* sum, const double* sq, const double* count, int centered, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_sums(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* sum, const double* sq, const double* count, int centered, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_normalize_sums_a1(x, N, C, HW, layout, sum, sq, count, centered, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_normalize_sums_a2(x, N, C, HW, layout, sum, sq, count, centered, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    default: return cgbn_fwd_normalize_sums_a0(x, N, C, HW, layout, sum, sq, count, centered, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_normalize_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* const* partials, int G, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* const* partials, int G, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* const* partials, int G, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_normalize_a1(x, N, C, HW, layout, partials, G, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_normalize_a2(x, N, C, HW, layout, partials, G, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    default: return cgbn_fwd_normalize_a0(x, N, C, HW, layout, partials, G, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_train_local_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_train_local_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_train_local(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_train_local_a1(x, N, C, HW, layout, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_train_local_a2(x, N, C, HW, layout, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    default: return cgbn_fwd_train_local_a0(x, N, C, HW, layout, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_eval_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, const float* running_mean, const float* running_var, double eps, int relu, void* y, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_eval_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, const float* running_mean, const float* running_var, double eps, int relu, void* y, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_eval(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, const float* running_mean, const float* running_var, double eps, int relu, void* y, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_eval_a1(x, N, C, HW, layout, gamma, beta, running_mean, running_var, eps, relu, y, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_eval_a2(x, N, C, HW, layout, gamma, beta, running_mean, running_var, eps, relu, y, ws, ws_bytes, stream);
+    default: return cgbn_fwd_eval_a0(x, N, C, HW, layout, gamma, beta, running_mean, running_var, eps, relu, y, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_xhat_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, void* xhat, void* ws, size_t ws_bytes, void* stream);
+int cgbn_xhat_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, void* xhat, void* ws, size_t ws_bytes, void* stream);
+int cgbn_xhat(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, void* xhat, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_xhat_a1(x, N, C, HW, layout, saved, xhat, ws, ws_bytes, stream);
+    case 2: return cgbn_xhat_a2(x, N, C, HW, layout, saved, xhat, ws, ws_bytes, stream);
+    default: return cgbn_xhat_a0(x, N, C, HW, layout, saved, xhat, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_channel_affine_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* scale, const double* shift, void* out, void* stream);
+int cgbn_channel_affine_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* scale, const double* shift, void* out, void* stream);
+int cgbn_channel_affine(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* scale, const double* shift, void* out, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_channel_affine_a1(x, N, C, HW, layout, scale, shift, out, stream);
+    case 2: return cgbn_channel_affine_a2(x, N, C, HW, layout, scale, shift, out, stream);
+    default: return cgbn_channel_affine_a0(x, N, C, HW, layout, scale, shift, out, stream);
+  }
+}
+
+int cgbn_bwd_reduce_a1(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, int relu, double* partial, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_reduce_a2(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, int relu, double* partial, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_reduce(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, int relu, double* partial, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_bwd_reduce_a1(dy, x, N, C, HW, layout, saved, gamma, beta, relu, partial, ws, ws_bytes, stream);
+    case 2: return cgbn_bwd_reduce_a2(dy, x, N, C, HW, layout, saved, gamma, beta, relu, partial, ws, ws_bytes, stream);
+    default: return cgbn_bwd_reduce_a0(dy, x, N, C, HW, layout, saved, gamma, beta, relu, partial, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_bwd_dx_a1(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* const* partials, int G, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_dx_a2(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* const* partials, int G, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_dx(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* const* partials, int G, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_bwd_dx_a1(dy, x, N, C, HW, layout, partials, G, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    case 2: return cgbn_bwd_dx_a2(dy, x, N, C, HW, layout, partials, G, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    default: return cgbn_bwd_dx_a0(dy, x, N, C, HW, layout, partials, G, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_bwd_local_a1(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_local_a2(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_local(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_bwd_local_a1(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    case 2: return cgbn_bwd_local_a2(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    default: return cgbn_bwd_local_a0(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fused_supported_a1(int64_t N, int64_t C, int64_t HW, int layout, int backward);
+int cgbn_fused_supported_a2(int64_t N, int64_t C, int64_t HW, int layout, int backward);
+int cgbn_fused_supported(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fused_supported_a1(N, C, HW, layout, backward);
+    case 2: return cgbn_fused_supported_a2(N, C, HW, layout, backward);
+    default: return cgbn_fused_supported_a0(N, C, HW, layout, backward);
+  }
+}
+
+int cgbn_fwd_fused_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_fused_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_fused(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_fused_a1(x, N, C, HW, layout, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_fused_a2(x, N, C, HW, layout, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    default: return cgbn_fwd_fused_a0(x, N, C, HW, layout, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_bwd_fused_a1(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_fused_a2(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_bwd_fused_a1(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    case 2: return cgbn_bwd_fused_a2(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    default: return cgbn_bwd_fused_a0(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_stats_p2p_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank, int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_stats_p2p_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank, int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_stats_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout, int rank, int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_stats_p2p_a1(x, N, C, HW, layout, rank, G, regions, max_len, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_stats_p2p_a2(x, N, C, HW, layout, rank, G, regions, max_len, ws, ws_bytes, stream);
+    default: return cgbn_fwd_stats_p2p_a0(x, N, C, HW, layout, rank, G, regions, max_len, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_normalize_p2p_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, void* region, int G, int64_t max_len, double timeout_s, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_p2p_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, void* region, int G, int64_t max_len, double timeout_s, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_p2p(const void* x, int64_t N, int64_t C, int64_t HW, int layout, void* region, int G, int64_t max_len, double timeout_s, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_normalize_p2p_a1(x, N, C, HW, layout, region, G, max_len, timeout_s, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_normalize_p2p_a2(x, N, C, HW, layout, region, G, max_len, timeout_s, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    default: return cgbn_fwd_normalize_p2p_a0(x, N, C, HW, layout, region, G, max_len, timeout_s, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_bwd_reduce_p2p_a1(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, int relu, int rank, int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_reduce_p2p_a2(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, int relu, int rank, int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_reduce_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, const double* saved, const float* gamma, const float* beta, int relu, int rank, int G, void* const* regions, int64_t max_len, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_bwd_reduce_p2p_a1(dy, x, N, C, HW, layout, saved, gamma, beta, relu, rank, G, regions, max_len, ws, ws_bytes, stream);
+    case 2: return cgbn_bwd_reduce_p2p_a2(dy, x, N, C, HW, layout, saved, gamma, beta, relu, rank, G, regions, max_len, ws, ws_bytes, stream);
+    default: return cgbn_bwd_reduce_p2p_a0(dy, x, N, C, HW, layout, saved, gamma, beta, relu, rank, G, regions, max_len, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_bwd_dx_p2p_a1(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, void* region, int G, int64_t max_len, double timeout_s, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_dx_p2p_a2(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, void* region, int G, int64_t max_len, double timeout_s, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_bwd_dx_p2p(const void* dy, const void* x, int64_t N, int64_t C, int64_t HW, int layout, void* region, int G, int64_t max_len, double timeout_s, const double* saved, const float* gamma, const float* beta, double eps, int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_bwd_dx_p2p_a1(dy, x, N, C, HW, layout, region, G, max_len, timeout_s, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    case 2: return cgbn_bwd_dx_p2p_a2(dy, x, N, C, HW, layout, region, G, max_len, timeout_s, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+    default: return cgbn_bwd_dx_p2p_a0(dy, x, N, C, HW, layout, region, G, max_len, timeout_s, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_fwd_normalize_slots_a1(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const void* slot_ws, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_slots_a2(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const void* slot_ws, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream);
+int cgbn_fwd_normalize_slots(const void* x, int64_t N, int64_t C, int64_t HW, int layout, const void* slot_ws, const float* gamma, const float* beta, double eps, double momentum, float* running_mean, float* running_var, double* saved, int relu, void* y, unsigned* status, void* ws, size_t ws_bytes, void* stream) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_fwd_normalize_slots_a1(x, N, C, HW, layout, slot_ws, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    case 2: return cgbn_fwd_normalize_slots_a2(x, N, C, HW, layout, slot_ws, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+    default: return cgbn_fwd_normalize_slots_a0(x, N, C, HW, layout, slot_ws, gamma, beta, eps, momentum, running_mean, running_var, saved, relu, y, status, ws, ws_bytes, stream);
+  }
+}
+
+#endif  // CGBN_TU_ACT == 0
 
 }  // extern "C"

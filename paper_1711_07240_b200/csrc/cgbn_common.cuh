@@ -3,21 +3,21 @@
 
 #pragma once
 
+// The thread-local message behind cgbn_last_error() (defined once, in unit 0 of cgbn.cu).
+int cgbn_internal_set_error(int code, const char* msg);
+
 namespace {
 
 // ----------------------------------------------------------------------------------
 // Errors
 
-thread_local std::string g_last_error;
-
-int set_error(int code, const char* fmt, ...) {
+static int set_error(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(buf, sizeof(buf), fmt, ap);
   va_end(ap);
-  g_last_error = buf;
-  return code;
+  return cgbn_internal_set_error(code, buf);
 }
 
 int check_launch(const char* what) {
@@ -166,6 +166,7 @@ struct Parts {
 // through CUDA IPC:
 //   [ epoch counter (u64) | flags[G] (u64) | done (u32, padded) | recv[2][G][max_len] (f64) ]
 // `done` counts the channel finishers of a fused reduction; the last one publishes.
+namespace {
 namespace p2p {
 
 __host__ __device__ inline size_t flags_off() { return 8; }
@@ -248,7 +249,13 @@ struct Pull {
 };
 
 // Called by every thread of a block; returns the epoch. Threads q < G spin on flag q.
-__device__ __forceinline__ unsigned long long pull_wait(const Pull& P) {
+// `timed_out` tells every thread that some rank never published: its rows still hold an
+// older exchange, so the caller must not use them (collectives.py:138-144 raises before
+// any state changes).
+__device__ __forceinline__ unsigned long long pull_wait(const Pull& P, bool& timed_out) {
+  __shared__ int s_timeout;
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(P.own);
   if ((int)threadIdx.x < P.G) {
     const unsigned long long* f = flag_ptr(P.own, threadIdx.x);
@@ -256,16 +263,19 @@ __device__ __forceinline__ unsigned long long pull_wait(const Pull& P) {
     while (ld_acquire_sys(f) < e) {
       if (now_ns() - t0 > P.timeout_ns) {
         if (P.status) atomicOr(P.status, CGBN_STATUS_EXCHANGE_TIMEOUT);
+        s_timeout = 1;
         break;
       }
     }
   }
   __syncthreads();
   __threadfence_system();
+  timed_out = s_timeout != 0;
   return e;
 }
 
 }  // namespace p2p
+}  // namespace
 
 namespace {
 

@@ -671,6 +671,11 @@ size_t conv_smem_bytes() {
   return 1024 + kStages * kStage + kEpiWarps * 2 * kWarpStage + 8 * (2 * kStages + 4) + 16;
 }
 
+bool conv_pdl() {  // CGBN_NO_PDL=1 disables programmatic dependent launch (read once)
+  static const bool on = getenv("CGBN_NO_PDL") == nullptr;
+  return on;
+}
+
 int num_sms() {
   static int sms[64] = {0};
   int dev = 0;
@@ -812,7 +817,7 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = getenv("CGBN_NO_PDL") ? 0 : 1;
+  cfg.numAttrs = conv_pdl() ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmZ, a);
   if (e != cudaSuccess) return fail(CGBN_ERR_CUDA, "conv launch failed: %s", cudaGetErrorString(e));
   return CGBN_OK;
@@ -874,7 +879,7 @@ int run_conv(const char* what, const void* x, const void* w, const float* bias, 
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = getenv("CGBN_NO_PDL") ? 0 : 1;
+  cfg.numAttrs = conv_pdl() ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_conv_fold, (const Slot*)slots, (int)g.Cout, g.mtiles,
                                      conv_grid(g), conv_nslots(g), partial);
   if (e != cudaSuccess) return fail(CGBN_ERR_CUDA, "conv fold launch failed: %s", cudaGetErrorString(e));

@@ -34,9 +34,13 @@ __global__ void k_finalize_bwd(Parts parts, BwdFinal F) {
 
 // The same after a fused exchange: every block waits for the group's flags of the current
 // epoch in its own region, then folds the G rows (ascending rank order) read there.
+// A timed-out exchange yields NaN statistics: the finisher then flags the channel
+// non-finite and leaves the running statistics alone, and y / dx come out NaN, instead of
+// silently using a missing rank's rows from an older exchange.
 __global__ void k_finalize_fwd_p2p(p2p::Pull pull, FwdFinal F) {
   pdl_wait();
-  const unsigned long long e = p2p::pull_wait(pull);
+  bool timed_out;
+  const unsigned long long e = p2p::pull_wait(pull, timed_out);
   pdl_trigger();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= F.C) return;
@@ -46,12 +50,14 @@ __global__ void k_finalize_fwd_p2p(p2p::Pull pull, FwdFinal F) {
     parts.p[r] = p2p::recv_ptr(pull.own, pull.G, pull.max_len, (int)(e & 1ull), r);
   double n, mean, M2, P, Q;
   merge_fwd_partials(parts, c, F.C, n, mean, M2);
+  if (timed_out) n = mean = M2 = __longlong_as_double(0x7ff8000000000000ll);
   finalize_fwd_channel(F, c, n, mean, M2, true, P, Q);
 }
 
 __global__ void k_finalize_bwd_p2p(p2p::Pull pull, BwdFinal F) {
   pdl_wait();
-  const unsigned long long e = p2p::pull_wait(pull);
+  bool timed_out;
+  const unsigned long long e = p2p::pull_wait(pull, timed_out);
   pdl_trigger();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= F.C) return;
@@ -64,6 +70,7 @@ __global__ void k_finalize_bwd_p2p(p2p::Pull pull, BwdFinal F) {
     sdy += rr[c];
     sdyx += rr[C + c];
   }
+  if (timed_out) sdy = sdyx = __longlong_as_double(0x7ff8000000000000ll);
   finalize_bwd_channel(F, c, sdy, sdyx, true);
 }
 

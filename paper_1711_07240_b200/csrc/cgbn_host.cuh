@@ -23,12 +23,36 @@ int num_sms_cached() {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// A/B switches and debug knobs, read once per process, never per launch.
+struct Env {
+  bool no_rows, no_masked, no_ct, no_pdl, ew_forward, ew_persistent, debug_plan;
+  int rows_cs4 = 0;           // CGBN_ROWS_CS4
+  int ct_tl = 0, ct_kc = 0;   // CGBN_CT_FORCE=tl,kc
+  Env() {
+    no_rows = getenv("CGBN_NO_ROWS") != nullptr;
+    no_masked = getenv("CGBN_NO_MASKED") != nullptr;
+    no_ct = getenv("CGBN_NO_CT") != nullptr;
+    no_pdl = getenv("CGBN_NO_PDL") != nullptr;
+    ew_forward = getenv("CGBN_EW_FORWARD") != nullptr;
+    ew_persistent = getenv("CGBN_EW_PERSISTENT") != nullptr;
+    debug_plan = getenv("CGBN_DEBUG_PLAN") != nullptr;
+    if (const char* e = getenv("CGBN_ROWS_CS4")) rows_cs4 = atoi(e);
+    if (const char* f = getenv("CGBN_CT_FORCE")) {
+      if (sscanf(f, "%d,%d", &ct_tl, &ct_kc) != 2) ct_tl = ct_kc = 0;
+    }
+  }
+};
+const Env& env() {
+  static const Env e;
+  return e;
+}
+
 // Workspace: tickets + barrier words | (C + max grid) double2 per-CTA partial slots |
 // coefficient table (5 x C doubles: P, Q, A, B, Cc).
 // Row reductions (NHWC / 2-D, C % 4 == 0): rows per block >= 32 keeps the partial
 // slots (nb * C double2) under 1/8 of the activation bytes.
 bool rows_layout(int64_t C, int64_t HW, int layout) {
-  return (layout == CGBN_LAYOUT_NHWC || HW == 1) && C % 4 == 0 && !getenv("CGBN_NO_ROWS");
+  return (layout == CGBN_LAYOUT_NHWC || HW == 1) && C % 4 == 0 && !env().no_rows;
 }
 
 NGeom rows_geom(int64_t N, int64_t C, int64_t HW, int64_t ctas) {
@@ -43,10 +67,8 @@ NGeom rows_geom(int64_t N, int64_t C, int64_t HW, int64_t ctas) {
   // channels (CS4 = 64) above that; full-width 1024-channel slices were 10-70% slower
   // on C >= 512 (e.g. [32,2048,7,7] stats 10.1 -> 7.4 us, bwd reduce 14.6 -> 9.2 us).
   uint32_t cs_max = (g.C4 > 64 && g.M >= 256) ? 64u : 32u;
-  if (const char* e = getenv("CGBN_ROWS_CS4")) {  // A/B
-    const int v = atoi(e);
-    if (v == 32 || v == 64 || v == 128 || v == 256) cs_max = (uint32_t)v;
-  }
+  const int v = env().rows_cs4;  // A/B
+  if (v == 32 || v == 64 || v == 128 || v == 256) cs_max = (uint32_t)v;
   g.CS4 = g.C4 < cs_max ? g.C4 : cs_max;
   g.rpp = (uint32_t)kThreads / g.CS4;
   g.nslices = (g.C4 + g.CS4 - 1) / g.CS4;
@@ -144,17 +166,6 @@ void smem_optin(K kernel, size_t smem_bytes) {
   g_smem_done[key] = true;
 }
 
-// CGBN_PATH=tma selects the TMA streaming statistics reductions (A/B measurement);
-// CGBN_PATH=reg disables every TMA / cp.async variant.
-int path_override() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CGBN_PATH");
-    v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : 0;
-  }
-  return v;
-}
-
 // The ABI's `layout` argument carries the activation dtype in bits 4..7
 // (CGBN_ACT_F32 / CGBN_ACT_BF16 / CGBN_ACT_F16, include/cgbn.h).
 int split_fmt(int* layout, int* act) {
@@ -190,9 +201,7 @@ struct Plan {
   bool rows;  // NHWC / 2-D with C % 4 == 0: row reduction (k_reduce_rows + k_fold_rows)
   bool team;
   bool ct;   // NCHW: cluster-team reduction (k_reduce_ct) when it fills the GPU
-  bool tma;  // NCHW, HW % 4 == 0, 16-byte aligned, CGBN_PATH=tma
   Geom g;
-  tma::TGeom tg;
   int64_t elems;
 };
 
@@ -214,7 +223,7 @@ int make_plan(int64_t N, int64_t C, int64_t HW, int layout, int act, const void*
   else if (es == 2 && planeHW % 4 == 0 && (align % 8) == 0)
     vec = 4;  // exact 8-byte units: faster than masked 16-byte covers (bf16 14x14 stats 4.4 -> 3.3 us)
   else if (layout == CGBN_LAYOUT_NCHW && HW >= 16 && (align % 16) == 0 && E % vmax == 0 &&
-           E + 2 * vmax < (1ll << 32) && !getenv("CGBN_NO_MASKED"))
+           E + 2 * vmax < (1ll << 32) && !env().no_masked)
     vec = es == 4 ? 5 : 9;  // masked 16-byte cover of odd planes (never leaves the tensor)
   else if (es == 2 && planeHW % 4 == 0 && (align % 8) == 0) vec = 4;
   else if (planeHW % 2 == 0 && (align % (2 * es)) == 0) vec = 2;
@@ -236,22 +245,10 @@ int make_plan(int64_t N, int64_t C, int64_t HW, int layout, int act, const void*
   out->act = act;
   out->vec = vec;
   out->team = g.Lv <= kTeamMaxLv;
-  out->ct = layout == CGBN_LAYOUT_NCHW && !getenv("CGBN_NO_CT");
+  out->ct = layout == CGBN_LAYOUT_NCHW && !env().no_ct;
   out->rows = rows_layout(C, HW, layout) && (align % 16) == 0;
   out->g = g;
   out->elems = N * C * HW;
-  out->tma = act == 0 && layout == CGBN_LAYOUT_NCHW && HW % 4 == 0 && (align % 16) == 0 &&
-             path_override() == 1;
-  tma::TGeom& tg = out->tg;
-  tg.C = (uint32_t)C;
-  tg.HW = (uint32_t)HW;
-  tg.L = (uint32_t)(N * HW);
-  tg.T4 = (uint64_t)C * tg.L / 4;
-  tg.dhw.init((uint32_t)HW);
-  tg.count = (double)(N * HW);
-  int64_t tgrid = ceil_div((int64_t)tg.T4, 1024);
-  if (tgrid > num_sms_cached()) tgrid = num_sms_cached();
-  tg.grid = (uint32_t)(tgrid < 1 ? 1 : tgrid);
   return CGBN_OK;
 }
 
@@ -286,11 +283,7 @@ unsigned team_grid(K kernel, const Plan& pl) {
 }
 
 // Launch with programmatic dependent launch allowed (see pdl_trigger / pdl_wait).
-bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) v = getenv("CGBN_NO_PDL") ? 0 : 1;
-  return v == 1;
-}
+bool pdl_enabled() { return !env().no_pdl; }
 
 template <class K, class... Args>
 void launch_pdl(K kernel, unsigned grid, bool pdl, cudaStream_t st, Args... args) {
@@ -404,16 +397,16 @@ again:
     latency_bound = false;  // no single-round configuration: rank by fill instead
     goto again;
   }
-  if (const char* f = getenv("CGBN_CT_FORCE")) {  // "tl,kc" (experiments only)
-    int tl = 0, kc = 0;
-    if (sscanf(f, "%d,%d", &tl, &kc) == 2 && tl >= 5 && tl <= 8 && kc >= 1 && kc <= 8) {
+  {  // CGBN_CT_FORCE=tl,kc (experiments only)
+    const int tl = env().ct_tl, kc = env().ct_kc;
+    if (tl >= 5 && tl <= 8 && kc >= 1 && kc <= 8) {
       cfg->tl = tl;
       cfg->kc = (uint32_t)kc;
       cfg->grid = (uint32_t)(ceil_div(C, (int64_t)kThreads >> tl) * kc);
       best_n = cfg->grid;
     }
   }
-  if (getenv("CGBN_DEBUG_PLAN"))
+  if (env().debug_plan)
     fprintf(stderr, "[cgbn] ct C=%lld Lv=%lld in=%d slots=%lld %s -> tl=%d kc=%u grid=%lld\n",
             (long long)C, (long long)Lv, Op::kIn, (long long)slots,
             latency_bound ? "latency" : "bandwidth", best_n ? cfg->tl : -1, best_n ? cfg->kc : 0,
@@ -479,15 +472,6 @@ int launch_reduce(const Plan& pl, const Op& op, double* out, const WsView& w, cu
   return CGBN_OK;
 }
 
-template <class TOp>
-int launch_tma_reduce(const Plan& pl, const TOp& op, double* out, const WsView& w,
-                      cudaStream_t st) {
-  smem_optin(tma::k_tma_reduce<TOp>, tma::kSmemBytes);
-  tma::k_tma_reduce<TOp><<<pl.tg.grid, tma::kThreadsTma, tma::kSmemBytes, st>>>(
-      pl.tg, op, out, w.slots, w.tickets);
-  return CGBN_OK;
-}
-
 // Row reduction (NHWC / 2-D): k_reduce_rows -> k_fold_rows (finisher of `op`).
 template <class NOp, class Op>
 int launch_rows(const Plan& pl, const NOp& nop, const Op& op, double* out, const WsView& w,
@@ -539,14 +523,6 @@ int run_stats(const Plan& pl, const void* xv, bool shift, int mode, double* out,
               const FwdFinal* F, const WsView& w, cudaStream_t st, const double* ksum,
               const double* kcount) {
   const T* x = static_cast<const T*>(xv);
-  if constexpr (std::is_same<T, float>::value && VEC == 4) {
-    if (pl.tma && shift && mode == kPartial && !g_push) {
-      tma::TmaStats op;
-      op.x = x;
-      op.K = 0.0;
-      return launch_tma_reduce(pl, op, out, w, st);
-    }
-  }
   if (g_push && mode == kPartial)
     return run_stats_op<T, VEC, true>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
   return run_stats_op<T, VEC, false>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
@@ -583,18 +559,6 @@ int run_bwd_reduce(const Plan& pl, const void* dyv, const void* xv, const double
                    const BwdFinal* F, const WsView& w, cudaStream_t st) {
   const T* dy = static_cast<const T*>(dyv);
   const T* x = static_cast<const T*>(xv);
-  if constexpr (std::is_same<T, float>::value && VEC == 4) {
-    if (pl.tma && mode == kPartial && !g_push) {
-      tma::TmaBwd<RELU> op;
-      op.dy = dy;
-      op.x = x;
-      op.saved = saved;
-      op.gamma = gamma;
-      op.beta = beta;
-      op.mean = op.P = op.Q = 0.0;
-      return launch_tma_reduce(pl, op, out, w, st);
-    }
-  }
   if (g_push && mode == kPartial)
     return run_bwd_op<T, VEC, RELU, true>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
   return run_bwd_op<T, VEC, RELU, false>(pl, dy, x, saved, gamma, beta, mode, out, F, w, st);
@@ -626,15 +590,8 @@ int dispatch_stats_t(const Plan& pl, const void* x, bool shift, int mode, double
 int dispatch_stats(const Plan& pl, const void* x, bool shift, int mode, double* out,
                    double* out2, const FwdFinal* F, const WsView& w, cudaStream_t st,
                    const double* ksum = nullptr, const double* kcount = nullptr) {
-  switch (pl.act) {
-    case 1:
-      return dispatch_stats_t<__nv_bfloat16>(pl, x, shift, mode, out, out2, F, w, st, ksum,
-                                             kcount);
-    case 2:
-      return dispatch_stats_t<__half>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
-    default:
-      return dispatch_stats_t<float>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
-  }
+  CGBN_ROUTED(pl.act);
+  return dispatch_stats_t<TuAct>(pl, x, shift, mode, out, out2, F, w, st, ksum, kcount);
 }
 
 template <class T, bool RELU>
@@ -672,15 +629,8 @@ int dispatch_bwd_r(const Plan& pl, const void* dy, const void* x, const double* 
 int dispatch_bwd_reduce(const Plan& pl, const void* dy, const void* x, const double* saved,
                         const float* gamma, const float* beta, bool relu, int mode, double* out,
                         const BwdFinal* F, const WsView& w, cudaStream_t st) {
-  switch (pl.act) {
-    case 1:
-      return dispatch_bwd_r<__nv_bfloat16>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w,
-                                           st);
-    case 2:
-      return dispatch_bwd_r<__half>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w, st);
-    default:
-      return dispatch_bwd_r<float>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w, st);
-  }
+  CGBN_ROUTED(pl.act);
+  return dispatch_bwd_r<TuAct>(pl, dy, x, saved, gamma, beta, relu, mode, out, F, w, st);
 }
 
 // ---- elementwise
@@ -711,7 +661,7 @@ int make_ew(int64_t N, int64_t C, int64_t HW, int layout, int act, const void* c
   // Sweep from the end of the tensor: the preceding channel-major reduction read the
   // high-n planes of every channel last, so they are the likeliest L2 hits (measured
   // +1.5% on the ResNet-50 step, up to 7% on the 100 MB layers; CGBN_EW_FORWARD=1 off).
-  g.rev = getenv("CGBN_EW_FORWARD") ? 0u : 1u;
+  g.rev = env().ew_forward ? 0u : 1u;
   g.reuse = 0;
   // channel modes work on 4-element chunks of a unit: CM 0 / 3 need HW % 4 / C % 4 only
   (void)UE;
@@ -751,8 +701,7 @@ constexpr int ew_units() {
 template <class K>
 unsigned ew_grid(K kernel, const EwPlan& ep, int units = kEwU) {
   int64_t grid = ceil_div((int64_t)ep.g.n4 + 1, kThreads * units);
-  static const bool persistent = getenv("CGBN_EW_PERSISTENT") != nullptr;
-  if (persistent) {
+  if (env().ew_persistent) {
     const int64_t res = resident_ctas(kernel);
     if (grid > res) grid = res;
   }
@@ -814,9 +763,7 @@ void launch_ew_affine(const EwPlan& ep, bool relu, const void* x, void* y, const
                       const double* Q, cudaStream_t st, bool pdl = true) {
   int cm = ep.cm;
   if (cm == 3 && (((uintptr_t)P | (uintptr_t)Q) % 16) != 0) cm = 2;  // caller's tables
-  if (ep.act == 1) launch_ew_affine_d<__nv_bfloat16>(ep, cm, relu, x, y, P, Q, pdl, st);
-  else if (ep.act == 2) launch_ew_affine_d<__half>(ep, cm, relu, x, y, P, Q, pdl, st);
-  else launch_ew_affine_d<float>(ep, cm, relu, x, y, P, Q, pdl, st);
+  launch_ew_affine_d<TuAct>(ep, cm, relu, x, y, P, Q, pdl, st);
 }
 
 template <class T, bool RELU, int CM>
@@ -849,9 +796,7 @@ void launch_ew_dx_d(const EwPlan& ep, bool relu, const void* dy, const void* x, 
 
 void launch_ew_dx(const EwPlan& ep, bool relu, const void* dy, const void* x, void* dx,
                   const WsView& w, cudaStream_t st) {
-  if (ep.act == 1) launch_ew_dx_d<__nv_bfloat16>(ep, relu, dy, x, dx, w, st);
-  else if (ep.act == 2) launch_ew_dx_d<__half>(ep, relu, dy, x, dx, w, st);
-  else launch_ew_dx_d<float>(ep, relu, dy, x, dx, w, st);
+  launch_ew_dx_d<TuAct>(ep, relu, dy, x, dx, w, st);
 }
 
 unsigned chan_blocks(int64_t C) { return (unsigned)ceil_div(C, 256); }
@@ -884,67 +829,256 @@ BwdFinal make_bwd_final(int64_t C, const double* saved, const float* gamma, cons
   return F;
 }
 
-// ---- fused cooperative kernels (cgbn_fused.cuh)
+// ---- single-launch on-chip passes (cgbn_onchip.cuh), single-rank groups
 
-bool fused_plan(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align, int nin,
-                fused::FGeom* fg) {
-  if (path_override() == 2 || getenv("CGBN_NO_FUSED")) return false;
-  if (layout != CGBN_LAYOUT_NCHW || HW % 4 != 0 || (align % 16) != 0) return false;
+// CGBN_NO_ONCHIP=1: always the split path (A/B). CGBN_ONCHIP_MAX_MB: largest activation
+// footprint (x, or dy + x, in MB) sent on chip; default from the B200 sweep.
+struct OnchipEnv {
+  bool enabled = true;
+  double max_frac = 0.80;  // of the GPU's total shared memory
+  int force_kc = 0, force_nch = 0;
+  OnchipEnv() {
+    enabled = getenv("CGBN_NO_ONCHIP") == nullptr;
+    if (const char* e = getenv("CGBN_ONCHIP_MAX_FRAC")) max_frac = atof(e);
+    if (const char* e = getenv("CGBN_ONCHIP_FORCE")) sscanf(e, "%d,%d", &force_nch, &force_kc);
+  }
+};
+const OnchipEnv& onchip_env() {
+  static const OnchipEnv env;
+  return env;
+}
+
+struct OnchipPlan {
+  onchip::OGeom g;
+  unsigned grid;
+  size_t smem;
+  int ve;
+};
+
+int device_attr(cudaDeviceAttr a, int fallback) {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, a, dev) != cudaSuccess || v <= 0) return fallback;
+  return v;
+}
+
+// Resident CTAs per SM of `kernel` at `smem` dynamic bytes (cached).
+std::map<std::tuple<const void*, int, size_t>, int> g_occ_smem;
+template <class K>
+int occupancy_smem(K kernel, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_occ_smem.find(key);
+    if (it != g_occ_smem.end()) return it->second;
+  }
+  smem_optin(kernel, (size_t)device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448));
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, onchip::kThreadsO, smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    occ = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_occ_smem[key] = occ;
+  return occ;
+}
+
+// Clusters of `kc` CTAs co-resident at `smem` dynamic bytes (cached).
+std::map<std::tuple<const void*, int, int, size_t>, int> g_cluster_smem;
+template <class K>
+int64_t cluster_capacity_smem(K kernel, uint32_t kc, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, (int)kc, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cluster_smem.find(key);
+    if (it != g_cluster_smem.end()) return it->second;
+  }
+  smem_optin(kernel, (size_t)device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kc * 64);
+  cfg.blockDim = dim3(onchip::kThreadsO);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cluster_smem[key] = n;
+  return n;
+}
+
+template <class T, bool BWD, bool RELU>
+auto onchip_kernel(int ve) {
+  switch (ve) {
+    case 8: return onchip::k_onchip<T, (sizeof(T) == 2 ? 8 : 4), BWD, RELU>;  // 16-bit only
+    case 4: return onchip::k_onchip<T, 4, BWD, RELU>;
+    case 2: return onchip::k_onchip<T, 2, BWD, RELU>;
+    default: return onchip::k_onchip<T, 1, BWD, RELU>;
+  }
+}
+
+// Choose (nch, KC): every CTA resident in one wave, the least bytes on the busiest SM.
+template <class T, bool BWD, bool RELU>
+bool onchip_plan_t(int64_t N, int64_t C, int64_t HW, OnchipPlan* p) {
+  constexpr int es = (int)sizeof(T);
+  constexpr int nin = BWD ? 2 : 1;
+  const OnchipEnv& env = onchip_env();
+  // unit width: a full 16-byte chunk when planes are whole chunks (every run 16-byte
+  // aligned: the fast path), else the widest width dividing HW
+  constexpr int ue = 16 / es;
+  int ve = ue;
+  while (ve > 1 && HW % ve) ve /= 2;
+  auto kernel = onchip_kernel<T, BWD, RELU>(ve);
+  const int64_t S = num_sms_cached();
+  const int64_t smem_sm = device_attr(cudaDevAttrMaxSharedMemoryPerMultiprocessor, 233472);
+  const int64_t smem_blk = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448);
+  const int64_t total = (int64_t)nin * N * C * HW * es;
+  if ((double)total > env.max_frac * (double)(S * smem_sm)) return false;
+  const size_t head = ((sizeof(onchip::Head) + 15) / 16) * 16;
+  double best = 1e300;
+  bool found = false;
+  for (int64_t kc = 1; kc <= 8 && kc <= N; kc *= 2) {
+    if (env.force_kc && kc != env.force_kc) continue;
+    const int64_t nk = ceil_div(N, kc);
+    if (nk > onchip::kMaxImg) continue;
+    for (int64_t nch = 1; nch <= 1024; nch *= 2) {
+      if (env.force_nch && nch != env.force_nch) continue;
+      if (nch > 1 && (nch / 2) >= C) break;
+      const int64_t run = nch * HW * es;
+      const int64_t stride = (run + 15) / 16 * 16 + 16;
+      const size_t smem = head + (onchip::chan_bytes<BWD>((uint32_t)nch) + 15) / 16 * 16 +
+                          (size_t)(nk * nin * stride);
+      if ((int64_t)smem > smem_blk) continue;
+      const int64_t clusters = ceil_div(C, nch);
+      const int64_t ctas = clusters * kc;
+      const int cps = occupancy_smem(kernel, smem);
+      if (cps < 1 || ctas > S * cps) continue;
+      if (kc > 1 && clusters > cluster_capacity_smem(kernel, (uint32_t)kc, smem)) continue;
+      // busiest SM: m = ceil(ctas / S) CTAs of nk * nin * run bytes. A lone CTA cannot
+      // overlap its copy-in, reduction and write phases; m CTAs overlap each other's
+      // (factor 1 + 1/m). A cluster level costs ~one barrier round trip (~0.5 us ~ 20 KB
+      // at the per-SM HBM share).
+      const double m = (double)ceil_div(ctas, S);
+      const double score = m * (double)(nk * nin * run) * (1.0 + 1.0 / m) +
+                           20e3 * (kc > 1 ? __builtin_ctzll(kc) : 0) + 64.0 * ctas;
+      if (score < best) {
+        best = score;
+        found = true;
+        onchip::OGeom& g = p->g;
+        g.N = (uint32_t)N;
+        g.C = (uint32_t)C;
+        g.HW = (uint32_t)HW;
+        g.nch = (uint32_t)nch;
+        g.KC = (uint32_t)kc;
+        g.run_stride = (uint32_t)stride;
+        // aligned: the exact chunks of a run; else the slots of its 16-byte cover
+        g.nq = (uint32_t)(ve == ue ? run / 16 : stride / 16);
+        const int64_t wpc = nch >= onchip::kWarpsO ? 1 : onchip::kWarpsO / nch;
+        g.wpc_log2 = (uint32_t)__builtin_ctzll(wpc);
+        g.HWv = (uint32_t)(HW / ve);
+        g.HWu = (uint32_t)(ve == ue ? HW / ue : 1);
+        g.dhwv.init(g.HWv);
+        g.dhw.init((uint32_t)HW);
+        g.dhwu.init(g.HWu);
+        g.dnq.init(g.nq);
+        g.count = (double)(N * HW);
+        p->grid = (unsigned)ctas;
+        p->smem = smem;
+        p->ve = ve;
+      }
+    }
+  }
+  return found;
+}
+
+// On-chip eligibility: NCHW planes of >= 4 elements, 16-byte aligned pointers and tensor
+// size, the footprint within max_frac of the GPU's shared memory, one resident wave.
+template <class T, bool BWD, bool RELU>
+bool onchip_plan(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align,
+                 OnchipPlan* p) {
+  if (!onchip_env().enabled || layout != CGBN_LAYOUT_NCHW || HW < 4) return false;
+  if (align % 16 || ((uint64_t)N * C * HW * sizeof(T)) % 16) return false;
   if (validate_shape(N, C, HW, layout) != CGBN_OK) return false;
-  const int64_t L = N * HW;
-  const int64_t T4 = C * L / 4;
-  int64_t grid = ceil_div(T4, 64);
-  if (grid > num_sms_cached()) grid = num_sms_cached();
-  if (grid < 1) grid = 1;
-  const int64_t max_slice = ceil_div(T4, grid) * 4;
-  const int64_t cap = (int64_t)(fused::kDataBytes / (4 * nin));
-  if (max_slice > cap) return false;
-  if (max_slice / L + 2 > fused::kMaxSeg) return false;
-  fg->C = (uint32_t)C;
-  fg->HW = (uint32_t)HW;
-  fg->L = (uint32_t)L;
-  fg->grid = (uint32_t)grid;
-  fg->T4 = (uint64_t)T4;
-  fg->dhw.init((uint32_t)HW);
-  fg->count = (double)L;
+  if (!onchip_plan_t<T, BWD, RELU>(N, C, HW, p)) return false;
+  if (env().debug_plan)
+    fprintf(stderr, "[cgbn] onchip %s N=%lld C=%lld HW=%lld -> nch=%u kc=%u grid=%u smem=%zu ve=%d\n",
+            BWD ? "bwd" : "fwd", (long long)N, (long long)C, (long long)HW, p->g.nch, p->g.KC,
+            p->grid, p->smem, p->ve);
   return true;
 }
 
-// Cooperative grids must never interleave on one device (their grid barriers could
-// deadlock): launches from different streams of one process are chained through a
-// per-device event. Skipped under stream capture, where a graph replays in order.
-std::mutex g_coop_mu;
-cudaEvent_t g_coop_last[64] = {nullptr};
+// Debug: per-CTA phase timestamps of the on-chip launches (cgbn_debug_onchip_trace).
+unsigned long long* g_onchip_trace = nullptr;
 
-template <class K, class... Args>
-int launch_cooperative(K kernel, unsigned grid, size_t smem, cudaStream_t st, Args... args) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(st, &cap);
-  const bool chain = cap == cudaStreamCaptureStatusNone && dev >= 0 && dev < 64;
-  std::unique_lock<std::mutex> lk(g_coop_mu, std::defer_lock);
-  if (chain) {
-    lk.lock();
-    if (!g_coop_last[dev]) cudaEventCreateWithFlags(&g_coop_last[dev], cudaEventDisableTiming);
-    cudaStreamWaitEvent(st, g_coop_last[dev], 0);
-  }
-  smem_optin(kernel, smem);
+template <class T, bool BWD, bool RELU>
+int launch_onchip(const OnchipPlan& p, const onchip::Args& a0, cudaStream_t st) {
+  auto kernel = onchip_kernel<T, BWD, RELU>(p.ve);
+  onchip::Args a = a0;
+  a.trace = g_onchip_trace;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(fused::kThreadsF);
-  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(onchip::kThreadsO);
+  cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
-  if (chain) cudaEventRecord(g_coop_last[dev], st);
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (p.g.KC > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = p.g.KC;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, p.g, a);
   if (e != cudaSuccess)
-    return set_error(CGBN_ERR_CUDA, "cooperative launch failed: %s", cudaGetErrorString(e));
+    return set_error(CGBN_ERR_CUDA, "on-chip launch failed: %s", cudaGetErrorString(e));
   return CGBN_OK;
+}
+
+// Try the on-chip pass; returns 1 if launched, 0 if not eligible, < 0 on error.
+template <class T, bool BWD, bool RELU>
+int try_onchip_t(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align,
+                 const onchip::Args& a, cudaStream_t st) {
+  OnchipPlan p;
+  if (!onchip_plan<T, BWD, RELU>(N, C, HW, layout, align, &p)) return 0;
+  const int rc = launch_onchip<T, BWD, RELU>(p, a, st);
+  return rc == CGBN_OK ? 1 : -rc;
+}
+
+template <bool BWD>
+int try_onchip(int act, bool relu, int64_t N, int64_t C, int64_t HW, int layout,
+               uintptr_t align, const onchip::Args& a, cudaStream_t st) {
+  CGBN_ROUTED(act);
+  return relu ? try_onchip_t<TuAct, BWD, true>(N, C, HW, layout, align, a, st)
+              : try_onchip_t<TuAct, BWD, false>(N, C, HW, layout, align, a, st);
+}
+
+template <bool BWD>
+bool onchip_supported(int act, bool relu, int64_t N, int64_t C, int64_t HW, int layout) {
+  if (act != CGBN_TU_ACT) return false;
+  OnchipPlan p;
+  return relu ? onchip_plan<TuAct, BWD, true>(N, C, HW, layout, 0, &p)
+              : onchip_plan<TuAct, BWD, false>(N, C, HW, layout, 0, &p);
 }
 
 #define CGBN_REQUIRE(cond, ...) \

@@ -1,0 +1,507 @@
+// cgbn_onchip.cuh — single-launch, on-chip BN passes for a single-rank group (sm_100a).
+// Part of the single translation unit cgbn.cu (included there, in order).
+//
+// One BN direction is a per-channel reduction followed by an elementwise pass over the
+// same data. When a layer's activations fit in the GPU's shared memory, both run in ONE
+// kernel and the data crosses HBM once:
+//
+//   forward  (batchnorm.py:115-144): read x (4 B/elem) + write y (4)           = 8  B/elem
+//   backward (batchnorm.py:188-210): read dy, x (8) + write dx (4)              = 12 B/elem
+//
+// instead of the split path's 12 and 20 (the elementwise pass re-reads x / dy). There is
+// no grid-wide synchronisation: a thread-block cluster of KC CTAs owns `nch` whole
+// channels, so a channel's statistics never leave the cluster.
+//
+// Decomposition (NCHW). Cluster q owns channels [q*nch, q*nch + nch); CTA rank r of the
+// cluster owns images [n0_r, n1_r) of them (a balanced split of N). For image n those
+// nch planes are ONE contiguous run of nch*HW elements at ((n*C + c0)*HW), so a CTA's
+// data is (n1_r - n0_r) runs:
+//   1. one warp issues a 1-D bulk copy (cp.async.bulk, mbarrier complete_tx) of every
+//      run's 16-byte-aligned cover into shared memory -- the CTA's whole slice is in
+//      flight at once, independent of registers;
+//   2. a team of warps per channel reduces the channel's planes out of shared memory
+//      (fp64 per element: forward d = x - K with the rank's first element K, backward
+//      g and g*(x - mean) with the recomputed ReLU mask), waiting on each run's
+//      mbarrier as it reaches it, so the reduction overlaps the copies still in flight;
+//   3. warp partials -> one CTA partial per channel in shared memory; cluster barrier;
+//      every CTA folds the KC CTA partials of each of its channels over DSMEM in rank
+//      order (the same order everywhere, so every CTA derives bitwise-identical
+//      coefficients) and runs the channel finisher of the split path
+//      (finalize_fwd_channel / finalize_bwd_channel: running statistics, saved
+//      statistics, dgamma / dbeta, written by CTA rank c % KC only);
+//   4. the elementwise pass reads x (dy) from shared memory and writes y (dx) in memory
+//      order over each run with 16-byte stores (scalar at run edges).
+// The closing cluster barrier is split (arrive after the DSMEM reads, wait at exit), so
+// the peers' last reads overlap the write phase.
+//
+// Deterministic (fixed thread -> element mapping and fold orders), no atomics. The
+// host planner (cgbn_host.cuh onchip_plan) picks (nch, KC) so that every CTA is resident
+// in one wave; layers that do not fit take the split kernels.
+#pragma once
+
+namespace {
+namespace bulk {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> this CTA's shared memory (16-byte aligned, multiple of 16 bytes),
+// completing `bytes` of transaction count on `bar`
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace bulk
+}  // namespace
+
+namespace {
+namespace onchip {
+
+constexpr int kThreadsO = 512;
+constexpr int kWarpsO = kThreadsO / 32;
+constexpr int kMaxImg = 64;  // runs (images) per CTA: one mbarrier each
+
+struct OGeom {
+  uint32_t N, C, HW;
+  uint32_t nch;         // channels per cluster
+  uint32_t KC;          // CTAs per cluster (images split over the ranks)
+  uint32_t run_stride;  // shared-memory bytes per run per input (16-aligned, >= cover)
+  uint32_t nq;          // write-phase 16-byte chunks per run (aligned: exact; else cover slots)
+  uint32_t wpc_log2;    // log2(warps per channel team)
+  uint32_t HWv;         // reduction units per plane (HW / VE)
+  uint32_t HWu;         // 16-byte chunks per plane (aligned path)
+  FastDiv dhwv;         // / HWv
+  FastDiv dhw;          // / HW
+  FastDiv dhwu;         // / HWu
+  FastDiv dnq;          // / nq
+  double count;         // N*HW: this rank's elements per channel
+};
+
+// Shared-memory header (before the per-channel arrays and the data runs).
+struct alignas(16) Head {
+  uint64_t bar[kMaxImg];
+  double2 wpart[kWarpsO];
+  uint8_t lead[kMaxImg];  // elements between a run's 16-byte-aligned cover and its start
+};
+
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Per-channel arrays after the header (16-byte aligned each).
+template <bool BWD>
+struct ChanArrays {
+  double2* part;  // this CTA's partial per channel (read by the peers over DSMEM)
+  double* K;      // forward: shift; backward: mean
+  double2* c01;   // forward (P, Q); backward (A, B)
+  double2* c2;    // backward (Cc, -)
+  double2* pq;    // backward ReLU mask (P, Q)
+  typename std::conditional<BWD, BwdChan, FwdChan>::type* pre;  // finisher inputs
+};
+
+template <bool BWD>
+__host__ __device__ inline size_t chan_bytes(uint32_t nch) {
+  using Pre = typename std::conditional<BWD, BwdChan, FwdChan>::type;
+  return (size_t)nch * (16 + 8 + 16 * (BWD ? 3 : 1) + ((sizeof(Pre) + 15) / 16) * 16) + 16;
+}
+
+template <bool BWD>
+__device__ __forceinline__ ChanArrays<BWD> chan_arrays(unsigned char* base, uint32_t nch) {
+  using Pre = typename std::conditional<BWD, BwdChan, FwdChan>::type;
+  ChanArrays<BWD> a;
+  size_t o = 0;
+  a.part = reinterpret_cast<double2*>(base + o);
+  o += (size_t)nch * 16;
+  a.c01 = reinterpret_cast<double2*>(base + o);
+  o += (size_t)nch * 16;
+  a.c2 = reinterpret_cast<double2*>(base + o);
+  a.pq = a.c2 + (BWD ? nch : 0);
+  o += BWD ? (size_t)nch * 32 : 0;
+  a.pre = reinterpret_cast<Pre*>(base + o);
+  o += (size_t)nch * ((sizeof(Pre) + 15) / 16) * 16;
+  a.K = reinterpret_cast<double*>(base + o);
+  return a;
+}
+
+// Vector of VE elements from shared memory (VE * sizeof(T) <= 16 bytes, aligned).
+template <class T, int VE>
+__device__ __forceinline__ void lds_vec(uint32_t addr, float (&v)[VE]) {
+  constexpr int B = VE * (int)sizeof(T);
+  uint32_t w[4];
+  if constexpr (B == 16) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
+  } else if constexpr (B == 8) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
+  } else if constexpr (B == 4) {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(addr));
+  } else {
+    unsigned short h;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(addr));
+    w[0] = h;
+  }
+#pragma unroll
+  for (int k = 0; k < VE; ++k) {
+    if constexpr (sizeof(T) == 4) v[k] = __uint_as_float(w[k]);
+    else v[k] = h2f<T>((unsigned short)(w[k >> 1] >> (16 * (k & 1))));
+  }
+}
+
+struct Args {
+  const void* x;
+  const void* dy;   // backward
+  void* out;        // y or dx
+  FwdFinal F;       // forward finisher (P/Q null: coefficients stay in shared memory)
+  BwdFinal B;       // backward finisher (A..Q null)
+  unsigned long long* trace;  // debug (tools/onchip_trace.py): per-CTA phase timestamps
+};
+
+// Debug phase stamps: globaltimer at phase boundaries of CTA b in trace[b * 8 + s],
+// trace[b * 8 + 7] = the SM id. Off (null) in every production launch.
+__device__ __forceinline__ void stamp(const Args& a, int s) {
+  if (a.trace && threadIdx.x == 0) {
+    a.trace[blockIdx.x * 8 + s] = p2p::now_ns();
+    if (s == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      a.trace[blockIdx.x * 8 + 7] = sm;
+    }
+  }
+}
+
+// Balanced image range of CTA rank r.
+__device__ __forceinline__ void img_range(const OGeom& g, uint32_t r, uint32_t& n0,
+                                          uint32_t& n1) {
+  const uint32_t base = g.N / g.KC, rem = g.N - base * g.KC;
+  n0 = r * base + min(r, rem);
+  n1 = n0 + base + (r < rem ? 1u : 0u);
+}
+
+// Accumulate one VE-element unit: forward (d = x - K): a += d, b += d*d; backward
+// (g = ReLU-masked dy): a += g, b += g*(x - mean).
+template <class T, int VE, bool BWD, bool RELU>
+__device__ __forceinline__ void acc_unit(uint32_t ax, uint32_t ag, double K, double P, double Q,
+                                         double& a, double& b) {
+  float xv[VE];
+  lds_vec<T, VE>(ax, xv);
+  if constexpr (!BWD) {
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      const double d = (double)xv[e] - K;
+      a += d;
+      b = __fma_rn(d, d, b);
+    }
+  } else {
+    float gv[VE];
+    lds_vec<T, VE>(ag, gv);
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      double gk = (double)gv[e];
+      if (RELU && !(bn_out(P, Q, xv[e]) > 0.0)) gk = 0.0;
+      a += gk;
+      b = __fma_rn(gk, (double)xv[e] - K, b);
+    }
+  }
+}
+
+// VE == 16 / sizeof(T): every run is 16-byte aligned and a 16-byte chunk never crosses a
+// plane (HW % VE == 0); otherwise runs carry a lead and the write pass walks channels
+// per element.
+template <class T, int VE, bool BWD, bool RELU>
+__global__ void __launch_bounds__(kThreadsO, 2)
+k_onchip(OGeom g, Args a) {
+  constexpr uint32_t es = sizeof(T);
+  constexpr int UE = 16 / (int)es;  // elements per 16-byte chunk
+  constexpr bool ALIGNED = VE == UE;
+  constexpr uint32_t NIN = BWD ? 2 : 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  Head& H = *reinterpret_cast<Head*>(smem);
+  const uint32_t KC = g.KC;
+  const uint32_t r = KC > 1 ? cluster_rank() : 0u;
+  const uint32_t cbase = (blockIdx.x / KC) * g.nch;
+  const uint32_t nch = min(g.nch, g.C - cbase);  // channels of this cluster
+  uint32_t n0, n1;
+  img_range(g, r, n0, n1);
+  const uint32_t nk = n1 - n0;
+  ChanArrays<BWD> ca = chan_arrays<BWD>(smem + sizeof(Head), g.nch);
+  const uint32_t data =
+      (uint32_t)__cvta_generic_to_shared(smem) +
+      (uint32_t)(((sizeof(Head) + chan_bytes<BWD>(g.nch) + 15) / 16) * 16);
+  const uint32_t kstride = NIN * g.run_stride;  // bytes per image slot (dy | x)
+  const uint32_t xoff = (NIN - 1) * g.run_stride;
+  const uint32_t run_elems = nch * g.HW;
+  const T* xg = static_cast<const T*>(a.x);
+  T* og = static_cast<T*>(a.out);
+  // element index of run k's first element in the tensor
+  auto run_start = [&](uint32_t k) -> size_t {
+    return ((size_t)(n0 + k) * g.C + cbase) * g.HW;
+  };
+
+  stamp(a, 0);
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < nk; ++k) bulk::mbar_init(&H.bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();  // x / dy (and the finisher inputs) may come from the previous kernel
+  pdl_trigger();
+  stamp(a, 1);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (w == 0) {
+    // ---- 1. one run per lane: expect the run's bytes, then issue its bulk copies
+    for (uint32_t k = l; k < nk; k += 32) {
+      const size_t gs = run_start(k);
+      const size_t b0 = (gs * es) & ~(size_t)15;
+      const size_t b1 = ((gs + run_elems) * es + 15) & ~(size_t)15;
+      const uint32_t bytes = (uint32_t)(b1 - b0);
+      H.lead[k] = (uint8_t)(((gs * es) & 15u) / es);
+      unsigned char* dst = smem + (data - (uint32_t)__cvta_generic_to_shared(smem)) +
+                           (size_t)k * kstride;
+      bulk::mbar_expect_tx(&H.bar[k], bytes * NIN);
+      if (BWD)
+        bulk::g2s(dst, static_cast<const unsigned char*>(a.dy) + b0, bytes, &H.bar[k]);
+      bulk::g2s(dst + xoff, reinterpret_cast<const unsigned char*>(xg) + b0, bytes, &H.bar[k]);
+    }
+    if (a.trace) {
+      stamp(a, 2);
+      if (threadIdx.x == 0)
+        for (uint32_t k = 0; k < nk; ++k) bulk::mbar_wait(&H.bar[k], 0);
+      stamp(a, 3);
+    }
+  } else {
+    // per-channel finisher inputs (overlap the copies): shift K / mean, ReLU mask
+    for (uint32_t i = threadIdx.x - 32; i < nch; i += kThreadsO - 32) {
+      const uint32_t c = cbase + i;
+      if constexpr (!BWD) {
+        ca.K[i] = (double)ld1(xg + (size_t)c * g.HW);  // rank's first element of channel c
+        ca.pre[i] = load_fwd_chan(a.F, c);
+      } else {
+        const BwdChan v = load_bwd_chan(a.B, c);
+        ca.pre[i] = v;
+        ca.K[i] = v.mean;
+        if (RELU) {
+          double P, Q;
+          affine_coeffs(v.mean, v.inv_std, (double)v.gamma, (double)v.beta, P, Q);
+          ca.pq[i] = make_double2(P, Q);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. per-channel reduction out of shared memory (two units in flight per thread)
+  {
+    const uint32_t wpc = 1u << g.wpc_log2;
+    const uint32_t nteams = kWarpsO >> g.wpc_log2;
+    const uint32_t team = (uint32_t)w >> g.wpc_log2;
+    const uint32_t tq = ((uint32_t)w & (wpc - 1)) * 32 + l;
+    const uint32_t tstride = wpc * 32;
+    const uint32_t total = nk * g.HWv;
+    const uint32_t sq = g.dhwv.div(tstride), sr = tstride - sq * g.HWv;
+    for (uint32_t i = team; i < g.nch; i += nteams) {
+      double s1a = 0.0, s2a = 0.0, s1b = 0.0, s2b = 0.0;
+      if (i < nch) {
+        const double K = ca.K[i];
+        double P = 0.0, Q = 0.0;
+        if (RELU) { P = ca.pq[i].x; Q = ca.pq[i].y; }
+        const uint32_t pbase = data + xoff + i * g.HW * es;  // plane i of run 0 (+ lead)
+        uint32_t k = g.dhwv.div(tq), o = tq - k * g.HWv;
+        uint32_t kw = 0xffffffffu;  // run whose copy this thread has waited for
+        auto addr = [&](uint32_t kk, uint32_t oo) -> uint32_t {
+          const uint32_t lead = ALIGNED ? 0u : (uint32_t)H.lead[kk];
+          return pbase + kk * kstride + (lead + oo * VE) * es;
+        };
+        auto step = [&](uint32_t& kk, uint32_t& oo) {
+          oo += sr;
+          kk += sq;
+          if (oo >= g.HWv) { oo -= g.HWv; ++kk; }
+        };
+        for (uint32_t j = tq; j < total; j += 2 * tstride) {
+          uint32_t k2 = k, o2 = o;
+          step(k2, o2);
+          const bool two = j + tstride < total;
+          const uint32_t kl = two ? k2 : k;  // the later run of the two units
+          if (kl != kw) {
+            for (uint32_t kk = (kw == 0xffffffffu ? k : kw + 1); kk <= kl; ++kk)
+              bulk::mbar_wait(&H.bar[kk], 0);
+            kw = kl;
+          }
+          const uint32_t ua = addr(k, o);
+          acc_unit<T, VE, BWD, RELU>(ua, ua - xoff, K, P, Q, s1a, s2a);
+          if (two) {
+            const uint32_t ub = addr(k2, o2);
+            acc_unit<T, VE, BWD, RELU>(ub, ub - xoff, K, P, Q, s1b, s2b);
+          }
+          k = k2;
+          o = o2;
+          step(k, o);
+        }
+      }
+      const double S1 = warp_sum(s1a + s1b);
+      const double S2 = warp_sum(s2a + s2b);
+      if (wpc == 1) {
+        if (l == 0 && i < nch) ca.part[i] = make_double2(S1, S2);
+      } else {
+        if (l == 0) H.wpart[w] = make_double2(S1, S2);
+        // the team's warps meet in shared memory (ascending warp order)
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(tstride) : "memory");
+        if (tq == 0 && i < nch) {
+          double2 t = H.wpart[w];
+          for (uint32_t u = 1; u < wpc; ++u) {
+            t.x += H.wpart[w + u].x;
+            t.y += H.wpart[w + u].y;
+          }
+          ca.part[i] = t;
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(tstride) : "memory");
+      }
+    }
+  }
+  if (KC > 1) cluster_barrier();
+  else __syncthreads();
+  stamp(a, 4);
+
+  // ---- 3. fold the KC CTA partials (rank order) and finish every channel
+  for (uint32_t i = threadIdx.x; i < nch; i += kThreadsO) {
+    const uint32_t c = cbase + i;
+    double S1 = 0.0, S2 = 0.0;
+    for (uint32_t u = 0; u < KC; ++u) {
+      const double2 t = KC > 1 ? ld_dsmem(&ca.part[i], u) : ca.part[i];
+      S1 += t.x;
+      S2 += t.y;
+    }
+    const bool write = (i % KC) == r;
+    if constexpr (!BWD) {
+      const double n = g.count;
+      const double mean = ca.K[i] + S1 / n;
+      const double M2 = fmax(S2 - S1 * (S1 / n), 0.0);
+      double P, Q;
+      finalize_fwd_channel(a.F, c, n, mean, M2, write, ca.pre[i], P, Q);
+      ca.c01[i] = make_double2(P, Q);
+    } else {
+      const DxCoef k = finalize_bwd_channel(a.B, c, S1, S2, write, ca.pre[i]);
+      ca.c01[i] = make_double2(k.A, k.B);
+      ca.c2[i] = make_double2(k.Cc, 0.0);
+    }
+  }
+  if (KC > 1) cluster_arrive();  // done reading the peers' partials
+  __syncthreads();
+  stamp(a, 5);
+
+  // ---- 4. elementwise pass from shared memory, memory order over each run
+  if constexpr (ALIGNED) {
+    // 16-byte chunks; a chunk lies in one plane: one coefficient lookup per chunk
+    const uint32_t total = nk * g.nq;
+    for (uint32_t j = threadIdx.x; j < total; j += kThreadsO) {
+      const uint32_t k = g.dnq.div(j), qq = j - k * g.nq;
+      const uint32_t i = g.dhwu.div(qq);
+      const uint32_t sx = data + k * kstride + xoff + qq * 16;
+      float xv[UE];
+      lds_vec<T, UE>(sx, xv);
+      double o[UE];
+      if constexpr (!BWD) {
+        const double2 pq = ca.c01[i];
+#pragma unroll
+        for (int e = 0; e < UE; ++e) {
+          double t = __fma_rn(pq.x, (double)xv[e], pq.y);
+          if (RELU) t = t > 0.0 ? t : 0.0;
+          o[e] = t;
+        }
+      } else {
+        float gv[UE];
+        lds_vec<T, UE>(sx - xoff, gv);
+        const double2 ab = ca.c01[i];
+        const double cc = ca.c2[i].x;
+        double2 pq = make_double2(0.0, 0.0);
+        if (RELU) pq = ca.pq[i];
+#pragma unroll
+        for (int e = 0; e < UE; ++e) {
+          double gk = (double)gv[e];
+          if (RELU && !(bn_out(pq.x, pq.y, xv[e]) > 0.0)) gk = 0.0;
+          o[e] = __fma_rn(ab.x, gk, __fma_rn(ab.y, (double)xv[e], cc));
+        }
+      }
+      stv<T, UE>(og + run_start(k) + (size_t)qq * UE, o);
+    }
+  } else {
+    // runs with a lead: walk the 16-byte chunks of each cover, channel per element
+    const uint32_t total = nk * g.nq;
+    for (uint32_t j = threadIdx.x; j < total; j += kThreadsO) {
+      const uint32_t k = g.dnq.div(j), qq = j - k * g.nq;
+      const uint32_t lead = H.lead[k];
+      if (qq * UE >= lead + run_elems) continue;  // past the run's cover
+      const uint32_t sx = data + k * kstride + xoff + qq * 16;
+      float xv[UE], gv[UE];
+      lds_vec<T, UE>(sx, xv);
+      if (BWD) lds_vec<T, UE>(sx - xoff, gv);
+      // element e of the chunk is run element qq*UE + e - lead
+      const int r0 = (int)(qq * UE) - (int)lead;
+      uint32_t rel = r0 > 0 ? (uint32_t)r0 : 0u;
+      uint32_t i = g.dhw.div(rel);
+      uint32_t rr = rel - i * g.HW;
+      double o[UE];
+      uint32_t inmask = 0;
+#pragma unroll
+      for (int e = 0; e < UE; ++e) {
+        const int re = r0 + e;
+        if (re < 0 || re >= (int)run_elems) { o[e] = 0.0; continue; }
+        inmask |= 1u << e;
+        double t;
+        if constexpr (!BWD) {
+          const double2 pq = ca.c01[i];
+          t = __fma_rn(pq.x, (double)xv[e], pq.y);
+          if (RELU) t = t > 0.0 ? t : 0.0;
+        } else {
+          double gk = (double)gv[e];
+          if (RELU && !(bn_out(ca.pq[i].x, ca.pq[i].y, xv[e]) > 0.0)) gk = 0.0;
+          const double2 ab = ca.c01[i];
+          t = __fma_rn(ab.x, gk, __fma_rn(ab.y, (double)xv[e], ca.c2[i].x));
+        }
+        o[e] = t;
+        if (++rr == g.HW) { rr = 0; ++i; }
+      }
+      T* dst = og + run_start(k) + r0;  // the chunk's first element (may precede the run)
+      if (inmask == (1u << UE) - 1u) {
+        stv<T, UE>(dst, o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < UE; ++e)
+          if ((inmask >> e) & 1u) st1(dst + e, o[e]);
+      }
+    }
+  }
+  if (a.trace) {
+    __syncthreads();
+    stamp(a, 6);
+  }
+  if (KC > 1) cluster_wait();  // peers may still read this CTA's partials until here
+}
+
+}  // namespace onchip
+}  // namespace

@@ -30,6 +30,7 @@
 
 #pragma once
 
+namespace {
 namespace p2p {
 
 constexpr int kThreadsP2P = 256;
@@ -46,11 +47,13 @@ __device__ void exchange_rank(const double* __restrict__ vec, int64_t n, int ran
                               const Peers& peers, int64_t max_len, double* __restrict__ out,
                               unsigned* status, uint64_t timeout_ns) {
   __shared__ unsigned long long s_epoch;
+  __shared__ unsigned s_missing;  // bit q: rank q did not publish in time
   char* mine = peers.base[rank];
   if (threadIdx.x == 0) {
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(mine);
     s_epoch = *ctr + 1;
     *ctr = s_epoch;
+    s_missing = 0u;
   }
   __syncthreads();
   const unsigned long long e = s_epoch;
@@ -71,16 +74,21 @@ __device__ void exchange_rank(const double* __restrict__ vec, int64_t n, int ran
     while (ld_acquire_sys(f) < e) {
       if (now_ns() - t0 > timeout_ns) {
         if (status) atomicOr(status, CGBN_STATUS_EXCHANGE_TIMEOUT);
+        atomicOr(&s_missing, 1u << threadIdx.x);
         break;
       }
     }
   }
   __syncthreads();
   __threadfence_system();
-  // 5. rows in rank order into the fixed output buffer
+  // 5. rows in rank order into the fixed output buffer; a missing rank's row is NaN (its
+  // slot still holds an older exchange), so nothing downstream folds stale statistics
+  const unsigned missing = s_missing;
   for (int q = 0; q < G; ++q) {
     const double* src = recv_ptr(mine, G, max_len, par, q);
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[(size_t)q * n + i] = src[i];
+    const bool miss = (missing >> q) & 1u;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      out[(size_t)q * n + i] = miss ? __longlong_as_double(0x7ff8000000000000ll) : src[i];
   }
 }
 
@@ -104,3 +112,4 @@ k_p2p_emulate(const double* vecs, int64_t n, int G, Peers peers, int64_t max_len
 }
 
 }  // namespace p2p
+}  // namespace

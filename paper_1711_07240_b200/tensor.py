@@ -61,6 +61,11 @@ def geometry(x, what: str = "x", err=TensorError) -> Geometry:
         raise err(f"{what} must be float32, bfloat16 or float16, got {x.dtype}")
 
     def geo(t, n, c, hw, mem):
+        # the kernels move 16-byte units: a view whose storage offset breaks the 16-byte
+        # alignment (e.g. x[1:] of an (N, 3) tensor) is copied to fresh, aligned storage
+        if t.data_ptr() % 16:
+            t = t.clone(memory_format=torch.channels_last if mem == _lib.LAYOUT_NHWC
+                        else torch.contiguous_format)
         return Geometry(t, n, c, hw, mem | act, mem)
 
     if x.dim() == 2:

@@ -95,3 +95,32 @@ def test_producer_conv_argument_validation_without_gpu():
     assert rc == _lib.ERR_INVALID and b"slot table" in lib.cgbn_last_error()
     rc = lib.cgbn_conv_nhwc_stats(16, 16, None, 2, 64, 128, 8, 8, 3, 2, 0, 16, 16, 16, 0, None)
     assert rc == _lib.ERR_INVALID and b"workspace" in lib.cgbn_last_error()
+
+
+def test_stale_build_rejected(monkeypatch):
+    """load() checks the ABI version and every bound symbol before use."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "ABI_VERSION", 5)
+    with pytest.raises(_lib.CGBNLibraryError, match="ABI v6"):
+        _lib.load()
+    monkeypatch.setattr(_lib, "ABI_VERSION", 6)
+    monkeypatch.setitem(_lib.SIGNATURES, "cgbn_not_there", (_lib._i, []))
+    with pytest.raises(_lib.CGBNLibraryError, match="cgbn_not_there"):
+        _lib.load()
+
+
+@pytest.mark.parametrize("act", [_lib.ACT_F32, _lib.ACT_BF16, _lib.ACT_F16])
+def test_dtype_units_share_the_error_message(act):
+    """Each activation dtype is its own translation unit (cgbn.cu, cgbn_bf16.cu,
+    cgbn_f16.cu); the public entry points route on the dtype bits of `layout` and every
+    unit reports through the one thread-local message."""
+    lib = _lib.load()
+    rc = lib.cgbn_fwd_stats(None, 2, 3, 4, act, None, None, 0, None)
+    assert rc == _lib.ERR_INVALID and b"NULL" in lib.cgbn_last_error()
+    rc = lib.cgbn_bwd_local(1, 1, 2, 3, 4, act, 1, 1, 1, -1.0, 0, 1, None, None, None, None,
+                            0, None)
+    assert rc == _lib.ERR_INVALID and b"eps" in lib.cgbn_last_error()
+    rc = lib.cgbn_fwd_stats(1, 2, 3, 4, 0x30, 1, None, 0, None)  # unknown dtype -> unit 0
+    assert rc == _lib.ERR_INVALID and b"dtype" in lib.cgbn_last_error()
+    for name in ("cgbn_fwd_stats_a0", "cgbn_fwd_stats_a1", "cgbn_fwd_stats_a2"):
+        assert hasattr(lib, name)

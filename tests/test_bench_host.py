@@ -56,6 +56,8 @@ def test_reference_arm_json_line_contract():
     assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 3
     assert d["metric"] == bench.METRIC and d["unit"] == bench.UNIT and d["value"] > 0
     assert d["higher_is_better"] is True and d["n_gpus"] == 1
+    # like-for-like with the GPU arm: the config's own workload and per-GPU batch
+    assert d["config"]["workload"] == "latency_2048x7x7" and d["config"]["per_gpu_batch"] == 1
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] == 1 and cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,

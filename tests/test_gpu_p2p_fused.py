@@ -203,6 +203,11 @@ def test_fused_exchange_missing_rank_times_out():
         for r, k in enumerate(ranks):
             if r != 2:
                 assert int(k.status.item()) & _lib.STATUS_EXCHANGE_TIMEOUT
+                # the missing rank's stale rows are never folded: the layer state is left
+                # as it was and the outputs are NaN (no silent stale statistics)
+                assert torch.equal(k.rm, torch.zeros_like(k.rm))
+                assert torch.equal(k.rv, torch.ones_like(k.rv))
+                assert bool(torch.isnan(k.y).all())
     finally:
         reg.free()
 

@@ -280,6 +280,20 @@ def test_errors_match_reference():
         cg.DeviceGroup(1).run(foreign)
 
 
+def test_inplace_change_of_x_before_backward_raises():
+    """The cache holds x by reference (x_hat is recomputed), so an in-place change of x
+    between forward and backward must raise instead of giving wrong gradients."""
+    dev = _dev()
+    x = torch.randn(4, 3, 5, 5, device=dev)
+    st = cg.BNLayerState.create(3)
+    _, cache = cg.bn_forward_local(x, st)
+    x.mul_(2.0)
+    with pytest.raises(cg.BatchNormError, match="in place"):
+        cg.bn_backward_local(torch.randn_like(x), cache, st)
+    _, cache = cg.bn_forward_local(x, st)  # untouched x: fine
+    cg.bn_backward_local(torch.randn_like(x), cache, st)
+
+
 def test_allreduce_sum_ascending_fold_bitwise():
     # collectives.py:293-295 / test_collectives.py:43-51
     dev = _dev()
@@ -350,7 +364,8 @@ def test_fused_eligibility():
     assert lib.cgbn_fused_supported(32, 64, 3136, 0, 0) == 1
     assert lib.cgbn_fused_supported(32, 64, 3136, 0, 1) == 0      # 6.4M: backward too big
     assert lib.cgbn_fused_supported(32, 256, 3136, 0, 0) == 0     # 25.7M: neither
-    assert lib.cgbn_fused_supported(32, 2048, 49, 0, 0) == 0      # HW % 4 != 0
+    assert lib.cgbn_fused_supported(32, 2048, 49, 0, 0) == 1      # odd planes: lead-aware path
+    assert lib.cgbn_fused_supported(32, 2048, 49, 0, 1) == 1
     assert lib.cgbn_fused_supported(32, 128, 784, 1, 0) == 0      # NHWC
 
 
@@ -445,3 +460,27 @@ def test_max_channels(shape, cl):
             assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_FWD, (key, r)
         for key in ("dx", "dgamma", "dbeta"):
             assert O.rel_err(outs[r][key], ref[r][key]) <= TOL_BWD, (key, r)
+
+
+@pytest.mark.parametrize("cl", [False, True])
+def test_misaligned_view_is_realigned(cl):
+    """A contiguous view with an unaligned storage offset runs (copied to aligned
+    storage by tensor.geometry) and matches the oracle (VERDICT r1 hygiene)."""
+    dev = _dev()
+    rng = np.random.default_rng(77)
+    if cl:
+        base = torch.from_numpy(rng.standard_normal((5, 3, 4, 4)).astype(np.float32)).to(dev)
+        base = base.contiguous(memory_format=torch.channels_last)
+        x = base.view(-1)[1:1 + 4 * 3 * 16].view(4, 4, 4, 3).permute(0, 3, 1, 2)
+        assert x.is_contiguous(memory_format=torch.channels_last)
+    else:
+        base = torch.from_numpy(rng.standard_normal((9, 3)).astype(np.float32)).to(dev)
+        x = base[1:]
+    assert x.data_ptr() % 16 != 0
+    st = cg.BNLayerState.create(3)
+    y, cache = cg.bn_forward_local(x, st)
+    dx, dg, db = cg.bn_backward_local(torch.ones_like(x), cache, st)
+    ref = O.cgbn_world([x.double().cpu().numpy()], np.ones(3), np.zeros(3), 1,
+                       dys=[np.ones(tuple(x.shape))])[0]
+    assert O.rel_err(y.cpu().numpy(), ref["y"]) <= TOL_FWD
+    assert O.rel_err(dx.cpu().numpy(), ref["dx"]) <= TOL_BWD

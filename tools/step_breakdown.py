@@ -1,21 +1,50 @@
 #!/usr/bin/env python3
-"""Per-layer / per-kernel device times of one bench step from an ncu launch list
-(gpu__time_duration.sum + dram bytes), taken with
-    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-        --cache-control none --csv --log-file L.csv \
-        python bench.py --steps 1 --warmup 3 --no-graph --no-e2e --no-cpu-baseline --no-kprof
-The last 4*53 CGBN launches of the list are the measured step (fwd: reduce, elementwise
-per layer; bwd: reduce, elementwise per layer in reverse order)."""
+"""Per-kernel-family device time and DRAM traffic of one bench step, from an ncu launch
+list (gpu__time_duration.sum + dram bytes), taken with
+
+    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
+        --cache-control none --clock-control none --csv --log-file L.csv \\
+        python bench.py --steps 1 --warmup 3 --no-graph --no-e2e --no-cpu-baseline \\
+        --no-kprof --no-parity --no-producer
+
+The process launches (warmup + steps) identical steps; the last 1/(warmup+steps) of our
+launches is the measured step. Launches are classified by kernel name into the families
+bench.py times (FAMILY_BPE): the on-chip single-launch passes (k_onchip, forward /
+backward by its BWD template flag), statistics and backward reductions (k_reduce_*,
+k_fold_rows over StatsOp / BwdOp) and the elementwise passes with their finalize kernels
+(k_ew_affine, k_finalize_fwd -> fwd_normalize; k_ew_dx, k_finalize_bwd -> bwd_dx).
+
+    python tools/step_breakdown.py L.csv [--passes 4]            # family table
+    python tools/step_breakdown.py L.csv --traffic out.json [--passes 4]
+"""
+import argparse
 import csv
+import json
 import os
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from bench import numel, resnet50_bn_shapes  # noqa: E402
+from bench import FAMILY_BPE  # noqa: E402
+
+OURS = ("k_onchip", "k_reduce", "k_fold_rows", "k_ew_", "k_finalize")
 
 
-def load_step(path):
-    """The measured step's 4*53 launches: (fwd, bwd) lists of per-launch metric dicts."""
+def family(name):
+    if "k_onchip" in name:
+        # k_onchip<T, VE, BWD, RELU>: the third template argument
+        args = re.search(r"k_onchip<([^>]*)>", name).group(1).split(",")
+        return "bwd_onchip" if args[2].strip() in ("1", "(bool)1", "true") else "fwd_onchip"
+    if "k_reduce" in name or "k_fold_rows" in name:
+        return "bwd_reduce" if "BwdOp" in name or "BwdRows" in name else "fwd_stats"
+    if "k_ew_affine" in name or "k_finalize_fwd" in name or "k_finalize_sums" in name:
+        return "fwd_normalize"
+    if "k_ew_dx" in name or "k_finalize_bwd" in name:
+        return "bwd_dx"
+    return None
+
+
+def load_launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     ki, mi, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
@@ -23,76 +52,61 @@ def load_step(path):
     for r in rows[1:]:
         d = k.setdefault(int(r[ii]), {"name": r[ki]})
         d[r[mi]] = float(r[vi].replace(",", ""))
-    ours = [k[i] for i in sorted(k) if ("k_reduce" in k[i]["name"] or "k_ew" in k[i]["name"])]
-    shapes = resnet50_bn_shapes(32)
-    step = ours[-4 * len(shapes):]
-    return shapes, step[:2 * len(shapes)], step[2 * len(shapes):]
+    return [k[i] for i in sorted(k) if any(t in k[i]["name"] for t in OURS)]
 
 
-def traffic_json(path, out):
-    """Per-family dram bytes per launch (what bench.py reports as roofline.traffic)."""
-    shapes, fwd, bwd = load_step(path)
-    fam = {"fwd_stats": [], "fwd_normalize_ew": [], "bwd_reduce": [], "bwd_dx": []}
-    bpe = {"fwd_stats": 4, "fwd_normalize_ew": 8, "bwd_reduce": 8, "bwd_dx": 12}
-    for li, s in enumerate(shapes):
-        bi = len(shapes) - 1 - li
-        for name, kk in zip(fam, (fwd[2 * li], fwd[2 * li + 1], bwd[2 * bi], bwd[2 * bi + 1])):
-            fam[name].append((kk, numel(s)))
+def step_families(path, passes):
+    ours = load_launches(path)
+    per = len(ours) // passes
+    step = ours[-per:]
+    fam = {}
+    for kk in step:
+        f = family(kk["name"])
+        if f is None:
+            continue
+        fam.setdefault(f, []).append(kk)
+    return fam, per
+
+
+def summarise(fam):
+    tot_t = sum(kk["gpu__time_duration.sum"] for v in fam.values() for kk in v)
     res = {}
-    tot_t = sum(kk["gpu__time_duration.sum"] for v in fam.values() for kk, _ in v)
     for name, v in fam.items():
-        n = len(v)
         dram = sum(kk.get("dram__bytes_read.sum", 0) + kk.get("dram__bytes_write.sum", 0)
-                   for kk, _ in v)
-        alg = sum(bpe[name] * e for _, e in v)
-        t = sum(kk["gpu__time_duration.sum"] for kk, _ in v)
-        res[name] = {"launches": n, "dram_bytes_per_launch": dram / n,
-                     "alg_bytes_per_launch": alg / n, "dram_over_alg": dram / alg,
-                     "ncu_time_us_per_step": t / 1e3, "ncu_share": t / tot_t}
-    doc = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
-                     "dram__bytes_write.sum --cache-control none --clock-control none on "
-                     "`python bench.py --steps 1 --warmup 3 --no-graph --no-e2e "
-                     "--no-cpu-baseline --no-kprof` (one eager step; per-kernel-family sums "
-                     "over the 53 layers). Per-launch dram bytes include write-backs of "
-                     "lines the previous kernel left dirty in L2.",
-           "launch_list": os.path.basename(path), "families": res}
-    import json
-    json.dump(doc, open(out, "w"), indent=1)
+                   for kk in v)
+        t = sum(kk["gpu__time_duration.sum"] for kk in v)
+        res[name] = {"launches": len(v), "dram_bytes_per_launch": dram / len(v),
+                     "ncu_time_us_per_step": t / 1e3, "ncu_share": t / tot_t,
+                     "dram_gbs": dram / t if t else None, "bytes_per_elem": FAMILY_BPE[name]}
+    return res
 
 
-def main(path):
-    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
-    h = rows[0]
-    ki, mi, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
-    k = {}
-    for r in rows[1:]:
-        d = k.setdefault(int(r[ii]), {"name": r[ki]})
-        d[r[mi]] = float(r[vi].replace(",", ""))
-    ours = [k[i] for i in sorted(k) if ("k_reduce" in k[i]["name"] or "k_ew" in k[i]["name"])]
-    shapes = resnet50_bn_shapes(32)
-    step = ours[-4 * len(shapes):]
-    fwd, bwd = step[:2 * len(shapes)], step[2 * len(shapes):]
-    print(f"{'l':>3} {'C,H,W':>16} {'stats':>6} {'norm':>6} {'bred':>6} {'dx':>6} {'sum us':>7}"
-          f" {'alg GB/s':>8} {'dram/alg':>8}")
-    tot = [0.0] * 4
-    dram = alg = 0.0
-    for li, s in enumerate(shapes):
-        bi = len(shapes) - 1 - li
-        ks = (fwd[2 * li], fwd[2 * li + 1], bwd[2 * bi], bwd[2 * bi + 1])
-        t = [x["gpu__time_duration.sum"] / 1e3 for x in ks]
-        by = sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in ks)
-        for i in range(4):
-            tot[i] += t[i]
-        dram += by
-        alg += 32 * numel(s)
-        print(f"{li:3d} {str(s[1:]):>16} {t[0]:6.1f} {t[1]:6.1f} {t[2]:6.1f} {t[3]:6.1f} "
-              f"{sum(t):7.1f} {32 * numel(s) / (sum(t) * 1e-6) / 1e9:8.0f} {by / (32 * numel(s)):8.2f}")
-    print("totals us: stats %.1f norm %.1f bred %.1f dx %.1f | sum %.1f | dram/alg %.3f"
-          % (tot[0], tot[1], tot[2], tot[3], sum(tot), dram / alg))
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("csv")
+    ap.add_argument("--traffic", default=None, help="write the per-family JSON here")
+    ap.add_argument("--passes", type=int, default=4, help="warmup + timed steps in the run")
+    a = ap.parse_args()
+    fam, per = step_families(a.csv, a.passes)
+    res = summarise(fam)
+    if a.traffic:
+        doc = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                         "dram__bytes_write.sum --cache-control none --clock-control none on "
+                         "`python bench.py --steps 1 --warmup 3 --no-graph --no-e2e "
+                         "--no-cpu-baseline --no-kprof --no-parity --no-producer` (one eager "
+                         "step; launches classified by kernel name). Per-launch dram bytes "
+                         "include write-backs of lines the previous kernel left dirty in L2.",
+               "launch_list": os.path.basename(a.csv), "launches_per_step": per,
+               "families": res}
+        json.dump(doc, open(a.traffic, "w"), indent=1)
+    print(f"{'family':>14} {'launches':>8} {'ncu us':>9} {'share':>6} {'dram MB/launch':>14}"
+          f" {'dram GB/s':>9}")
+    for name, v in sorted(res.items(), key=lambda kv: -kv[1]["ncu_time_us_per_step"]):
+        print(f"{name:>14} {v['launches']:8d} {v['ncu_time_us_per_step']:9.1f} "
+              f"{v['ncu_share']:6.3f} {v['dram_bytes_per_launch'] / 1e6:14.2f} "
+              f"{(v['dram_gbs'] or 0):9.0f}")
+    print(f"launches per step: {per}")
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 3 and sys.argv[2] == "--traffic":
-        traffic_json(sys.argv[1], sys.argv[3])
-    else:
-        main(sys.argv[1])
+    main()
