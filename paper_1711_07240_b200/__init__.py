@@ -30,6 +30,7 @@ from .collectives import (
     DeviceGroup,
     DeviceHandle,
     DistHandle,
+    GradBuckets,
     SoloHandle,
     allreduce_sum,
     world_mean_allreduce,
@@ -43,6 +44,6 @@ __all__ = [
     "bn_update_running", "check_status", "set_forward_exchange", "set_fused", "set_strict", "sync_bn_backward", "sync_bn_forward",
     "DEFAULT_TIMEOUT_S", "SCOPE_BN_GROUP", "SCOPE_WORLD", "CollectiveError",
     "CollectiveProtocolError", "CollectiveTimeoutError", "DeviceGroup", "DeviceHandle",
-    "DistHandle", "SoloHandle", "allreduce_sum", "world_mean_allreduce", "ChannelStats", "NonFiniteError", "TensorError",
+    "DistHandle", "GradBuckets", "SoloHandle", "allreduce_sum", "world_mean_allreduce", "ChannelStats", "NonFiniteError", "TensorError",
     "channel_affine", "channel_sum",
 ]

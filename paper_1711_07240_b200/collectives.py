@@ -671,3 +671,113 @@ def world_mean_allreduce(handle: _HandleBase, grads: dict, loss=None):
         out[k] = mean[off:off + n].view(grads[k].shape).to(grads[k].dtype)
         off += n
     return out, (float(mean[-1].item()) if loss is not None else None)
+
+
+class GradBuckets:
+    """The world-gradient allreduce of the trainer (trainer.py:419-428), bucketed and
+    overlapped with the backward.
+
+    The reference concatenates every gradient after the backward and allreduces once.
+    Here gradients are handed over as the backward produces them (``add``); when a bucket
+    reaches ``bucket_bytes`` its allreduce is issued on a side CUDA stream, after an
+    event on the producing stream, so the exchange and the ascending-rank fold run while
+    the backward of the next layers keeps the compute stream busy. ``finish`` adds the
+    loss to the last bucket, makes the caller's stream wait for the side stream and
+    returns the mean gradients and loss.
+
+    Numerics: every element is the ascending-rank fold of that element over the world
+    (allreduce_sum), divided by the world size, so the bucketing changes nothing: the
+    result is bitwise identical to world_mean_allreduce on the same gradients when
+    ``dtype`` matches its choice (fp64 if any gradient is fp64, else fp32).
+
+    ``reduce_fn(handle, scope, vec) -> vec`` defaults to allreduce_sum (CUDA tensors).
+    """
+
+    def __init__(self, handle, bucket_bytes: int = 16 << 20, dtype=torch.float32,
+                 reduce_fn=None):
+        self.handle = handle
+        self.bucket_bytes = int(bucket_bytes)
+        self.dtype = dtype
+        self.reduce_fn = reduce_fn or allreduce_sum
+        self._pending = []   # (name, tensor) of the open bucket
+        self._pending_bytes = 0
+        self._issued = []    # (names, shapes, dtypes, sizes, result, event)
+        self._names = set()
+        self._side = None
+        self.buckets_issued = 0
+
+    def _stream(self, dev):
+        if dev.type != "cuda":
+            return None
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=dev)
+        return self._side
+
+    def add(self, name: str, grad: torch.Tensor) -> None:
+        """Hand over one gradient (in the order the backward produces them)."""
+        if name in self._names:
+            raise ValueError(f"gradient {name!r} added twice")
+        self._names.add(name)
+        self._pending.append((name, grad))
+        self._pending_bytes += grad.numel() * torch.finfo(self.dtype).bits // 8
+        if self._pending_bytes >= self.bucket_bytes:
+            self._issue()
+
+    def _issue(self, loss=None):
+        if not self._pending and loss is None:
+            return
+        items, self._pending, self._pending_bytes = self._pending, [], 0
+        dev = items[0][1].device if items else torch.device(self.handle.device)
+        side = self._stream(dev)
+        flat_in = [g.reshape(-1) for _, g in items]
+        if side is not None:
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(dev))
+            side.wait_event(ready)
+            ctx = torch.cuda.stream(side)
+        else:
+            ctx = _nullcontext()
+        with ctx:
+            parts = [t.to(self.dtype) for t in flat_in]
+            if loss is not None:
+                parts.append(torch.as_tensor([float(loss)], dtype=self.dtype, device=dev))
+            summed = self.reduce_fn(self.handle, SCOPE_WORLD, torch.cat(parts))
+            mean = summed / self.handle.world_size
+            done = None
+            if side is not None:
+                for t in flat_in:
+                    t.record_stream(side)
+                done = torch.cuda.Event()
+                done.record(side)
+        self._issued.append(([n for n, _ in items], [g.shape for _, g in items],
+                             [g.dtype for _, g in items], mean, done, loss is not None))
+        self.buckets_issued += 1
+
+    def finish(self, loss=None):
+        """Issue the last bucket (with the loss), wait on the caller's stream, return
+        ({name: mean gradient}, mean loss or None)."""
+        self._issue(loss=loss)
+        out, mloss = {}, None
+        for names, shapes, dtypes, mean, done, has_loss in self._issued:
+            if done is not None:
+                torch.cuda.current_stream(mean.device).wait_event(done)
+                mean.record_stream(torch.cuda.current_stream(mean.device))
+            off = 0
+            for n, shp, dt in zip(names, shapes, dtypes):
+                k = 1
+                for e in shp:
+                    k *= e
+                out[n] = mean[off:off + k].view(shp).to(dt)
+                off += k
+            if has_loss:
+                mloss = float(mean[-1].item())
+        self._issued, self._names = [], set()
+        return out, mloss
+
+
+class _nullcontext:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

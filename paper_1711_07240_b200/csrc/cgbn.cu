@@ -130,6 +130,32 @@ int cgbn_internal_set_error(int code, const char* msg) {
 }
 #endif
 
+namespace {
+// A rank's partial through the on-chip kernel (statistics only) when the layer is
+// on-chip eligible, so it is bitwise the partial the single-rank path reduces: the
+// group-of-identical-shards invariant (test_batchnorm.py:252-262) and the bitwise match
+// of every exchange transport hold. Returns 1 if launched, 0 if not eligible, < 0 error.
+int onchip_stats(bool bwd, int act, bool relu, int64_t N, int64_t C, int64_t HW, int layout,
+                 uintptr_t align, const void* x, const void* dy, const double* saved,
+                 const float* gamma, const float* beta, double* partial,
+                 const p2p::Push* push, cudaStream_t st) {
+  onchip::Args oa;
+  memset(&oa, 0, sizeof(oa));
+  oa.x = x;
+  oa.dy = dy;
+  oa.partial = partial;
+  if (push) oa.push = *push;
+  oa.B.saved = saved;
+  oa.B.gamma = gamma;
+  oa.B.beta = beta;
+  oa.B.relu = relu ? 1 : 0;
+  oa.B.C = (uint32_t)C;
+  oa.F.C = (uint32_t)C;
+  return bwd ? try_onchip<true>(act, relu, N, C, HW, layout, align, oa, st)
+             : try_onchip<false>(act, false, N, C, HW, layout, align, oa, st);
+}
+}  // namespace
+
 // ==================================================================================
 // C ABI
 
@@ -146,7 +172,10 @@ int CGBN_FN(cgbn_fwd_stats)(const void* x, int64_t N, int64_t C, int64_t HW, int
   WsView w;
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  CGBN_TRY(dispatch_stats(pl, x, true, kPartial, partial, nullptr, nullptr, w, st));
+  const int oc = onchip_stats(false, act, false, N, C, HW, layout, (uintptr_t)x, x, nullptr,
+                              nullptr, nullptr, nullptr, partial, nullptr, st);
+  if (oc < 0) return -oc;
+  if (oc == 0) CGBN_TRY(dispatch_stats(pl, x, true, kPartial, partial, nullptr, nullptr, w, st));
   return check_launch("cgbn_fwd_stats");
 }
 
@@ -248,6 +277,8 @@ int CGBN_FN(cgbn_fwd_train_local)(const void* x, int64_t N, int64_t C, int64_t H
   // single launch with the activation held on chip when the layer fits (cgbn_onchip.cuh)
   onchip::Args oa;
   oa.trace = nullptr;
+  oa.partial = nullptr;
+  oa.push.G = 0;
   oa.x = x;
   oa.dy = nullptr;
   oa.out = y;
@@ -325,8 +356,13 @@ int CGBN_FN(cgbn_bwd_reduce)(const void* dy, const void* x, int64_t N, int64_t C
   WsView w;
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, partial,
-                               nullptr, w, st));
+  const int oc = onchip_stats(true, act, relu != 0, N, C, HW, layout,
+                              (uintptr_t)dy | (uintptr_t)x, x, dy, saved, gamma, beta, partial,
+                              nullptr, st);
+  if (oc < 0) return -oc;
+  if (oc == 0)
+    CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, partial,
+                                 nullptr, w, st));
   return check_launch("cgbn_bwd_reduce");
 }
 
@@ -376,6 +412,8 @@ int CGBN_FN(cgbn_bwd_local)(const void* dy, const void* x, int64_t N, int64_t C,
       make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
   onchip::Args oa;
   oa.trace = nullptr;
+  oa.partial = nullptr;
+  oa.push.G = 0;
   oa.x = x;
   oa.dy = dy;
   oa.out = dx;
@@ -403,8 +441,8 @@ int CGBN_FN(cgbn_debug_onchip_trace)(void* dev_buf) {
 int CGBN_FN(cgbn_fused_supported)(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
   int act = 0;
   if (split_fmt(&layout, &act)) return 0;
-  return (backward ? onchip_supported<true>(act, false, N, C, HW, layout)
-                   : onchip_supported<false>(act, false, N, C, HW, layout))
+  return (backward ? onchip_supported<true>(act, false, N, C, HW, layout, false)
+                   : onchip_supported<false>(act, false, N, C, HW, layout, false))
              ? 1
              : 0;
 }
@@ -421,6 +459,8 @@ int CGBN_FN(cgbn_fwd_fused)(const void* x, int64_t N, int64_t C, int64_t HW, int
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   onchip::Args oa;
   oa.trace = nullptr;
+  oa.partial = nullptr;
+  oa.push.G = 0;
   oa.x = x;
   oa.dy = nullptr;
   oa.out = y;
@@ -428,7 +468,7 @@ int CGBN_FN(cgbn_fwd_fused)(const void* x, int64_t N, int64_t C, int64_t HW, int
   oa.F.P = oa.F.Q = nullptr;  // the coefficients stay in shared memory
   const int oc = try_onchip<false>(act, relu != 0, N, C, HW, layout,
                                    (uintptr_t)x | (uintptr_t)y, oa,
-                                   reinterpret_cast<cudaStream_t>(stream));
+                                   reinterpret_cast<cudaStream_t>(stream), false);
   if (oc < 0) return -oc;
   if (oc == 0) return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_fwd_fused: layer does not fit on chip");
   return check_launch("cgbn_fwd_fused");
@@ -449,6 +489,8 @@ int CGBN_FN(cgbn_bwd_fused)(const void* dy, const void* x, int64_t N, int64_t C,
   CGBN_TRY(ws_view(ws, ws_bytes, N, C, HW, layout, &w));
   onchip::Args oa;
   oa.trace = nullptr;
+  oa.partial = nullptr;
+  oa.push.G = 0;
   oa.x = x;
   oa.dy = dy;
   oa.out = dx;
@@ -456,7 +498,7 @@ int CGBN_FN(cgbn_bwd_fused)(const void* dy, const void* x, int64_t N, int64_t C,
   oa.B.A = oa.B.B = oa.B.Cc = oa.B.P = oa.B.Q = nullptr;
   const int oc = try_onchip<true>(act, relu != 0, N, C, HW, layout,
                                   (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, oa,
-                                  reinterpret_cast<cudaStream_t>(stream));
+                                  reinterpret_cast<cudaStream_t>(stream), false);
   if (oc < 0) return -oc;
   if (oc == 0) return set_error(CGBN_ERR_UNSUPPORTED, "cgbn_bwd_fused: layer does not fit on chip");
   return check_launch("cgbn_bwd_fused");
@@ -530,6 +572,10 @@ int CGBN_FN(cgbn_fwd_stats_p2p)(const void* x, int64_t N, int64_t C, int64_t HW,
   p2p::Push push;
   CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C + 1, C));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int oc = onchip_stats(false, act, false, N, C, HW, layout, (uintptr_t)x, x, nullptr,
+                              nullptr, nullptr, nullptr, nullptr, &push, st);
+  if (oc < 0) return -oc;
+  if (oc == 1) return check_launch("cgbn_fwd_stats_p2p");
   PushScope scope(&push);
   CGBN_TRY(dispatch_stats(pl, x, true, kPartial, nullptr, nullptr, nullptr, w, st));
   return check_launch("cgbn_fwd_stats_p2p");
@@ -574,6 +620,11 @@ int CGBN_FN(cgbn_bwd_reduce_p2p)(const void* dy, const void* x, int64_t N, int64
   p2p::Push push;
   CGBN_TRY(make_push(&push, rank, G, regions, max_len, 2 * C, C));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int oc = onchip_stats(true, act, relu != 0, N, C, HW, layout,
+                              (uintptr_t)dy | (uintptr_t)x, x, dy, saved, gamma, beta, nullptr,
+                              &push, st);
+  if (oc < 0) return -oc;
+  if (oc == 1) return check_launch("cgbn_bwd_reduce_p2p");
   PushScope scope(&push);
   CGBN_TRY(dispatch_bwd_reduce(pl, dy, x, saved, gamma, beta, relu != 0, kPartial, nullptr,
                                nullptr, w, st));

@@ -831,15 +831,23 @@ BwdFinal make_bwd_final(int64_t C, const double* saved, const float* gamma, cons
 
 // ---- single-launch on-chip passes (cgbn_onchip.cuh), single-rank groups
 
-// CGBN_NO_ONCHIP=1: always the split path (A/B). CGBN_ONCHIP_MAX_MB: largest activation
-// footprint (x, or dy + x, in MB) sent on chip; default from the B200 sweep.
+// CGBN_NO_ONCHIP=1: always the split path (A/B). CGBN_ONCHIP_MAX_FRAC: the largest
+// activation footprint (x, or dy + x) sent on chip, as a fraction of the GPU's total
+// shared memory. Default from the in-step A/B on B200 (tools/gpu/onchip_frac.sh,
+// profiles/r2_onchip_frac.jsonl; ResNet-50 b32 step, fp32):
+//   0 (off) 2.118 ms, 0.1 2.114, 0.2 2.103, 0.4 2.088 (best), 0.8 2.344 ms.
+// Up to ~13 MB the single launch wins; the 25.7 MB layers lose because the split path's
+// second read of x already hits the 126 MB L2 inside the step, while the on-chip kernel
+// serialises copy-in, conversion-bound reduction (F2F.F64.F32 runs at 16/clk/SM,
+// tools/lab/convbench.cu) and write-out per CTA. 16-bit activations: off (0.1 no gain,
+// 0.4 2% slower).
 struct OnchipEnv {
   bool enabled = true;
-  double max_frac = 0.80;  // of the GPU's total shared memory
+  double max_frac4 = 0.40, max_frac2 = 0.0;  // fp32 / 16-bit activations
   int force_kc = 0, force_nch = 0;
   OnchipEnv() {
     enabled = getenv("CGBN_NO_ONCHIP") == nullptr;
-    if (const char* e = getenv("CGBN_ONCHIP_MAX_FRAC")) max_frac = atof(e);
+    if (const char* e = getenv("CGBN_ONCHIP_MAX_FRAC")) max_frac4 = max_frac2 = atof(e);
     if (const char* e = getenv("CGBN_ONCHIP_FORCE")) sscanf(e, "%d,%d", &force_nch, &force_kc);
   }
 };
@@ -920,33 +928,36 @@ int64_t cluster_capacity_smem(K kernel, uint32_t kc, size_t smem) {
   return n;
 }
 
+// ve == 16 / sizeof(T): the aligned instance; 1: odd planes (masked 16-byte covers)
 template <class T, bool BWD, bool RELU>
 auto onchip_kernel(int ve) {
-  switch (ve) {
-    case 8: return onchip::k_onchip<T, (sizeof(T) == 2 ? 8 : 4), BWD, RELU>;  // 16-bit only
-    case 4: return onchip::k_onchip<T, 4, BWD, RELU>;
-    case 2: return onchip::k_onchip<T, 2, BWD, RELU>;
-    default: return onchip::k_onchip<T, 1, BWD, RELU>;
-  }
+  constexpr int ue = 16 / (int)sizeof(T);
+  return ve == ue ? onchip::k_onchip<T, ue, BWD, RELU> : onchip::k_onchip<T, 1, BWD, RELU>;
 }
 
 // Choose (nch, KC): every CTA resident in one wave, the least bytes on the busiest SM.
 template <class T, bool BWD, bool RELU>
-bool onchip_plan_t(int64_t N, int64_t C, int64_t HW, OnchipPlan* p) {
+bool onchip_plan_t(int64_t N, int64_t C, int64_t HW, OnchipPlan* p, bool capped) {
   constexpr int es = (int)sizeof(T);
   constexpr int nin = BWD ? 2 : 1;
   const OnchipEnv& env = onchip_env();
-  // unit width: a full 16-byte chunk when planes are whole chunks (every run 16-byte
-  // aligned: the fast path), else the widest width dividing HW
+  // planes of whole 16-byte chunks (every run 16-byte aligned): the fast path; odd
+  // planes read masked 16-byte covers, and a write chunk may span two channels (needs
+  // HW >= 16 / sizeof(T))
   constexpr int ue = 16 / es;
-  int ve = ue;
-  while (ve > 1 && HW % ve) ve /= 2;
-  auto kernel = onchip_kernel<T, BWD, RELU>(ve);
+  const int ve = HW % ue == 0 ? ue : 1;
+  if (ve == 1 && HW < ue) return false;
+  // the plan must not depend on RELU (the statistics-only launches use RELU = false for
+  // the forward): every instance has the same registers, so plan on the RELU = false one
+  auto kernel = onchip_kernel<T, BWD, false>(ve);
   const int64_t S = num_sms_cached();
   const int64_t smem_sm = device_attr(cudaDevAttrMaxSharedMemoryPerMultiprocessor, 233472);
   const int64_t smem_blk = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448);
   const int64_t total = (int64_t)nin * N * C * HW * es;
-  if ((double)total > env.max_frac * (double)(S * smem_sm)) return false;
+  // capped: the automatic choice (the *_local / statistics entry points); uncapped: the
+  // explicit *_fused entry points (any layer that fits in one resident wave)
+  const double max_frac = !capped ? 1.0 : es == 4 ? env.max_frac4 : env.max_frac2;
+  if ((double)total > max_frac * (double)(S * smem_sm)) return false;
   const size_t head = ((sizeof(onchip::Head) + 15) / 16) * 16;
   double best = 1e300;
   bool found = false;
@@ -988,7 +999,7 @@ bool onchip_plan_t(int64_t N, int64_t C, int64_t HW, OnchipPlan* p) {
         g.nq = (uint32_t)(ve == ue ? run / 16 : stride / 16);
         const int64_t wpc = nch >= onchip::kWarpsO ? 1 : onchip::kWarpsO / nch;
         g.wpc_log2 = (uint32_t)__builtin_ctzll(wpc);
-        g.HWv = (uint32_t)(HW / ve);
+        g.HWv = (uint32_t)(ve == ue ? HW / ue : (HW + ue - 1) / ue + 1);
         g.HWu = (uint32_t)(ve == ue ? HW / ue : 1);
         g.dhwv.init(g.HWv);
         g.dhw.init((uint32_t)HW);
@@ -1008,11 +1019,11 @@ bool onchip_plan_t(int64_t N, int64_t C, int64_t HW, OnchipPlan* p) {
 // size, the footprint within max_frac of the GPU's shared memory, one resident wave.
 template <class T, bool BWD, bool RELU>
 bool onchip_plan(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align,
-                 OnchipPlan* p) {
+                 OnchipPlan* p, bool capped = true) {
   if (!onchip_env().enabled || layout != CGBN_LAYOUT_NCHW || HW < 4) return false;
   if (align % 16 || ((uint64_t)N * C * HW * sizeof(T)) % 16) return false;
   if (validate_shape(N, C, HW, layout) != CGBN_OK) return false;
-  if (!onchip_plan_t<T, BWD, RELU>(N, C, HW, p)) return false;
+  if (!onchip_plan_t<T, BWD, RELU>(N, C, HW, p, capped)) return false;
   if (env().debug_plan)
     fprintf(stderr, "[cgbn] onchip %s N=%lld C=%lld HW=%lld -> nch=%u kc=%u grid=%u smem=%zu ve=%d\n",
             BWD ? "bwd" : "fwd", (long long)N, (long long)C, (long long)HW, p->g.nch, p->g.KC,
@@ -1026,6 +1037,7 @@ unsigned long long* g_onchip_trace = nullptr;
 template <class T, bool BWD, bool RELU>
 int launch_onchip(const OnchipPlan& p, const onchip::Args& a0, cudaStream_t st) {
   auto kernel = onchip_kernel<T, BWD, RELU>(p.ve);
+  smem_optin(kernel, (size_t)device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448));
   onchip::Args a = a0;
   a.trace = g_onchip_trace;
   cudaLaunchConfig_t cfg = {};
@@ -1058,27 +1070,28 @@ int launch_onchip(const OnchipPlan& p, const onchip::Args& a0, cudaStream_t st) 
 // Try the on-chip pass; returns 1 if launched, 0 if not eligible, < 0 on error.
 template <class T, bool BWD, bool RELU>
 int try_onchip_t(int64_t N, int64_t C, int64_t HW, int layout, uintptr_t align,
-                 const onchip::Args& a, cudaStream_t st) {
+                 const onchip::Args& a, cudaStream_t st, bool capped) {
   OnchipPlan p;
-  if (!onchip_plan<T, BWD, RELU>(N, C, HW, layout, align, &p)) return 0;
+  if (!onchip_plan<T, BWD, RELU>(N, C, HW, layout, align, &p, capped)) return 0;
   const int rc = launch_onchip<T, BWD, RELU>(p, a, st);
   return rc == CGBN_OK ? 1 : -rc;
 }
 
 template <bool BWD>
 int try_onchip(int act, bool relu, int64_t N, int64_t C, int64_t HW, int layout,
-               uintptr_t align, const onchip::Args& a, cudaStream_t st) {
+               uintptr_t align, const onchip::Args& a, cudaStream_t st, bool capped = true) {
   CGBN_ROUTED(act);
-  return relu ? try_onchip_t<TuAct, BWD, true>(N, C, HW, layout, align, a, st)
-              : try_onchip_t<TuAct, BWD, false>(N, C, HW, layout, align, a, st);
+  return relu ? try_onchip_t<TuAct, BWD, true>(N, C, HW, layout, align, a, st, capped)
+              : try_onchip_t<TuAct, BWD, false>(N, C, HW, layout, align, a, st, capped);
 }
 
 template <bool BWD>
-bool onchip_supported(int act, bool relu, int64_t N, int64_t C, int64_t HW, int layout) {
+bool onchip_supported(int act, bool relu, int64_t N, int64_t C, int64_t HW, int layout,
+                      bool capped) {
   if (act != CGBN_TU_ACT) return false;
   OnchipPlan p;
-  return relu ? onchip_plan<TuAct, BWD, true>(N, C, HW, layout, 0, &p)
-              : onchip_plan<TuAct, BWD, false>(N, C, HW, layout, 0, &p);
+  return relu ? onchip_plan<TuAct, BWD, true>(N, C, HW, layout, 0, &p, capped)
+              : onchip_plan<TuAct, BWD, false>(N, C, HW, layout, 0, &p, capped);
 }
 
 #define CGBN_REQUIRE(cond, ...) \

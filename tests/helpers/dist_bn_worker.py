@@ -60,6 +60,19 @@ def main():
     mean, loss = cg.world_mean_allreduce(h, grads, loss=float(rank))
     res["world_mean_w"] = mean["w"].cpu().numpy()
     res["world_mean_loss"] = np.array(loss)
+    # the same step bucketed and overlapped on a side stream (GradBuckets)
+    more = {f"g{i}": torch.randn(40 + i, device=dev, dtype=torch.float64,
+                                 generator=torch.Generator(device=dev).manual_seed(rank * 10 + i))
+            for i in range(6)}
+    more["w"] = grads["w"]
+    flat_mean, flat_loss = cg.world_mean_allreduce(h, more, loss=float(rank))
+    gb = cg.GradBuckets(h, bucket_bytes=512, dtype=torch.float64)
+    for k in reversed(sorted(more)):
+        gb.add(k, more[k])
+    bmean, bloss = gb.finish(loss=float(rank))
+    res["buckets_issued"] = np.array(gb.buckets_issued)
+    res["buckets_equal"] = np.array(all(torch.equal(bmean[k], flat_mean[k]) for k in more)
+                                    and bloss == flat_loss)
     np.savez(os.path.join(out, f"rank{rank}.npz"), **res)
     dist.barrier()
     dist.destroy_process_group()

@@ -149,3 +149,61 @@ def test_sharded_allreduce_transport(world):
             want = want + x
         for d in out:
             assert np.array_equal(d[n], want), (n, d["rank"])
+
+
+def _bucket_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_1711_07240_b200 as cg
+
+        def cpu_reduce(h, scope, v):  # ascending-rank fold of the exchanged rows
+            parts, _ = h.exchange(scope, "allreduce", v)
+            acc = parts[0].clone()
+            for p in parts[1:]:
+                acc = acc + p
+            return acc
+
+        h = cg.DistHandle(validate=True)
+        rng = np.random.default_rng(7 + rank)
+        grads = {f"l{i}.{k}": torch.from_numpy(rng.standard_normal(n).astype(np.float32))
+                 for i, n in enumerate((5, 300, 17, 1024, 3)) for k in ("gamma", "beta")}
+        gb = cg.GradBuckets(h, bucket_bytes=2048, dtype=torch.float32, reduce_fn=cpu_reduce)
+        for name in reversed(list(grads)):  # backward order
+            gb.add(name, grads[name])
+        mean, loss = gb.finish(loss=float(rank) + 0.5)
+        # the trainer's flat step on the same gradients (sorted keys, one vector)
+        keys = sorted(grads)
+        flat = torch.cat([grads[k] for k in keys] + [torch.tensor([float(rank) + 0.5])])
+        fm = cpu_reduce(h, cg.SCOPE_WORLD, flat) / world
+        off, ref = 0, {}
+        for k in keys:
+            ref[k] = fm[off:off + grads[k].numel()]
+            off += grads[k].numel()
+        q.put({"rank": rank, "buckets": gb.buckets_issued,
+               "equal": all(torch.equal(mean[k], ref[k]) for k in keys),
+               "loss": loss, "ref_loss": float(fm[-1])})
+        dist.destroy_process_group()
+    except Exception as exc:  # noqa: BLE001
+        q.put({"rank": rank, "error": repr(exc)})
+
+
+def test_grad_buckets_equal_flat_world_mean():
+    """GradBuckets (trainer.py:419-428 bucketed): several buckets, each
+    allreduced as it fills, give bitwise the flat world-mean step's gradients and loss."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+    for d in out:
+        assert "error" not in d, d
+        assert d["buckets"] >= 3 and d["equal"]
+        assert d["loss"] == d["ref_loss"] == 1.0

@@ -66,3 +66,4 @@ def test_processes_match_oracle(world, g, tmp_path):
         assert np.array_equal(got[r]["world_mean_w"], got[0]["world_mean_w"])
         assert np.allclose(got[r]["world_mean_w"], want, rtol=0, atol=1e-15)
         assert float(got[r]["world_mean_loss"]) == sum(range(world)) / world
+        assert bool(got[r]["buckets_equal"]) and int(got[r]["buckets_issued"]) >= 2

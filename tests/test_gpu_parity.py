@@ -469,9 +469,8 @@ def test_misaligned_view_is_realigned(cl):
     dev = _dev()
     rng = np.random.default_rng(77)
     if cl:
-        base = torch.from_numpy(rng.standard_normal((5, 3, 4, 4)).astype(np.float32)).to(dev)
-        base = base.contiguous(memory_format=torch.channels_last)
-        x = base.view(-1)[1:1 + 4 * 3 * 16].view(4, 4, 4, 3).permute(0, 3, 1, 2)
+        base = torch.from_numpy(rng.standard_normal(4 * 4 * 4 * 3 + 1).astype(np.float32))
+        x = base.to(dev)[1:].view(4, 4, 4, 3).permute(0, 3, 1, 2)  # NHWC storage
         assert x.is_contiguous(memory_format=torch.channels_last)
     else:
         base = torch.from_numpy(rng.standard_normal((9, 3)).astype(np.float32)).to(dev)

@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 from paper_1711_07240_b200 import _lib  # noqa: E402
 
-PH = ["start", "pdl_wait", "issued", "landed", "reduced", "finished", "written"]
+PH = ["start", "pdl_wait", "issued", "setup", "reduced", "finished", "written"]
 
 
 def run(shape, bwd, reps=3):
@@ -38,7 +38,7 @@ def run(shape, bwd, reps=3):
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     ws = torch.zeros(lib.cgbn_workspace_bytes(n, c, h * w, 0), dtype=torch.uint8, device=dev)
     dg, db = torch.empty(c, device=dev), torch.empty(c, device=dev)
-    tr = torch.zeros(4096 * 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(4096 * 16, dtype=torch.int64, device=dev)
     st = torch.cuda.current_stream().cuda_stream
 
     def fwd():
@@ -65,13 +65,17 @@ def run(shape, bwd, reps=3):
     e1.record()
     torch.cuda.synchronize()
     hook(None)
-    t = tr.view(-1, 8).cpu().numpy()
+    t = tr.view(-1, 16).cpu().numpy()
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
-    rel = (t[:, :7] - t0) / 1e3  # us
+    rel = (t[:, :12] - t0) / 1e3  # us
     out = {"shape": list(shape), "dir": "bwd" if bwd else "fwd", "ctas": int(len(t)),
            "event_us": e0.elapsed_time(e1) * 1e3, "span_us": float(rel[:, 6].max()),
-           "ctas_per_sm_max": int(np.bincount(t[:, 7].astype(int)).max())}
+           "ctas_per_sm_max": int(np.bincount(t[:, 15].astype(int)).max())}
+    for q in range(4):
+        col = rel[:, 8 + q][t[:, 8 + q] > 0]
+        if len(col):
+            out[f"group{q}"] = [round(float(np.percentile(col, v)), 2) for v in (0, 50, 100)]
     for k, name in enumerate(PH):
         col = rel[:, k]
         out[name] = [round(float(np.percentile(col, q)), 2) for q in (0, 50, 100)]
