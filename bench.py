@@ -333,8 +333,8 @@ def _layer_paths(lib, shapes, lay):
     fwd, bwd = [], []
     for s in shapes:
         n, c, h, w = s
-        fwd.append(bool(lib.cgbn_fused_supported(n, c, h * w, lay, 0)))
-        bwd.append(bool(lib.cgbn_fused_supported(n, c, h * w, lay, 1)))
+        fwd.append(bool(lib.cgbn_onchip_selected(n, c, h * w, lay, 0)))
+        bwd.append(bool(lib.cgbn_onchip_selected(n, c, h * w, lay, 1)))
     return fwd, bwd
 
 
@@ -486,8 +486,12 @@ def bench_parity(cg, torch, shapes, xs, dys, states, dev, esize):
         cand = [i for i, s in enumerate(shapes) if s[2] == hw and i not in pick]
         if cand:
             pick.append(max(cand, key=lambda i: numel(shapes[i])))
-    tol_y = 1e-5 if esize == 4 else 1e-2
-    tol_dx = 1e-4 if esize == 4 else 1e-2
+    # 16-bit activations: y and dx carry one rounding to the activation dtype
+    # (tests/test_gpu_half.py OUT_TOL)
+    if esize == 4:
+        tol_y, tol_dx = 1e-5, 1e-4
+    else:
+        tol_y = tol_dx = 8e-3 if xs[0].dtype == torch.bfloat16 else 1.5e-3
     worst = {}
     layers = []
     h = cg.SoloHandle(dev)
@@ -1062,39 +1066,53 @@ def run_gpu_arm(args):
         ms_e = statistics.median(ms_e_steps)
         # the PCIe floor of the same step: the same H2D and D2H copies on the same two
         # streams with no compute between them (both directions concurrently)
-        def copy_only_step():
+        def copy_only_step(h2d=True, d2h=True):
             comp = torch.cuda.current_stream(dev)
             s_in.wait_stream(comp)
             s_out.wait_stream(comp)
-            with torch.cuda.stream(s_in):
-                for i in range(n_l):
-                    dx_in[i].copy_(hx[i], non_blocking=True)
-                for i in range(n_l - 1, -1, -1):
-                    ddy_in[i].copy_(hdy[i], non_blocking=True)
-            with torch.cuda.stream(s_out):
-                for i in range(n_l):
-                    hy[i].copy_(xs[i], non_blocking=True)
-                for i in range(n_l - 1, -1, -1):
-                    hdx[i].copy_(dys[i], non_blocking=True)
+            if h2d:
+                with torch.cuda.stream(s_in):
+                    for i in range(n_l):
+                        dx_in[i].copy_(hx[i], non_blocking=True)
+                    for i in range(n_l - 1, -1, -1):
+                        ddy_in[i].copy_(hdy[i], non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s_out):
+                    for i in range(n_l):
+                        hy[i].copy_(xs[i], non_blocking=True)
+                    for i in range(n_l - 1, -1, -1):
+                        hdx[i].copy_(dys[i], non_blocking=True)
             comp.wait_stream(s_in)
             comp.wait_stream(s_out)
 
-        copy_only_step()
-        torch.cuda.synchronize()
-        a0.record()
-        for _ in range(k_e):
-            copy_only_step()
-        a1.record()
-        torch.cuda.synchronize()
-        ms_copy = a0.elapsed_time(a1) / k_e
+        def time_copies(**kw):
+            copy_only_step(**kw)
+            torch.cuda.synchronize()
+            a0.record()
+            for _ in range(k_e):
+                copy_only_step(**kw)
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / k_e
+
+        # the PCIe floor of the step: each direction alone, and both at once (the e2e
+        # step overlaps them, so max(h2d, d2h) is the bound it could reach)
+        ms_h2d = time_copies(d2h=False)
+        ms_d2h = time_copies(h2d=False)
+        ms_both = time_copies()
+        ms_copy = max(ms_h2d, ms_d2h)
         if world > 1:
             tt = torch.tensor([ms_e], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms_e = float(tt.item())
         e2e = {"value": step_bytes_rank * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
                "copy_only_ms_per_step": ms_copy,
+               "copy_ms": {"h2d_alone": ms_h2d, "d2h_alone": ms_d2h, "both_at_once": ms_both},
                "pcie_gbs_per_direction": 2 * esize * sum(elems) / (ms_copy * 1e-3) / 1e9,
                "frac_of_copy_bound": ms_copy / ms_e,
+               "copy_bound": "max(H2D alone, D2H alone) of the step's bytes on the same "
+                             "streams: the time a step whose copies fully overlap each other "
+                             "and the compute would take",
                "h2d_bytes_per_step": 2 * esize * sum(elems),
                "d2h_bytes_per_step": 2 * esize * sum(elems),
                "ms_per_step": ms_e, "ms_mean": sum(ms_e_steps) / k_e, "steps": k_e,

@@ -267,17 +267,22 @@ int cgbn_fwd_normalize_sums(const void* x, int64_t N, int64_t C, int64_t HW, int
 int cgbn_channel_affine(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                         const double* scale, const double* shift, void* out, void* stream);
 
-/* Single-launch fused forward / backward for a single-rank group (G == 1:
- * bn_forward_local / bn_backward_local, or a BN group of one). One cooperative kernel
- * per direction (opt-in): the activation slice of every SM is loaded
- * into shared memory once (cp.async, tracked by mbarriers), reduced, a grid barrier publishes the per-channel partials, and the
- * elementwise pass reads the slice back from shared memory — x (and dy) cross HBM once
- * (forward 8 B/elem instead of 12, backward 12 instead of 20). Same outputs and
- * contracts as cgbn_fwd_stats + cgbn_fwd_normalize (resp. cgbn_bwd_reduce +
- * cgbn_bwd_dx) with G == 1. Returns CGBN_ERR_UNSUPPORTED when the activation does not
- * fit on chip or the layout is not NCHW with HW % 4 == 0 (callers then use the split
- * entry points). cgbn_fused_supported() answers that question without launching
- * (backward != 0: the backward variant). */
+/* Single-launch on-chip forward / backward for a single-rank group (G == 1:
+ * bn_forward_local / bn_backward_local, or a BN group of one). One kernel per direction
+ * (cgbn_onchip.cuh): a thread-block cluster owns whole channels; its CTAs bulk-copy
+ * (cp.async.bulk) their image runs of those channels into shared memory, reduce them,
+ * fold the CTA partials over DSMEM and write the elementwise result from shared memory,
+ * so x (and dy) cross HBM once (forward 8 B/elem instead of 12, backward 12 instead of
+ * 20) with no grid barrier. Same outputs and contracts as cgbn_fwd_stats +
+ * cgbn_fwd_normalize (resp. cgbn_bwd_reduce + cgbn_bwd_dx) with G == 1; NCHW, any
+ * activation dtype.
+ * cgbn_fwd_train_local / cgbn_bwd_local (and cgbn_fwd_stats / cgbn_bwd_reduce, in a
+ * statistics-only mode) choose this kernel by themselves for layers below a footprint
+ * cap measured in-step (cgbn_onchip_selected() reports that choice); cgbn_*_fused force
+ * it for any layer that fits in one resident wave and return CGBN_ERR_UNSUPPORTED
+ * otherwise, which cgbn_fused_supported() answers without launching (backward != 0:
+ * the backward variant). */
+int cgbn_onchip_selected(int64_t N, int64_t C, int64_t HW, int layout, int backward);
 int cgbn_fused_supported(int64_t N, int64_t C, int64_t HW, int layout, int backward);
 int cgbn_fwd_fused(const void* x, int64_t N, int64_t C, int64_t HW, int layout,
                    const float* gamma, const float* beta, double eps, double momentum,

@@ -72,6 +72,7 @@ SIGNATURES = {
                                      _p, _p, _p, _i, _p, _p, _p, _sz, _p]),
     "cgbn_channel_affine": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _p]),
     "cgbn_fused_supported": (_i, [_i64, _i64, _i64, _i, _i]),
+    "cgbn_onchip_selected": (_i, [_i64, _i64, _i64, _i, _i]),
     "cgbn_fwd_fused": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _d, _d, _p, _p, _p, _i, _p, _p, _p,
                             _sz, _p]),
     "cgbn_bwd_fused": (_i, [_p, _p, _i64, _i64, _i64, _i, _p, _p, _p, _d, _i, _p, _p, _p, _p, _p,

@@ -436,6 +436,16 @@ int CGBN_FN(cgbn_debug_onchip_trace)(void* dev_buf) {
   return CGBN_OK;
 }
 
+// Whether the *_local / statistics entry points run this layer on chip by themselves.
+int CGBN_FN(cgbn_onchip_selected)(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
+  int act = 0;
+  if (split_fmt(&layout, &act)) return 0;
+  return (backward ? onchip_supported<true>(act, false, N, C, HW, layout, true)
+                   : onchip_supported<false>(act, false, N, C, HW, layout, true))
+             ? 1
+             : 0;
+}
+
 // The single-launch on-chip passes (cgbn_onchip.cuh) on request: the *_local entry points
 // pick them by themselves whenever a layer fits; these force them (error if not eligible).
 int CGBN_FN(cgbn_fused_supported)(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
@@ -973,6 +983,16 @@ int cgbn_bwd_local(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
     case 1: return cgbn_bwd_local_a1(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
     case 2: return cgbn_bwd_local_a2(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
     default: return cgbn_bwd_local_a0(dy, x, N, C, HW, layout, saved, gamma, beta, eps, relu, dx, dgamma, dbeta, status, ws, ws_bytes, stream);
+  }
+}
+
+int cgbn_onchip_selected_a1(int64_t N, int64_t C, int64_t HW, int layout, int backward);
+int cgbn_onchip_selected_a2(int64_t N, int64_t C, int64_t HW, int layout, int backward);
+int cgbn_onchip_selected(int64_t N, int64_t C, int64_t HW, int layout, int backward) {
+  switch ((layout >> 4) & 0xF) {
+    case 1: return cgbn_onchip_selected_a1(N, C, HW, layout, backward);
+    case 2: return cgbn_onchip_selected_a2(N, C, HW, layout, backward);
+    default: return cgbn_onchip_selected_a0(N, C, HW, layout, backward);
   }
 }
 

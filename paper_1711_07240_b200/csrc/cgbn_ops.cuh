@@ -416,21 +416,19 @@ struct BwdOp : PushSlot<PUSH> {
   }
   __device__ __forceinline__ void acc(const Regs& r, double& a, double& b) const {
     if constexpr (sizeof(T) == 2 && VEC >= 4 && !RELU) {
-      // 16-bit activations: fp32 partials of the unit's VEC terms, one fp64 add each
-      // (see StatsOp::acc). x - mean uses the fp32 split mean = mh + ml, so the centring
-      // keeps ~2^-24 relative accuracy even when |mean| >> the spread.
-      const float mh = (float)mean;
-      const float ml = (float)(mean - (double)mh);
-      float s = 0.f, q = 0.f;
+      // 16-bit activations: sum g in an fp32 partial of the unit's VEC terms (bf16 / fp16
+      // values add exactly or nearly so), one fp64 add; sum g*(x - mean) per element in
+      // fp64 as for fp32 activations. (An fp32 partial of g*(x - mean) left ~1e-6
+      // absolute error on dgamma, 5e-4 relative on near-zero channels of [32,2048,7,7].)
+      float s = 0.f;
 #pragma unroll
       for (int k = 0; k < VEC; ++k) {
         if (masked_vm(VM) && !((r.m >> k) & 1u)) continue;
         const float gk = r.g.get(k);
         s += gk;
-        q = __fmaf_rn(gk, (r.x.get(k) - mh) - ml, q);
+        b = __fma_rn((double)gk, (double)r.x.get(k) - mean, b);
       }
       a += (double)s;
-      b += (double)q;
       return;
     }
 #pragma unroll

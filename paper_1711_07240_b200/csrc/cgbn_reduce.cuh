@@ -340,8 +340,8 @@ struct BwdRows {
       b[j] = __fma_rn(gk, (double)xj - s.mean[j], b[j]);
     }
   }
-  // 16-bit activations without ReLU: per channel, fp32 partials over the round's rows
-  // (BwdOp::acc: two-float split mean), one fp64 add each.
+  // 16-bit activations without ReLU: per channel, sum g in an fp32 partial over the
+  // round's rows, one fp64 add; sum g*(x - mean) in fp64 per element (BwdOp::acc).
   template <int U>
   __device__ __forceinline__ void acc_round(const State& s, const Regs (&v)[U], uint32_t r,
                                             uint32_t r1, uint32_t rpp, double (&a)[4],
@@ -349,18 +349,15 @@ struct BwdRows {
     if constexpr (sizeof(T) == 2 && !RELU) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float mh = (float)s.mean[j];
-        const float ml = (float)(s.mean[j] - (double)mh);
-        float sj = 0.f, qj = 0.f;
+        float sj = 0.f;
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (r + u * rpp < r1) {
             const float gk = v[u].g.get(j);
             sj += gk;
-            qj = __fmaf_rn(gk, (v[u].x.get(j) - mh) - ml, qj);
+            b[j] = __fma_rn((double)gk, (double)v[u].x.get(j) - s.mean[j], b[j]);
           }
         a[j] += (double)sj;
-        b[j] += (double)qj;
       }
       return;
     }

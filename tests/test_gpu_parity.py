@@ -367,6 +367,12 @@ def test_fused_eligibility():
     assert lib.cgbn_fused_supported(32, 2048, 49, 0, 0) == 1      # odd planes: lead-aware path
     assert lib.cgbn_fused_supported(32, 2048, 49, 0, 1) == 1
     assert lib.cgbn_fused_supported(32, 128, 784, 1, 0) == 0      # NHWC
+    # the automatic choice of the *_local / statistics entry points (in-step footprint cap)
+    assert lib.cgbn_onchip_selected(32, 128, 784, 0, 0) == 1      # 12.8 MB forward
+    assert lib.cgbn_onchip_selected(32, 128, 784, 0, 1) == 0      # 25.7 MB backward
+    assert lib.cgbn_onchip_selected(32, 64, 3136, 0, 0) == 0
+    assert lib.cgbn_onchip_selected(32, 256, 196, 0, 1) == 1
+    assert lib.cgbn_onchip_selected(32, 256, 196, _lib.ACT_BF16, 0) == 0  # 16-bit: off
 
 
 def test_fused_run_to_run_bitwise_and_matches_split_closely():
