@@ -877,34 +877,49 @@ def run_gpu_arm(args):
     torch.cuda.synchronize()
 
     use_graph = not args.no_graph
-    graph = None
-    graphs = []
+    graph = None  # the one-step graph (its kernel nodes are counted)
+    timed_graph = None  # rotating sets: one graph of all K timed steps
     graph_note = "cuda graph of the whole step" if use_graph else "eager"
     if use_graph:
         try:
-            for k, (xs_k, dys_k) in enumerate(sets):
-                try:  # keep the cudaGraph_t after instantiation (kernel-node count)
-                    gk = torch.cuda.CUDAGraph(keep_graph=(k == 0))
-                except TypeError:
-                    gk = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gk):
-                    step(xs_k, dys_k)
-                graphs.append(gk)
-            graph = graphs[0]
-            for gk in graphs:
-                gk.replay()
-            graph.replay()
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap):  # the capture stream's workspace / status word
+                step()                    # exist before capture (no fill kernels inside)
+            torch.cuda.current_stream().wait_stream(cap)
+            torch.cuda.synchronize()
+            try:  # keep the cudaGraph_t after instantiation (kernel-node count)
+                graph = torch.cuda.CUDAGraph(keep_graph=True)
+            except TypeError:
+                graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                step()
+            if n_sets > 1:
+                # small working sets: the K timed steps cycle through the rotating input
+                # sets inside ONE graph (one graph launch per timed region: a graph
+                # launch per ~10 us step would make the host the bound)
+                timed_graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(timed_graph, stream=cap):
+                    for k in range(args.steps):
+                        step(*sets[k % n_sets])
+                graph_note = (f"cuda graph of the {args.steps} timed steps over {n_sets} "
+                              "rotating input sets")
+            for _ in range(2):
+                (timed_graph or graph).replay()
             torch.cuda.synchronize()
         except Exception as exc:  # noqa: BLE001 - e.g. a collective that cannot be captured
             print(f"[bench] graph capture failed ({exc!r}); timing eager steps", file=sys.stderr)
-            graph, graphs = None, []
+            graph = timed_graph = None
             graph_note = "eager (graph capture failed)"
             torch.cuda.synchronize()
             barrier()
 
     def run_once(k=0):
-        if graph is not None:
-            graphs[k % len(graphs)].replay()
+        if timed_graph is not None:
+            if k == 0:
+                timed_graph.replay()  # all K steps
+        elif graph is not None:
+            graph.replay()
         else:
             step(*sets[k % len(sets)])
 
@@ -955,7 +970,21 @@ def run_gpu_arm(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks \
         else "fallback 6.65 TB/s (B200_PROFILING.md)"
-    dom = max(kern, key=lambda k: kern[k]["ms_per_step"]) if kern else None
+    # the dominant family: by its share of the step in the committed ncu launch list
+    # (profiles/r2_traffic.json: in-step, where L2 reuse between a reduction and its
+    # elementwise pass counts), else by the direct family time
+    dom, dom_by = None, None
+    if kern:
+        shares = {}
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic.json")))["families"]
+            shares = {k: tr[k]["ncu_share"] for k in kern if k in tr}
+        except Exception:  # noqa: BLE001
+            pass
+        if args.layout == "nchw" and args.act == "f32" and shares:
+            dom, dom_by = max(shares, key=shares.get), "ncu in-step share (profiles/r2_traffic.json)"
+        else:
+            dom, dom_by = max(kern, key=lambda k: kern[k]["ms_per_step"]), "direct family time"
     roofline = None
     if dom:
         fam = kern[dom]
@@ -972,7 +1001,7 @@ def run_gpu_arm(args):
                     "alg_bytes_per_launch": fam["alg_bytes_per_launch"],
                     "alg_bytes_per_elem": fam["bytes_per_elem"],
                     "launches": fam["launches_per_step"], "us_per_launch": t_launch * 1e6,
-                    "peak_source": peak_src, "timing": timing_mode,
+                    "peak_source": peak_src, "timing": timing_mode, "dominant_by": dom_by,
                     "note": ("achieved = the family's algorithmic bytes per launch (on-chip "
                              "passes: their compulsory 8 / 12 B per element; split passes: "
                              "SURVEY 8d's 4 / 8 / 8 / 12) / its directly timed, L2-cold "
