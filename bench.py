@@ -622,15 +622,26 @@ def producer_profile(cg, torch, dev, hbm_peak, batch=32, sets=3, iters=10):
             for x, st in zip(xs, sts):
                 cg.bn_forward_local(P.conv1x1(x, wt), st)
 
+        w4 = wt[:, :, None, None]
         t_conv, t_f, t_s = timed(conv), timed(fused), timed(split)
+        # the library baseline: cuDNN's conv (torch conv2d, bf16 out) + our BN forward, and
+        # our fused conv with the same bf16 output
+        t_cd = timed(lambda: [torch.nn.functional.conv2d(x, w4) for x in xs])
+        t_cds = timed(lambda: [cg.bn_forward_local(torch.nn.functional.conv2d(x, w4), st)
+                               for x, st in zip(xs, sts)])
+        t_f16 = timed(lambda: [P.conv1x1_bn_forward_local(x, wt, st, out_dtype=torch.bfloat16)
+                               for x, st in zip(xs, sts)])
         cb = batch * h * w * (2 * cin + 4 * cout) + 2 * cin * cout
         layers.append({"shape": [batch, cin, cout, h, w], "count": cnt, "conv_us": t_conv,
                        "conv_hbm_frac": cb / t_conv / 1e3 / hbm_peak,
-                       "fused_fwd_us": t_f, "split_fwd_us": t_s})
+                       "fused_fwd_us": t_f, "split_fwd_us": t_s, "cudnn_conv_us": t_cd,
+                       "cudnn_split_fwd_us": t_cds, "fused_bf16_fwd_us": t_f16})
         tot["fused_us"] += cnt * t_f
         tot["split_us"] += cnt * t_s
         tot["conv_us"] += cnt * t_conv
         tot["conv_bytes"] += cnt * cb
+        tot["cudnn_split_us"] = tot.get("cudnn_split_us", 0.0) + cnt * t_cds
+        tot["fused_bf16_us"] = tot.get("fused_bf16_us", 0.0) + cnt * t_f16
         del xs, sts
     # channels_last (NHWC x and z): 1x1 and 3x3 over all stages
     cl = torch.channels_last
@@ -647,13 +658,26 @@ def producer_profile(cg, torch, dev, hbm_peak, batch=32, sets=3, iters=10):
         t_f = timed(lambda: [fused_fn(x, wt, st, stride=sd) for x, st in zip(xs, sts)])
         t_s = timed(lambda: [cg.bn_forward_local(conv(x, wt, stride=sd), st)
                              for x, st in zip(xs, sts)])
+        pad = k // 2
+        t_cd = timed(lambda: [torch.nn.functional.conv2d(x, wt, stride=sd, padding=pad)
+                              for x in xs])
+        t_cds = timed(lambda: [cg.bn_forward_local(
+            torch.nn.functional.conv2d(x, wt, stride=sd, padding=pad), st)
+            for x, st in zip(xs, sts)])
+        t_f16 = timed(lambda: [fused_fn(x, wt, st, stride=sd, out_dtype=torch.bfloat16)
+                               for x, st in zip(xs, sts)])
         flops = 2.0 * batch * (h // sd) * (w // sd) * cout * cin * k * k
         nlayers.append({"k": k, "stride": sd, "shape": [batch, cin, cout, h, w], "count": cnt,
                         "conv_us": t_conv, "conv_tflops": flops / t_conv / 1e6,
-                        "fused_fwd_us": t_f, "split_fwd_us": t_s})
+                        "fused_fwd_us": t_f, "split_fwd_us": t_s, "cudnn_conv_us": t_cd,
+                        "cudnn_conv_tflops": flops / t_cd / 1e6, "cudnn_split_fwd_us": t_cds,
+                        "fused_bf16_fwd_us": t_f16})
         ntot["fused_us"] += cnt * t_f
         ntot["split_us"] += cnt * t_s
         ntot["conv_us"] += cnt * t_conv
+        ntot["cudnn_split_us"] = ntot.get("cudnn_split_us", 0.0) + cnt * t_cds
+        ntot["fused_bf16_us"] = ntot.get("fused_bf16_us", 0.0) + cnt * t_f16
+        ntot["cudnn_conv_us"] = ntot.get("cudnn_conv_us", 0.0) + cnt * t_cd
         del xs, sts
     return {
         "what": "conv (tcgen05, bf16 x/w, fp32 z) + BN forward; fused = conv epilogue "
@@ -662,6 +686,11 @@ def producer_profile(cg, torch, dev, hbm_peak, batch=32, sets=3, iters=10):
         "layers": "ResNet-50 stage 1-2 1x1-conv->BN layers (NCHW), batch 32, weighted by count",
         "fused_fwd_ms": tot["fused_us"] / 1e3, "split_fwd_ms": tot["split_us"] / 1e3,
         "speedup": tot["split_us"] / tot["fused_us"],
+        "vs_cudnn": {"what": "bf16 z: our fused conv+BN forward vs cuDNN's conv (torch conv2d) "
+                             "followed by our BN forward",
+                     "fused_bf16_fwd_ms": tot["fused_bf16_us"] / 1e3,
+                     "cudnn_split_fwd_ms": tot["cudnn_split_us"] / 1e3,
+                     "speedup": tot["cudnn_split_us"] / tot["fused_bf16_us"]},
         "conv_gbs": tot["conv_bytes"] / tot["conv_us"] / 1e3,
         "conv_hbm_frac": tot["conv_bytes"] / tot["conv_us"] / 1e3 / hbm_peak,
         "per_layer": layers,
@@ -672,6 +701,10 @@ def producer_profile(cg, torch, dev, hbm_peak, batch=32, sets=3, iters=10):
             "fused_fwd_ms": ntot["fused_us"] / 1e3, "split_fwd_ms": ntot["split_us"] / 1e3,
             "speedup": ntot["split_us"] / ntot["fused_us"],
             "conv_ms": ntot["conv_us"] / 1e3,
+            "vs_cudnn": {"fused_bf16_fwd_ms": ntot["fused_bf16_us"] / 1e3,
+                         "cudnn_split_fwd_ms": ntot["cudnn_split_us"] / 1e3,
+                         "cudnn_conv_ms": ntot["cudnn_conv_us"] / 1e3,
+                         "speedup": ntot["cudnn_split_us"] / ntot["fused_bf16_us"]},
             "per_layer": nlayers,
         },
     }
@@ -1129,7 +1162,7 @@ def run_gpu_arm(args):
         ms_h2d = time_copies(d2h=False)
         ms_d2h = time_copies(h2d=False)
         ms_both = time_copies()
-        ms_copy = max(ms_h2d, ms_d2h)
+        ms_copy = ms_both
         if world > 1:
             tt = torch.tensor([ms_e], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -1139,9 +1172,10 @@ def run_gpu_arm(args):
                "copy_ms": {"h2d_alone": ms_h2d, "d2h_alone": ms_d2h, "both_at_once": ms_both},
                "pcie_gbs_per_direction": 2 * esize * sum(elems) / (ms_copy * 1e-3) / 1e9,
                "frac_of_copy_bound": ms_copy / ms_e,
-               "copy_bound": "max(H2D alone, D2H alone) of the step's bytes on the same "
-                             "streams: the time a step whose copies fully overlap each other "
-                             "and the compute would take",
+               "frac_of_per_direction_bound": max(ms_h2d, ms_d2h) / ms_e,
+               "copy_bound": "the step's H2D and D2H bytes copied at once on the same two "
+                             "streams with no compute (both directions share the link: "
+                             "measured slower than either alone, see copy_ms)",
                "h2d_bytes_per_step": 2 * esize * sum(elems),
                "d2h_bytes_per_step": 2 * esize * sum(elems),
                "ms_per_step": ms_e, "ms_mean": sum(ms_e_steps) / k_e, "steps": k_e,

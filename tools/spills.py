@@ -1,12 +1,18 @@
 #!/usr/bin/env python3
-"""Summarise csrc/ptxas.log: registers and spill bytes per kernel (demangled).
-    python tools/spills.py [substring]"""
+"""Summarise the ptxas logs of the build (csrc/ptxas_a0/a1/a2.log: the fp32, bf16 and fp16
+units; ptxas_conv.log): registers and spill bytes per kernel (demangled).
+    python tools/spills.py [substring] [--spills]"""
+import glob
 import re
 import subprocess
 import sys
 
-log = open("paper_1711_07240_b200/csrc/ptxas.log").read().splitlines()
-flt = sys.argv[1] if len(sys.argv) > 1 else ""
+log = []
+for f in sorted(glob.glob("paper_1711_07240_b200/csrc/ptxas_*.log")):
+    log += open(f).read().splitlines()
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+only_spills = "--spills" in sys.argv
+flt = args[0] if args else ""
 cur = None
 rows = []
 for line in log:
@@ -28,5 +34,5 @@ names = subprocess.run(["c++filt"], input="\n".join(r["name"] for r in rows), te
 for r, n in zip(rows, names):
     n = n.replace("(anonymous namespace)::", "")
     n = n.split("(")[0]
-    if flt in n:
+    if flt in n and (r["spill"] or not only_spills):
         print(f"{r['regs']:4d} regs {r['spill']:4d} B spill  {n}")
