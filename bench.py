@@ -650,7 +650,9 @@ def producer_profile(cg, torch, dev, hbm_peak, batch=32, sets=3, iters=10):
     for k, sd, cin, cout, h, w, cnt in PRODUCER_LAYERS_NHWC:
         xs = [torch.randn(batch, cin, h, w, device=dev).to(torch.bfloat16).contiguous(
             memory_format=cl) for _ in range(sets)]
-        wt = (torch.randn(cout, cin, k, k, device=dev) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+        # channels_last weights too, as model.to(memory_format=channels_last) leaves them
+        wt = (torch.randn(cout, cin, k, k, device=dev) / (k * k * cin) ** 0.5).to(
+            torch.bfloat16).contiguous(memory_format=cl)
         sts = [cg.BNLayerState.create(cout, device=dev) for _ in range(sets)]
         conv = P.conv3x3 if k == 3 else P.conv1x1
         fused_fn = P.conv3x3_bn_forward_local if k == 3 else P.conv1x1_bn_forward_local

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CGBN_ABI_VERSION 6
+#define CGBN_ABI_VERSION 7
 
 #define CGBN_LAYOUT_NCHW 0
 #define CGBN_LAYOUT_NHWC 1
@@ -293,7 +293,7 @@ int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
                    int relu, void* dx, float* dgamma, float* dbeta, unsigned* status, void* ws,
                    size_t ws_bytes, void* stream);
 
-/* Producer fusion (ABI v6). The layer that feeds a BN in the
+/* Producer fusion (ABI v7). The layer that feeds a BN in the
  * reference model is a GEMM-shaped convolution (model.py:235-242, out = cols @ W^T + b)
  * whose output _train_forward immediately re-reads for its statistics (batchnorm.py:118,
  * channel_sum, tensor.py:143-153). cgbn_conv1x1_stats computes the pointwise (1x1) case
@@ -335,8 +335,9 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
  * 2, any H and W; z is [N][Ho][Wo][Cout] with Ho = (H + 2 pad - ksize) / stride + 1. The
  * 3x3 and strided cases are an implicit GEMM on TMA im2col loads (taps x Cin/64 k-steps;
  * the hardware walks the output pixels, shifts each window by the tap and zero-fills
- * outside the image). w: bf16 [Cout][Cin] (ksize 1) or [9][Cout][Cin] with tap =
- * 3 * ky + kx (the reference's (Cout, Cin, 3, 3) weight permuted). Cin and Cout must be
+ * outside the image). w: bf16 [Cout][Cin] (ksize 1) or [Cout][9][Cin] with tap =
+ * 3 * ky + kx (OHWI: torch's channels_last (Cout, Cin, 3, 3) weight as it lies in memory;
+ * ABI v7 — v6 took [9][Cout][Cin]). Cin and Cout must be
  * multiples of 8. Statistics contract as cgbn_conv1x1_stats; ws: cgbn_conv_nhwc_ws_bytes
  * bytes. */
 size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W, int ksize,

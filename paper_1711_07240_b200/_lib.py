@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CGBN_LIB", os.path.join(_HERE, "libcgbn.so"))
 
 # Keep in sync with include/cgbn.h
-ABI_VERSION = 6  # CGBN_ABI_VERSION the bindings below were written for
+ABI_VERSION = 7  # CGBN_ABI_VERSION the bindings below were written for
 LAYOUT_NCHW = 0
 LAYOUT_NHWC = 1
 ACT_F32 = 0x00   # activation dtype, OR'd into the layout argument

@@ -39,15 +39,26 @@ int cgbn_internal_set_error(int code, const char* msg);
 namespace {
 
 constexpr int BM = 128;       // output channels per tile (TMEM lanes)
-constexpr int BN = 128;       // pixels per tile (TMEM columns)
 constexpr int BK = 64;        // input channels per ring stage (128 B of bf16)
 constexpr int kEpiWarps = 8;
-constexpr int kHalf = 64;                       // tile columns per epilogue warp
+constexpr int kChunk = 64;                      // tile columns per epilogue step
 constexpr uint32_t kWarpStage = 32 * 128;       // one staged box (32 rows x 128 B): 4 KB
 constexpr int kConvThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilogue warps
 constexpr uint32_t kTileA = BM * BK * 2;      // 16 KB
-constexpr uint32_t kTileB = BK * BN * 2;      // 16 KB (two 64-pixel boxes of 8 KB)
-constexpr uint32_t kStage = kTileA + kTileB;  // 32 KB
+
+// Pixel-tile width TBN (the MMA's N, TMEM columns per accumulator): 128 or 256. A wider
+// tile stages fewer weight bytes per MAC (the ring's fill rate, ~40 B/clk per SM, is what
+// bounds these convolutions), at the price of half as many tiles.
+template <int TBN>
+struct Tile {
+  static constexpr uint32_t kTileB = BK * TBN * 2;         // 16 / 32 KB
+  static constexpr uint32_t kStage = kTileA + kTileB;      // 32 / 48 KB
+  static constexpr int kStages = TBN == 128 ? 4 : 3;       // 128 / 144 KB of ring
+  static constexpr int kHalfCols = TBN / 2;                // columns per epilogue warp
+  static constexpr int kChunks = kHalfCols / kChunk;       // 1 / 2 steps per tile
+  static constexpr size_t kSmem =
+      1024 + kStages * kStage + kEpiWarps * 2 * kWarpStage + 8 * (2 * kStages + 4) + 16;
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -217,13 +228,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, A K-major, B MN-major, N, M.
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, A K-major, B MN-major (NCHW x:
-// pixels contiguous) or K-major (NHWC x: channels contiguous), N, M.
-constexpr uint32_t kIdescBase = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) |
-                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-constexpr uint32_t kIdesc = kIdescBase | (1u << 16);
-constexpr uint32_t kIdescKB = kIdescBase;
+// pixels contiguous, bit 16) or K-major (NHWC x: channels contiguous), N = TBN, M = 128.
+template <int TBN>
+__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+         ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
 
 // Layout / geometry modes of the conv kernel
 constexpr int kNCHW1 = 0;  // NCHW x and z, 1x1: pixel tiles within one image
@@ -281,31 +292,35 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 // image, so the CTAs running together share their x tiles in L2). gridDim.x is a
 // multiple of the number of channel tiles, so every tile of a CTA has the same 128
 // output channels and each epilogue thread keeps one channel for the whole kernel.
+// A tile is 128 output channels x TBN pixels (TBN = 128 or 256).
 //   warp 0        TMA: k-blocks of successive tiles through an S-stage ring, no pause
 //                 between tiles;
-//   warp 1        MMA issue into two TMEM accumulators (2 x 128 columns), so the
+//   warp 1        MMA issue into two TMEM accumulators (2 x TBN columns), so the
 //                 epilogue of tile i overlaps the loads and MMAs of tile i+1;
 //   warps 2..9    epilogue; warp w reaches TMEM lanes [32 * (w % 4), +32) and takes one
-//                 64-column half of the tile. Per 32 columns: tcgen05.ld, + bias, round to
-//                 the output type, stage the 32 rows x 128 B in the warp's own
-//                 128B-swizzled double buffer, one lane TMA-stores them; with STATS the
-//                 same registers feed the channel statistics.
+//                 TBN/2-column half of the tile in 64-column steps. Per step: tcgen05.ld,
+//                 + bias, round to the output type, stage the rows in the warp's own
+//                 double buffer, one lane TMA-stores them; with STATS the same registers
+//                 feed the channel statistics. The accumulator is handed back to the MMA
+//                 warp as soon as its last step is in registers.
 // Statistics (STATS): the shifted sums of the stored values, d = z - K with one shift K
-// per thread (the fp32 mean of its first half-tile, from a TMEM pre-pass on that tile
-// only): N, SD = sum d, SQ = sum d^2, fp64 per element (d is exact in fp64). |d| is of
-// the order of the channel's spread whatever its mean, so mean = K + SD/N and
-// M2 = SQ - SD^2/N keep the BN tolerances also for |mean| >> std.
+// per thread (the fp32 mean of its first step's values): N, SD = sum d, SQ = sum d^2,
+// fp64 per element (d is exact in fp64). |d| is of the order of the channel's spread
+// whatever its mean, so mean = K + SD/N and M2 = SQ - SD^2/N keep the BN tolerances also
+// for |mean| >> std.
 // Each (CTA, half) writes one Slot per channel; k_conv_fold merges the slots.
-template <int S, class OutT, bool STATS, int MODE>
+template <class OutT, bool STATS, int MODE, int TBN>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1x1(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmZ, const ConvArgs a) {
+  using T = Tile<TBN>;
+  constexpr int S = T::kStages;
   constexpr int kCols = OutTraits<OutT>::kCols;
-  constexpr int kBoxes = kHalf / kCols;  // staged 128-byte boxes per half-row
+  constexpr int kBoxes = kChunk / kCols;  // staged 128-byte boxes per step
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* ring = smem;                        // S x [A 16 KB | B 16 KB]
-  uint8_t* stage_out = smem + S * kStage;      // 8 warps x 2 x 4 KB (TMA store staging)
+  uint8_t* ring = smem;                        // S x [A 16 KB | B TBN x 128 B]
+  uint8_t* stage_out = smem + S * T::kStage;   // 8 warps x 2 x 4 KB (TMA store staging)
   uint64_t* full = (uint64_t*)(stage_out + kEpiWarps * 2 * kWarpStage);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;                 // [2] accumulator ready (MMA -> epilogue)
@@ -327,7 +342,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * TBN);
   if (STATS && blockIdx.x == 0 && threadIdx.x == 32 && a.header != nullptr) {
     cgbn_slots::Header h;
     h.nslots = 2 * ((gridDim.x + a.mtiles - 1) / a.mtiles);
@@ -351,20 +366,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int kTaps = MODE == kNHWC3 ? a.taps : 1;
       for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
         const int mt = tile % a.mtiles, rest = tile / a.mtiles;
-        const int p0 = (rest % a.tilesP) * BN, img = rest / a.tilesP;
+        const int p0 = (rest % a.tilesP) * TBN, img = rest / a.tilesP;
         for (int tap = 0; tap < kTaps; ++tap) {
           for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
             const uint32_t s = it % S;
             if (it >= (uint32_t)S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-            uint8_t* A = ring + s * kStage;
+            uint8_t* A = ring + s * T::kStage;
             uint8_t* B = A + kTileA;
-            mbar_expect_tx(&full[s], kStage);
+            mbar_expect_tx(&full[s], T::kStage);
             if constexpr (MODE == kNCHW1) {
               tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
-              tma_load_3d(B, &tmX, &full[s], p0, kb * BK, img);
-              tma_load_3d(B + kTileB / 2, &tmX, &full[s], p0 + 64, kb * BK, img);
+#pragma unroll
+              for (int j = 0; j < TBN / 64; ++j)  // 64-pixel boxes of 8 KB
+                tma_load_3d(B + j * 8192, &tmX, &full[s], p0 + 64 * j, kb * BK, img);
             } else if constexpr (MODE == kNHWC1) {
-              // x as [N*H*W][Cin]: 128 pixels x 64 channels, K-major like W
+              // x as [N*H*W][Cin]: TBN pixels x 64 channels, K-major like W
               tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
               tma_load_2d(B, &tmX, &full[s], kb * BK, p0);
             } else {
@@ -384,31 +400,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
+      constexpr uint32_t kId = idesc<TBN>(MODE == kNCHW1);
       uint32_t it = 0, li = 0;
       for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++li) {
         const uint32_t acc = li & 1;
         if (li >= 2) mbar_wait(&tempty[acc], ((li >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
+        const uint32_t d = tmem + acc * TBN;
         const int ksteps = (MODE == kNHWC3 ? a.taps : 1) * a.kblocks;
         for (int kb = 0; kb < ksteps; ++kb, ++it) {
           const uint32_t s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
-          const uint32_t A = smem_u32(ring + s * kStage);
+          const uint32_t A = smem_u32(ring + s * T::kStage);
           const uint32_t B = A + kTileA;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // A: K-major rows of 128 B, 8-row atoms 1024 B apart; K step = 32 B in the
-            //    row. B: MN-major, 64-pixel halves 8 KB apart (LBO), 8-channel groups
+            //    row. B: MN-major, 64-pixel blocks 8 KB apart (LBO), 8-channel groups
             //    1 KB apart (SBO); K step = 16 rows = 2 KB.
             const uint64_t ad = sdesc(A + k * 32, 16, 1024);
             if constexpr (MODE == kNCHW1) {
-              const uint64_t bd = sdesc(B + k * 2048, kTileB / 2, 1024);
-              mma_bf16(d, ad, bd, kIdesc, (kb | k) != 0);
-            } else {  // NHWC: B [128 px][64 ci] K-major, the same layout as A
+              const uint64_t bd = sdesc(B + k * 2048, 8192, 1024);
+              mma_bf16(d, ad, bd, kId, (kb | k) != 0);
+            } else {  // NHWC: B [TBN px][64 ci] K-major, the same layout as A
               const uint64_t bd = sdesc(B + k * 32, 16, 1024);
-              mma_bf16(d, ad, bd, kIdescKB, (kb | k) != 0);
+              mma_bf16(d, ad, bd, kId, (kb | k) != 0);
             }
           }
           mma_commit(&empty[s]);
@@ -435,16 +452,23 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++li) {
       const int rest = tile / a.mtiles;
       const int pt = rest % a.tilesP, img = rest / a.tilesP;
-      const int p0 = pt * BN + half * kHalf;
-      const int nvalid = max(0, min(kHalf, (MODE == kNCHW1 ? a.HW : a.M) - p0));
       const uint32_t acc = li & 1;
       mbar_wait(&tfull[acc], (li >> 1) & 1);
       tc_fence_after();
-      const uint32_t trow = tmem + acc * BN + half * kHalf + ((uint32_t)(sub * 32) << 16);
-      if (active && nvalid > 0) {
-        // the half-row's 64 values: both TMEM loads in flight, one wait
+#pragma unroll 1
+      for (int j = 0; j < T::kChunks; ++j) {
+        const int col = half * T::kHalfCols + j * kChunk;
+        const int p0 = pt * TBN + col;
+        const int nvalid = max(0, min(kChunk, (MODE == kNCHW1 ? a.HW : a.M) - p0));
+        const bool work = active && nvalid > 0;  // warp-uniform
         float v[64];
-        tmem_ld32x2(trow, v);
+        if (work)  // both 32-column TMEM loads in flight, one wait
+          tmem_ld32x2(tmem + acc * TBN + col + ((uint32_t)(sub * 32) << 16), v);
+        if (j == T::kChunks - 1) {  // the accumulator is in registers: hand it back
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        if (!work) continue;
         if (has_bias) {
 #pragma unroll
           for (int i = 0; i < 64; ++i) v[i] += bias;
@@ -452,7 +476,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
         for (int i = 0; i < 64; ++i) v[i] = OutTraits<OutT>::round(v[i]);
         if constexpr (STATS) {
-          if (!have_shift) {  // the shift: fp32 mean of this thread's first half-tile
+          if (!have_shift) {  // the shift: fp32 mean of this thread's first step
             float t[64];
 #pragma unroll
             for (int i = 0; i < 64; ++i) t[i] = i < nvalid ? v[i] : 0.f;
@@ -470,7 +494,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           double s8[8], q8[8];  // 8 independent chains (fp64 latency)
 #pragma unroll
           for (int i = 0; i < 8; ++i) s8[i] = q8[i] = 0.0;
-          if (nvalid == kHalf) {  // every half-tile but the pixel tail: no masking
+          if (nvalid == kChunk) {  // every step but the pixel tail: no masking
 #pragma unroll
             for (int i = 0; i < 64; ++i) {
               const double d = (double)v[i] - Kd;
@@ -488,14 +512,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           SD += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
           SQ += ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
         }
-        // the previous tile's stores must have finished reading the warp's buffer
+        // the previous step's stores must have finished reading the warp's buffer
         if (g > 0) {
           if (lane == 0) bulk_wait_read0();
           __syncwarp();
         }
         if constexpr (MODE == kNCHW1) {
-          // stage the half-row as 128-byte rows (fp32: 2 boxes of 32 columns; bf16: 1 box
-          // of 64), 128B swizzle: 16-byte chunk q of row r at q ^ (r & 7)
+          // stage the step as 128-byte rows (fp32: 2 boxes of 32 columns; bf16: 1 box of
+          // 64), 128B swizzle: 16-byte chunk q of row r at q ^ (r & 7)
 #pragma unroll
           for (int bx = 0; bx < kBoxes; ++bx) {
             uint8_t* buf = wbuf + bx * kWarpStage;
@@ -524,7 +548,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // warp's 32 channels (lane = channel), so each store instruction writes one
           // contiguous row (no bank conflicts without a swizzle)
 #pragma unroll
-          for (int r = 0; r < kHalf; ++r) {
+          for (int r = 0; r < kChunk; ++r) {
             if constexpr (sizeof(OutT) == 4)
               reinterpret_cast<float*>(wbuf)[r * 32 + lane] = v[r];
             else
@@ -547,8 +571,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         ++g;
         N += (double)nvalid;
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
     }
     if constexpr (STATS) {
       if (cvalid) {
@@ -562,7 +584,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+  if (warp == 1) tmem_dealloc(tmem, 2 * TBN);
 }
 
 // Slots -> this rank's forward partial [mean (C) | M2 (C) | count]. One block of 32
@@ -633,10 +655,10 @@ using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// NHWC x for the implicit GEMM: dims {C, W, H, N}; each load is 64 channels x 128 output
+// NHWC x for the implicit GEMM: dims {C, W, H, N}; each load is 64 channels x tbn output
 // pixels; the tap is the instruction's offset.
 int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int64_t H,
-                    int64_t W, int ksize, int stride, int pad) {
+                    int64_t W, int ksize, int stride, int pad, int tbn) {
   static EncodeIm2colFn fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -657,7 +679,7 @@ int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int6
   const int lower[2] = {lo, lo}, upper[2] = {hi, hi};
   const cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
-                  lower, upper, BK, BN, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  lower, upper, BK, (cuuint32_t)tbn, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -665,11 +687,7 @@ int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int6
   return CGBN_OK;
 }
 
-constexpr int kStages = 4;
-
-size_t conv_smem_bytes() {
-  return 1024 + kStages * kStage + kEpiWarps * 2 * kWarpStage + 8 * (2 * kStages + 4) + 16;
-}
+size_t conv_smem_bytes(int tbn) { return tbn == 256 ? Tile<256>::kSmem : Tile<128>::kSmem; }
 
 bool conv_pdl() {  // CGBN_NO_PDL=1 disables programmatic dependent launch (read once)
   static const bool on = getenv("CGBN_NO_PDL") == nullptr;
@@ -690,16 +708,64 @@ int num_sms() {
 }
 
 // Conv geometry: mode (kNCHW1 / kNHWC1 / kNHWC3), extents, tiles. NCHW: pixel tiles of
-// 128 within one image (tiles = channel tiles x pixel tiles x images); NHWC: pixel tiles
-// of 128 over the flattened N*H*W.
+// tbn within one image (tiles = channel tiles x pixel tiles x images); NHWC: pixel tiles
+// of tbn over the flattened N*H*W.
 struct Geo {
   int mode;
   int64_t N, Cin, Cout, H, W, HW, M;
   int ksize, stride, pad;
   int64_t Ho, Wo;
-  int tilesP, mtiles, kblocks;
+  int tbn, tilesP, mtiles, kblocks;
   int64_t tiles;
 };
+
+int conv_grid_for(int64_t mtiles, int64_t tiles) {
+  if (mtiles <= 0 || tiles <= 0) return 1;  // invalid extents: validate() reports them
+  const int sms = num_sms();
+  int64_t n = mtiles <= sms ? (int64_t)(sms / mtiles) * mtiles : mtiles;
+  return (int)std::min<int64_t>(n, tiles);
+}
+
+// CGBN_CONV_TBN=128|256 pins the pixel-tile width (read once; experiments only).
+int forced_tbn() {
+  static const int v = [] {
+    const char* e = getenv("CGBN_CONV_TBN");
+    const int t = e ? atoi(e) : 0;
+    return t == 128 || t == 256 ? t : 0;
+  }();
+  return v;
+}
+
+void set_tiles(Geo& g, int tbn) {
+  g.tbn = tbn;
+  g.tilesP = (int)(((g.mode == kNCHW1 ? g.HW : g.M) + tbn - 1) / tbn);
+  g.tiles = (int64_t)g.mtiles * g.tilesP * (g.mode == kNCHW1 ? g.N : 1);
+}
+
+// Tile width: the ring's fill rate bounds these kernels (one k-block stages 16 KB of W
+// plus tbn x 128 B of x at ~40 B/clk per SM, against 2 x tbn clocks of MMA), so a step
+// costs max(fill, MMA) ~ (16384 + 128 tbn) / 40 clocks, and a launch costs its rounds of
+// tiles (ceil(tiles / grid)) x k-blocks x that, plus a per-tile epilogue drain. 256-wide
+// tiles stage 25% fewer bytes per MAC but halve the tile count: small layers keep 128.
+int plan_tbn(const Geo& g0) {
+  if (forced_tbn()) return forced_tbn();
+  double best = 0.0;
+  int pick = 128;
+  for (int tbn : {128, 256}) {
+    Geo g = g0;
+    set_tiles(g, tbn);
+    const int grid = conv_grid_for(g.mtiles, g.tiles);
+    const int64_t rounds = (g.tiles + grid - 1) / grid;
+    const int64_t ksteps = (int64_t)g.kblocks * (g.mode == kNHWC3 ? g.ksize * g.ksize : 1);
+    const double step = std::max((16384.0 + 128.0 * tbn) / 40.0, 2.0 * tbn);
+    const double cost = (double)rounds * ((double)ksteps * step + 4.0 * tbn);
+    if (tbn == 128 || cost < best) {
+      best = cost;
+      pick = tbn;
+    }
+  }
+  return pick;
+}
 
 Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t W,
              int ksize = 1, int stride = 1) {
@@ -719,28 +785,27 @@ Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t 
   g.M = N * g.Ho * g.Wo;
   g.mtiles = (int)((Cout + BM - 1) / BM);
   g.kblocks = (int)((Cin + BK - 1) / BK);
-  if (mode == kNCHW1) {
-    g.tilesP = (int)((g.HW + BN - 1) / BN);
-    g.tiles = (int64_t)g.mtiles * g.tilesP * N;
-  } else {
-    g.tilesP = (int)((g.M + BN - 1) / BN);
-    g.tiles = (int64_t)g.mtiles * g.tilesP;
-  }
+  set_tiles(g, 128);
+  set_tiles(g, plan_tbn(g));
   return g;
 }
 
 // Conv grid: one CTA per SM, rounded down to a multiple of the channel tiles (so a CTA's
 // tiles share their channels), at most one CTA per tile.
-int conv_grid(const Geo& g) {
-  const int sms = num_sms();
-  int64_t n = g.mtiles <= sms ? (int64_t)(sms / g.mtiles) * g.mtiles : g.mtiles;
-  return (int)std::min<int64_t>(n, g.tiles);
-}
+int conv_grid(const Geo& g) { return conv_grid_for(g.mtiles, g.tiles); }
 
+// Statistics slots: two per (CTA, channel); sized for the largest grid any tile width
+// can get (the header records the grid that ran).
+int conv_nslots_max(int64_t mtiles) {
+  const int sms = num_sms();
+  const int64_t grid = mtiles <= sms ? (int64_t)(sms / mtiles) * mtiles : mtiles;
+  return (int)(2 * ((grid + mtiles - 1) / mtiles));
+}
 int conv_nslots(const Geo& g) { return 2 * ((conv_grid(g) + g.mtiles - 1) / g.mtiles); }
 
-size_t stats_ws_bytes(const Geo& g) {
-  return sizeof(cgbn_slots::Header) + (size_t)conv_nslots(g) * (size_t)g.Cout * sizeof(Slot);
+size_t stats_ws_bytes(int64_t Cout) {
+  return sizeof(cgbn_slots::Header) +
+         (size_t)conv_nslots_max((Cout + BM - 1) / BM) * (size_t)Cout * sizeof(Slot);
 }
 
 template <class OutT, int MODE>
@@ -751,10 +816,10 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
       sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUtensorMap tmW, tmX, tmZ;
-  if constexpr (MODE == kNHWC3) {  // w[tap][Cout][Cin]
-    const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout,
-                              (cuuint64_t)(g.ksize * g.ksize)};
-    const cuuint64_t ws[2] = {(cuuint64_t)g.Cin * 2, (cuuint64_t)(g.Cin * g.Cout * 2)};
+  if constexpr (MODE == kNHWC3) {  // w[Cout][tap][Cin] (OHWI): dims {Cin, Cout, tap}
+    const int64_t taps = g.ksize * g.ksize;
+    const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout, (cuuint64_t)taps};
+    const cuuint64_t ws[2] = {(cuuint64_t)(taps * g.Cin * 2), (cuuint64_t)g.Cin * 2};
     const cuuint32_t wb[3] = {BK, BM, 1};
     if (int rc = make_map(&tmW, bf, 3, w, wd, ws, wb, "w")) return rc;
   } else {  // w[Cout][Cin]
@@ -776,16 +841,17 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
     if constexpr (MODE == kNHWC1) {  // x as [M][Cin]
       const cuuint64_t xd[2] = {(cuuint64_t)g.Cin, (cuuint64_t)g.M};
       const cuuint64_t xs[1] = {(cuuint64_t)g.Cin * 2};
-      const cuuint32_t xb[2] = {BK, BN};
+      const cuuint32_t xb[2] = {BK, (cuuint32_t)g.tbn};
       if (int rc = make_map(&tmX, bf, 2, x, xd, xs, xb, "x")) return rc;
     } else {
-      if (int rc = make_im2col_map(&tmX, x, g.N, g.Cin, g.H, g.W, g.ksize, g.stride, g.pad))
+      if (int rc = make_im2col_map(&tmX, x, g.N, g.Cin, g.H, g.W, g.ksize, g.stride, g.pad,
+                                   g.tbn))
         return rc;
     }
     // z as [M][Cout], box {32 channels, 64 pixels}, unswizzled (transposed staging)
     const cuuint64_t zd[2] = {(cuuint64_t)g.Cout, (cuuint64_t)g.M};
     const cuuint64_t zs[1] = {(cuuint64_t)g.Cout * sz};
-    const cuuint32_t zb[2] = {32, (cuuint32_t)kHalf};
+    const cuuint32_t zb[2] = {32, (cuuint32_t)kChunk};
     if (int rc = make_map(&tmZ, zdt, 2, z, zd, zs, zb, "z", CU_TENSOR_MAP_SWIZZLE_NONE)) return rc;
   }
   ConvArgs a;
@@ -805,8 +871,9 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
   a.pad = g.pad;
   a.ksize = g.ksize;
   a.taps = g.ksize * g.ksize;
-  const size_t smem = conv_smem_bytes();
-  auto kern = slots ? k_conv1x1<kStages, OutT, true, MODE> : k_conv1x1<kStages, OutT, false, MODE>;
+  const size_t smem = conv_smem_bytes(g.tbn);
+  auto kern = g.tbn == 256 ? (slots ? k_conv1x1<OutT, true, MODE, 256> : k_conv1x1<OutT, false, MODE, 256>)
+                           : (slots ? k_conv1x1<OutT, true, MODE, 128> : k_conv1x1<OutT, false, MODE, 128>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)conv_grid(g));
@@ -854,7 +921,7 @@ int run_conv(const char* what, const void* x, const void* w, const float* bias, 
   cudaStream_t st = (cudaStream_t)stream;
   Slot* slots = nullptr;
   if (stats) {
-    const size_t need = stats_ws_bytes(g);
+    const size_t need = stats_ws_bytes(g.Cout);
     if (!ws || ws_bytes < need)
       return fail(CGBN_ERR_INVALID, "%s: workspace too small (need %lld, got %lld)", what,
                   (long long)need, (long long)ws_bytes);
@@ -899,7 +966,7 @@ extern "C" {
 
 size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW) {
   if (N <= 0 || Cout <= 0 || HW <= 0) return 0;
-  return stats_ws_bytes(make_geo(kNCHW1, N, 8, Cout, 1, HW));
+  return stats_ws_bytes(Cout);
 }
 
 int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
@@ -919,7 +986,7 @@ size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W, in
                                int stride) {
   const int mode = nhwc_mode(ksize, stride);
   if (N <= 0 || Cout <= 0 || H <= 0 || W <= 0 || mode < 0) return 0;
-  return stats_ws_bytes(make_geo(mode, N, 8, Cout, H, W, ksize, stride));
+  return stats_ws_bytes(Cout);
 }
 
 int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,

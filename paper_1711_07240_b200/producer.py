@@ -94,7 +94,8 @@ def _check(x, weight, bias, out_dtype, k, stride=1):
                 "take the channel as the innermost dimension (NCHW rows cannot be shifted "
                 "by one element in a TMA box)")
         cout = weight.shape[0]
-        wt = weight.permute(2, 3, 0, 1).reshape(9, cout, cin)  # [tap = 3 ky + kx][Cout][Cin]
+        # [Cout][tap = 3 ky + kx][Cin] (OHWI): a channels_last weight as it is, no copy
+        wt = weight.permute(0, 2, 3, 1).reshape(cout, 9, cin)
     if stride not in (1, 2):
         raise BatchNormError(f"stride must be 1 or 2, got {stride}")
     if stride != 1 and not nhwc:

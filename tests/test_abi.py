@@ -53,7 +53,7 @@ def test_constants_match_header():
 
 def test_abi_version_and_argument_validation_without_gpu():
     lib = _lib.load()
-    assert lib.cgbn_abi_version() == 6
+    assert lib.cgbn_abi_version() == 7
     assert b"sm_100a" in lib.cgbn_build_info()
     # invalid shapes are rejected on the host before any CUDA call
     rc = lib.cgbn_fwd_stats(None, 2, 3, 4, 0, None, None, 0, None)
@@ -101,9 +101,9 @@ def test_stale_build_rejected(monkeypatch):
     """load() checks the ABI version and every bound symbol before use."""
     monkeypatch.setattr(_lib, "_lib", None)
     monkeypatch.setattr(_lib, "ABI_VERSION", 5)
-    with pytest.raises(_lib.CGBNLibraryError, match="ABI v6"):
+    with pytest.raises(_lib.CGBNLibraryError, match="ABI v7"):
         _lib.load()
-    monkeypatch.setattr(_lib, "ABI_VERSION", 6)
+    monkeypatch.setattr(_lib, "ABI_VERSION", 7)
     monkeypatch.setitem(_lib.SIGNATURES, "cgbn_not_there", (_lib._i, []))
     with pytest.raises(_lib.CGBNLibraryError, match="cgbn_not_there"):
         _lib.load()

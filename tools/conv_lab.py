@@ -56,7 +56,8 @@ def main():
     for k, sd, cin, cout, h, w, cnt in layers:
         xs = [torch.randn(a.batch, cin, h, w, device=dev).to(torch.bfloat16).contiguous(
             memory_format=cl) for _ in range(a.sets)]
-        wt = (torch.randn(cout, cin, k, k, device=dev) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+        wt = (torch.randn(cout, cin, k, k, device=dev) / (k * k * cin) ** 0.5).to(
+            torch.bfloat16).contiguous(memory_format=cl)
         conv = P.conv3x3 if k == 3 else P.conv1x1
         stats = P.conv3x3_stats if k == 3 else P.conv1x1_stats
         bf = torch.bfloat16
