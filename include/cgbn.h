@@ -304,14 +304,21 @@ int cgbn_bwd_fused(const void* dy, const void* x, int64_t N, int64_t C, int64_t 
  * the vector cgbn_fwd_stats(z) would produce, so the exchange and cgbn_fwd_normalize
  * follow unchanged and the BN forward no longer reads z for its statistics.
  *  bias     : Cout floats or NULL.
- *  ws       : cgbn_conv1x1_ws_bytes(N, Cout, HW) bytes, 16-byte aligned (the per-CTA
- *             statistics slot table; need not be zeroed).
+ *  ws       : cgbn_conv1x1_ws_bytes(N, Cin, Cout, HW) bytes, 16-byte aligned: the per-CTA
+ *             statistics slot table and the split-K partials; the LAST 16 KB of the
+ *             ws_bytes passed are the split-K tickets (ABI v7), which must be zero before
+ *             the first call on a buffer (allocate it zero-filled) and are left zero by
+ *             every call, so one buffer serves layers of any shape.
  *  partial  : may be NULL: the fold is skipped and the slot table stays in ws for
  *             cgbn_fwd_normalize_slots (below).
  * Two launches (the conv, then a per-channel fold of the tile partials). Returns
  * CGBN_ERR_UNSUPPORTED when H*W or Cin is not a multiple of 8 (TMA row strides).
- * cgbn_conv1x1 is the same convolution without the statistics (the unfused producer). */
-size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cout, int64_t HW);
+ * cgbn_conv1x1 is the same convolution without the statistics (the unfused producer); its
+ * ws (same size and contract) may be NULL, which only forgoes split-K.
+ * Split-K: layers with fewer 128-pixel tiles than SMs cut each tile's k-steps into up to 4
+ * ranges on as many CTAs; the last range's CTA adds the others' fp32 partials in range
+ * order (deterministic) before the epilogue. */
+size_t cgbn_conv1x1_ws_bytes(int64_t N, int64_t Cin, int64_t Cout, int64_t HW);
 /* Single-rank groups (bn_forward_local, or a BN group of one): call the *_stats entry
  * point with partial = NULL, which leaves the statistics slot table in ws (a 32-byte
  * header written by the conv kernel, then the per-CTA slots), and pass that ws here as
@@ -324,7 +331,8 @@ int cgbn_fwd_normalize_slots(const void* x, int64_t N, int64_t C, int64_t HW, in
                              float* running_var, double* saved, int relu, void* y,
                              unsigned* status, void* ws, size_t ws_bytes, void* stream);
 int cgbn_conv1x1(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
-                 int64_t Cout, int64_t HW, int out_dtype, void* z, void* stream);
+                 int64_t Cout, int64_t HW, int out_dtype, void* z, void* ws, size_t ws_bytes,
+                 void* stream);
 int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
                        int64_t Cout, int64_t HW, int out_dtype, void* z, double* partial,
                        void* ws, size_t ws_bytes, void* stream);
@@ -340,11 +348,11 @@ int cgbn_conv1x1_stats(const void* x, const void* w, const float* bias, int64_t 
  * ABI v7 — v6 took [9][Cout][Cin]). Cin and Cout must be
  * multiples of 8. Statistics contract as cgbn_conv1x1_stats; ws: cgbn_conv_nhwc_ws_bytes
  * bytes. */
-size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cout, int64_t H, int64_t W, int ksize,
-                               int stride);
+size_t cgbn_conv_nhwc_ws_bytes(int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t W,
+                               int ksize, int stride);
 int cgbn_conv_nhwc(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
                    int64_t Cout, int64_t H, int64_t W, int ksize, int stride, int out_dtype,
-                   void* z, void* stream);
+                   void* z, void* ws, size_t ws_bytes, void* stream);
 int cgbn_conv_nhwc_stats(const void* x, const void* w, const float* bias, int64_t N, int64_t Cin,
                          int64_t Cout, int64_t H, int64_t W, int ksize, int stride, int out_dtype,
                          void* z, double* partial, void* ws, size_t ws_bytes, void* stream);

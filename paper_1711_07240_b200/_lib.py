@@ -86,11 +86,12 @@ SIGNATURES = {
                              _p, _p, _p, _p, _p, _sz, _p]),
     "cgbn_fwd_normalize_slots": (_i, [_p, _i64, _i64, _i64, _i, _p, _p, _p, _d, _d, _p, _p, _p,
                                       _i, _p, _p, _p, _sz, _p]),
-    "cgbn_conv1x1_ws_bytes": (_sz, [_i64, _i64, _i64]),
-    "cgbn_conv1x1": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i, _p, _p]),
+    "cgbn_conv1x1_ws_bytes": (_sz, [_i64, _i64, _i64, _i64]),
+    "cgbn_conv1x1": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i, _p, _p, _sz, _p]),
     "cgbn_conv1x1_stats": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i, _p, _p, _p, _sz, _p]),
-    "cgbn_conv_nhwc_ws_bytes": (_sz, [_i64, _i64, _i64, _i64, _i, _i]),
-    "cgbn_conv_nhwc": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _i, _i, _p, _p]),
+    "cgbn_conv_nhwc_ws_bytes": (_sz, [_i64, _i64, _i64, _i64, _i64, _i, _i]),
+    "cgbn_conv_nhwc": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _i, _i, _p, _p, _sz,
+                            _p]),
     "cgbn_conv_nhwc_stats": (_i, [_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _i, _i, _p, _p,
                                   _p, _sz, _p]),
 }

@@ -26,7 +26,7 @@ __host__ __device__ inline const Slot* table(const void* ws) {
 }
 
 // Merge of channel c's slots by a 32 x 32 block (lane = channel, warp w takes slots w,
-// w + 32, ...) against one shift K0 = slot 0's mean: A = sum n_k (mean_k - K0), B = sum
+// w + 32, ...) against one shift K0 = the first non-empty slot's mean: A = sum n_k (mean_k - K0), B = sum
 // M2_k + n_k (mean_k - K0)^2 (additions only), the 32 warp sums added in warp order by
 // warp 0, which gets (n, mean, M2); other warps' results are meaningless. Fixed order:
 // bitwise reproducible.
@@ -45,7 +45,16 @@ __device__ __forceinline__ void merge(const Slot* __restrict__ slots, int Cout, 
       const bool ok = s < nslots && (s >> 1) * mtiles + mt < grid;
       p[u] = ok ? slots[(size_t)s * Cout + c] : Slot{0.0, 0.0, 0.0};
     }
-    K0 = slots[c].mean;
+    // the shift: the first non-empty slot's mean (a CTA that only ran non-final split-K
+    // ranges leaves n = 0 slots)
+    for (int s = 0; s < nslots; ++s) {
+      if ((s >> 1) * mtiles + mt >= grid) continue;
+      const Slot q = slots[(size_t)s * Cout + c];
+      if (q.n > 0.0) {
+        K0 = q.mean;
+        break;
+      }
+    }
 #pragma unroll
     for (int u = 0; u < kFoldPerWarp; ++u) {
       if (p[u].n == 0.0) continue;

@@ -59,7 +59,8 @@ def _tile_scratch(device, nbytes):
     with _scratch_lock:
         buf = _scratch.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+            # zero-filled: the split-K tickets must start at zero (each call leaves them so)
+            buf = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
             _scratch[key] = buf
         _scratch.move_to_end(key)
         while len(_scratch) > 64:
@@ -134,12 +135,12 @@ def _conv(x, weight, bias, out_dtype, k, stats, stride=1, slots_only=False):
     st = stream_ptr(dev)
     od = _OUT[out_dtype]
     partial = None
-    if stats:
-        if not slots_only:
-            partial = torch.empty(2 * cout + 1, dtype=torch.float64, device=dev)
-        nb = (lib.cgbn_conv_nhwc_ws_bytes(n, cout, h, w, k, stride) if nhwc
-              else lib.cgbn_conv1x1_ws_bytes(n, cout, h * w))
-        ws = _tile_scratch(dev, nb)
+    if stats and not slots_only:
+        partial = torch.empty(2 * cout + 1, dtype=torch.float64, device=dev)
+    # slot table (statistics) and split-K scratch
+    nb = (lib.cgbn_conv_nhwc_ws_bytes(n, cin, cout, h, w, k, stride) if nhwc
+          else lib.cgbn_conv1x1_ws_bytes(n, cin, cout, h * w))
+    ws = _tile_scratch(dev, nb)
     name = f"conv{k}x{k}" + ("_stats" if stats else "")
     with _Span(name, 0):
         if nhwc and stats:
@@ -149,7 +150,7 @@ def _conv(x, weight, bias, out_dtype, k, stats, stride=1, slots_only=False):
                                           ws.data_ptr(), ws.numel(), st)
         elif nhwc:
             rc = lib.cgbn_conv_nhwc(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h, w, k,
-                                    stride, od, z.data_ptr(), st)
+                                    stride, od, z.data_ptr(), ws.data_ptr(), ws.numel(), st)
         elif stats:
             rc = lib.cgbn_conv1x1_stats(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h * w, od,
                                         z.data_ptr(),
@@ -157,7 +158,7 @@ def _conv(x, weight, bias, out_dtype, k, stats, stride=1, slots_only=False):
                                         ws.data_ptr(), ws.numel(), st)
         else:
             rc = lib.cgbn_conv1x1(x.data_ptr(), wt.data_ptr(), bp, n, cin, cout, h * w, od,
-                                  z.data_ptr(), st)
+                                  z.data_ptr(), ws.data_ptr(), ws.numel(), st)
         _lib.check(rc, "cgbn_" + ("conv_nhwc" if nhwc else "conv1x1") + ("_stats" if stats else ""))
     if slots_only:
         return z, ws

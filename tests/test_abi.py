@@ -78,15 +78,15 @@ def test_producer_conv_argument_validation_without_gpu():
     """The producer entry points reject bad arguments on the host, before any CUDA call,
     with the shared thread-local message (the conv lives in a second translation unit)."""
     lib = _lib.load()
-    rc = lib.cgbn_conv1x1(None, None, None, 2, 64, 128, 64, 0, None, None)
+    rc = lib.cgbn_conv1x1(None, None, None, 2, 64, 128, 64, 0, None, None, 0, None)
     assert rc == _lib.ERR_INVALID and b"null" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 64, 128, 8, 8, 2, 1, 0, 16, None)
+    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 64, 128, 8, 8, 2, 1, 0, 16, None, 0, None)
     assert rc == _lib.ERR_INVALID and b"ksize" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 60, 128, 8, 8, 3, 1, 0, 16, None)
+    rc = lib.cgbn_conv_nhwc(16, 16, None, 2, 60, 128, 8, 8, 3, 1, 0, 16, None, 0, None)
     assert rc == _lib.ERR_UNSUPPORTED and b"Cin" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv1x1(16, 16, None, 2, 64, 128, 49, 0, 16, None)
+    rc = lib.cgbn_conv1x1(16, 16, None, 2, 64, 128, 49, 0, 16, None, 0, None)
     assert rc == _lib.ERR_UNSUPPORTED and b"H*W" in lib.cgbn_last_error()
-    rc = lib.cgbn_conv1x1(16, 16, None, 2, 64, 128, 64, 0x20, 16, None)
+    rc = lib.cgbn_conv1x1(16, 16, None, 2, 64, 128, 64, 0x20, 16, None, 0, None)
     assert rc == _lib.ERR_INVALID and b"dtype" in lib.cgbn_last_error()
     rc = lib.cgbn_conv1x1_stats(16, 16, None, 2, 64, 128, 64, 0, 16, None, None, 0, None)
     assert rc == _lib.ERR_INVALID and b"workspace" in lib.cgbn_last_error()

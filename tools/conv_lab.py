@@ -15,6 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from bench import PRODUCER_LAYERS_NHWC  # noqa: E402
+import paper_1711_07240_b200 as cg  # noqa: E402
 from paper_1711_07240_b200 import producer as P  # noqa: E402
 
 
@@ -63,9 +64,19 @@ def main():
         bf = torch.bfloat16
         t_o = timed(lambda: [conv(x, wt, stride=sd, out_dtype=bf) for x in xs], a.iters, a.sets)
         t_s = timed(lambda: [stats(x, wt, stride=sd, out_dtype=bf) for x in xs], a.iters, a.sets)
+        # the statistics epilogue alone (slot table left in ws, no fold launch)
+        t_sl = timed(lambda: [P._conv(x, wt, None, bf, k, True, sd, slots_only=True)
+                              for x in xs], a.iters, a.sets)
         pad = k // 2
         t_c = timed(lambda: [torch.nn.functional.conv2d(x, wt, stride=sd, padding=pad)
                              for x in xs], a.iters, a.sets)
+        # the producer fusion itself: fused conv + BN forward vs cuDNN conv + our BN forward
+        sts = [cg.BNLayerState.create(cout, device=dev) for _ in range(a.sets)]
+        fused = P.conv3x3_bn_forward_local if k == 3 else P.conv1x1_bn_forward_local
+        t_f = timed(lambda: [fused(x, wt, st, stride=sd, out_dtype=bf) for x, st in zip(xs, sts)],
+                    a.iters, a.sets)
+        t_cs = timed(lambda: [cg.bn_forward_local(torch.nn.functional.conv2d(
+            x, wt, stride=sd, padding=pad), st) for x, st in zip(xs, sts)], a.iters, a.sets)
         # parity of the plain conv against cuDNN's (both bf16 out)
         z = conv(xs[0], wt, stride=sd, out_dtype=bf).float()
         zr = torch.nn.functional.conv2d(xs[0], wt, stride=sd, padding=pad).float()
@@ -73,15 +84,22 @@ def main():
         flops = 2.0 * a.batch * (h // sd) * (w // sd) * cout * cin * k * k
         print(json.dumps({"k": k, "stride": sd, "cin": cin, "cout": cout, "hw": h, "count": cnt,
                           "ours_us": round(t_o, 2), "ours_stats_us": round(t_s, 2),
+                          "ours_slots_us": round(t_sl, 2), "fused_us": round(t_f, 2),
+                          "cudnn_split_us": round(t_cs, 2),
                           "cudnn_us": round(t_c, 2), "ours_tflops": round(flops / t_o / 1e6),
                           "cudnn_tflops": round(flops / t_c / 1e6),
                           "ratio": round(t_c / t_o, 3), "rel_err": err}), flush=True)
         tot["ours"] += cnt * t_o
         tot["ours_stats"] += cnt * t_s
         tot["cudnn"] += cnt * t_c
+        tot["fused"] = tot.get("fused", 0.0) + cnt * t_f
+        tot["cudnn_split"] = tot.get("cudnn_split", 0.0) + cnt * t_cs
+        tot["slots"] = tot.get("slots", 0.0) + cnt * t_sl
         del xs
     print(json.dumps({"total_us": {k: round(v, 1) for k, v in tot.items()},
-                      "ratio": round(tot["cudnn"] / tot["ours"], 3)}), flush=True)
+                      "ratio": round(tot["cudnn"] / tot["ours"], 3),
+                      "fused_vs_cudnn_split": round(tot["cudnn_split"] / tot["fused"], 3)}),
+          flush=True)
 
 
 if __name__ == "__main__":
