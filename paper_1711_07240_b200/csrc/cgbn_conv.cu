@@ -56,13 +56,18 @@ constexpr size_t kTicketBytes = 16384;        // split-K tickets: 4096 tiles (se
 // k-block instead of 16 KB + TBN x 128 B.
 // STAGED: the epilogue stages z in shared memory for TMA stores (NCHW z, 64 KB); NHWC z
 // is stored straight from registers, and that space deepens the ring instead.
-template <int TBN, bool PAIR, bool STAGED>
+// KBS: 64-channel k-blocks per ring stage (2 for the NHWC modes: one TMA box carries two
+// k-blocks, which halves the producer's issue chain per MAC — measured, the single TMA
+// thread's ~500 clocks per stage bound the mainloop, not bandwidth; tools/lab/tmabench.cu).
+template <int TBN, bool PAIR, bool STAGED, int KBS = 1>
 struct Tile {
   static constexpr int kPix = PAIR ? TBN / 2 : TBN;          // pixels of x staged per CTA
-  static constexpr uint32_t kTileB = BK * kPix * 2;          // 8 .. 32 KB
-  static constexpr uint32_t kStage = kTileA + kTileB;        // 24 .. 48 KB
+  static constexpr uint32_t kTileA1 = kTileA;                // one k-block of W: 16 KB
+  static constexpr uint32_t kTileB1 = BK * kPix * 2;         // one k-block of x
+  static constexpr uint32_t kTileB = KBS * kTileB1;
+  static constexpr uint32_t kStage = KBS * kTileA + kTileB;  // 24 .. 96 KB
   static constexpr uint32_t kOut = STAGED ? kEpiWarps * 2 * kWarpStage : 0;
-  static constexpr int kStages = (int)((216u * 1024u - kOut) / kStage);  // 3 .. 9
+  static constexpr int kStages = (int)((216u * 1024u - kOut) / kStage);  // 2 .. 9
   static constexpr int kHalfCols = TBN / 2;                  // columns per epilogue warp
   static constexpr int kChunks = kHalfCols / kChunk;         // 1 / 2 steps per tile
   static constexpr size_t kSmem = 1024 + kStages * kStage + kOut + 8 * (2 * kStages + 4) + 16;
@@ -114,6 +119,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const void* src, int c0,
@@ -379,6 +392,7 @@ struct ConvArgs {
   // (channel tile fastest, then split, then pixel tile); the last split of a tile sums
   // the others' fp32 partials (part) once its ticket shows them all written
   int splits, kper, ksteps, units;
+  int kbs, kst;       // k-blocks per ring stage (1 or 2); stages per tap = ceil(kblocks / kbs)
   int* tickets;       // [tiles], zero between launches (the last split resets its own)
   float* part;        // [tiles][splits - 1][128 x 128]
   unsigned long long* trace;  // debug (cgbn_debug_conv_trace): [CTA][16 units][8 stamps]
@@ -439,7 +453,8 @@ template <class OutT, bool STATS, int MODE, int TBN, bool PAIR>
 __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps per SMSP
     k_conv1x1(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmZ, const ConvArgs a) {
-  using T = Tile<TBN, PAIR, MODE == kNCHW1>;
+  constexpr int KBS = (MODE != kNCHW1 && !PAIR && TBN == 128) ? 2 : 1;
+  using T = Tile<TBN, PAIR, MODE == kNCHW1, KBS>;
   constexpr int S = T::kStages;
   constexpr int kCols = OutTraits<OutT>::kCols;
   constexpr int kBoxes = kChunk / kCols;  // staged 128-byte boxes per step
@@ -492,60 +507,90 @@ __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps pe
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      uint32_t it = 0, pli = 0;
+      // The producer is one thread issuing a serial chain, so everything per k-step is
+      // incremental: the unit's pixel geometry is decoded once, taps / k-blocks are walked
+      // with counters (runtime divisions here cost ~50 clocks each, per k-step).
+      uint32_t it = 0, pli = 0, s = 0, ph = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++pli) {
         const UnitPos q = unit_pos(a, u);
         cstamp(a, pli, 0, gtimer());
         const int mt = q.mt, rest = q.rest;
         const int p0 = (rest % a.tilesP) * TBN, img = rest / a.tilesP;
-        {
-          for (int kk = q.kk0; kk < q.kk1; ++kk, ++it) {
-            const int tap = kk / a.kblocks, kb = kk - tap * a.kblocks;
-            const uint32_t s = it % S;
-            if (it >= (uint32_t)S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-            uint8_t* A = ring + s * T::kStage;
-            uint8_t* B = A + kTileA;
-            if constexpr (PAIR) {
-              // both CTAs' copies land on the leader's barrier; the leader expects them all
-              if (rank == 0) mbar_expect_tx(&full[s], 2 * T::kStage);
-              const uint32_t fb = mapa(smem_u32(&full[s]), 0);
-              const int px = p0 + (int)rank * T::kPix;  // this CTA's half of the pixels
-              if constexpr (MODE == kNCHW1) {
-                tma_load_2d_pair(A, &tmW, fb, kb * BK, mt * BM);
-#pragma unroll
-                for (int j = 0; j < T::kPix / 64; ++j)
-                  tma_load_3d_pair(B + j * 8192, &tmX, fb, px + 64 * j, kb * BK, img);
-              } else if constexpr (MODE == kNHWC1) {
-                tma_load_2d_pair(A, &tmW, fb, kb * BK, mt * BM);
-                tma_load_2d_pair(B, &tmX, fb, kb * BK, px);
-              } else {
-                const int n = px / a.HWo, rem = px % a.HWo;
-                tma_load_3d_pair(A, &tmW, fb, kb * BK, mt * BM, tap);
-                tma_load_im2col_4d_pair(B, &tmX, fb, kb * BK, (rem % a.Wo) * a.stride - a.pad,
-                                        (rem / a.Wo) * a.stride - a.pad, n,
-                                        (uint16_t)(tap % a.ksize), (uint16_t)(tap / a.ksize));
-              }
-              continue;
-            }
-            mbar_expect_tx(&full[s], T::kStage);
+        const int px = p0 + (PAIR ? (int)rank * T::kPix : 0);  // this CTA's pixels
+        int n = 0, w0 = 0, h0 = 0;
+        if constexpr (MODE == kNHWC3) {  // im2col base of pixel px: input position - pad
+          n = px / a.HWo;
+          const int rem = px - n * a.HWo;
+          const int ho = rem / a.Wo;
+          w0 = (rem - ho * a.Wo) * a.stride - a.pad;
+          h0 = ho * a.stride - a.pad;
+        }
+        // stage kk = (tap, k-block group): a.kst groups of a.kbs k-blocks per tap
+        int tap = q.kk0 / a.kst, kb = (q.kk0 - tap * a.kst) * a.kbs;
+        int ty = tap / a.ksize, tx = tap - ty * a.ksize;
+        for (int kk = q.kk0; kk < q.kk1; ++kk, ++it) {
+          if (it >= (uint32_t)S) mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* A = ring + s * T::kStage;
+          uint8_t* B = A + KBS * kTileA;
+          if constexpr (PAIR) {
+            // both CTAs' copies land on the leader's barrier; the leader expects them all
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * T::kStage);
+            const uint32_t fb = mapa(smem_u32(&full[s]), 0);
             if constexpr (MODE == kNCHW1) {
-              tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
+              tma_load_2d_pair(A, &tmW, fb, kb * BK, mt * BM);
 #pragma unroll
-              for (int j = 0; j < TBN / 64; ++j)  // 64-pixel boxes of 8 KB
-                tma_load_3d(B + j * 8192, &tmX, &full[s], p0 + 64 * j, kb * BK, img);
+              for (int j = 0; j < T::kPix / 64; ++j)
+                tma_load_3d_pair(B + j * 8192, &tmX, fb, px + 64 * j, kb * BK, img);
             } else if constexpr (MODE == kNHWC1) {
-              // x as [N*H*W][Cin]: TBN pixels x 64 channels, K-major like W
-              tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
-              tma_load_2d(B, &tmX, &full[s], kb * BK, p0);
+              tma_load_2d_pair(A, &tmW, fb, kb * BK, mt * BM);
+              tma_load_2d_pair(B, &tmX, fb, kb * BK, px);
             } else {
-              // implicit GEMM: the im2col base of output pixel p0 is its input position
-              // minus the padding; tap (ky, kx) is the instruction's offset
-              // (stride s: the traversal walks input positions s apart)
-              const int n = p0 / a.HWo, rem = p0 % a.HWo;
-              tma_load_3d(A, &tmW, &full[s], kb * BK, mt * BM, tap);
-              tma_load_im2col_4d(B, &tmX, &full[s], kb * BK, (rem % a.Wo) * a.stride - a.pad,
-                                 (rem / a.Wo) * a.stride - a.pad, n,
-                                 (uint16_t)(tap % a.ksize), (uint16_t)(tap / a.ksize));
+              tma_load_3d_pair(A, &tmW, fb, kb * BK, mt * BM, tap);
+              tma_load_im2col_4d_pair(B, &tmX, fb, kb * BK, w0, h0, n, (uint16_t)tx,
+                                      (uint16_t)ty);
+            }
+          } else if constexpr (MODE == kNCHW1) {
+            mbar_expect_tx(&full[s], T::kStage);
+            tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
+#pragma unroll
+            for (int j = 0; j < TBN / 64; ++j)  // 64-pixel boxes of 8 KB
+              tma_load_3d(B + j * 8192, &tmX, &full[s], p0 + 64 * j, kb * BK, img);
+          } else {
+            // a.kbs k-blocks per stage: W (and x for 1x1) as one box whose outer dimension
+            // walks the k-blocks ([kb][rows][64] in shared memory), x for 3x3 as one im2col
+            // box per k-block (tap (ky, kx) is the instruction's offset from the base;
+            // stride s: the traversal walks input positions s apart)
+            const int nk = min(a.kbs, a.kblocks - kb);  // k-blocks of this stage
+            if constexpr (MODE == kNHWC1) {
+              mbar_expect_tx(&full[s], (uint32_t)a.kbs * (kTileA + T::kTileB1));
+              if (a.kbs == 1) {
+                tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
+                tma_load_2d(B, &tmX, &full[s], kb * BK, p0);
+              } else {  // views {64, rows, k-block}
+                tma_load_3d(A, &tmW, &full[s], 0, mt * BM, kb);
+                tma_load_3d(B, &tmX, &full[s], 0, p0, kb);
+              }
+            } else {
+              mbar_expect_tx(&full[s], (uint32_t)a.kbs * kTileA + (uint32_t)nk * T::kTileB1);
+              if (a.kbs == 1)
+                tma_load_3d(A, &tmW, &full[s], kb * BK, mt * BM, tap);
+              else  // view {64, Cout, tap, k-block}
+                tma_load_4d(A, &tmW, &full[s], 0, mt * BM, tap, kb);
+              for (int j = 0; j < nk; ++j)
+                tma_load_im2col_4d(B + j * T::kTileB1, &tmX, &full[s], (kb + j) * BK, w0, h0, n,
+                                   (uint16_t)tx, (uint16_t)ty);
+            }
+          }
+          if (++s == (uint32_t)S) {
+            s = 0;
+            ph ^= 1;
+          }
+          if ((kb += a.kbs) >= a.kblocks) {
+            kb = 0;
+            ++tap;
+            if (++tx == a.ksize) {
+              tx = 0;
+              ++ty;
             }
           }
         }
@@ -563,24 +608,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps pe
         const uint32_t d = tmem + acc * TBN;
         const UnitPos q = unit_pos(a, u);
         const int ksteps = q.kk1 - q.kk0;
+        int kbg = q.kk0 % a.kst;  // k-block group within the tap: k-blocks kbg * kbs ..
         for (int kb = 0; kb < ksteps; ++kb, ++it) {
+          const int nk = MODE == kNCHW1 ? 1 : min(a.kbs, a.kblocks - kbg * a.kbs);
+          if (++kbg == a.kst) kbg = 0;
           const uint32_t s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
-          const uint32_t A = smem_u32(ring + s * T::kStage);
-          const uint32_t B = A + kTileA;
+          const uint32_t A0 = smem_u32(ring + s * T::kStage);
+          const uint32_t B0 = A0 + KBS * kTileA;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // A: K-major rows of 128 B, 8-row atoms 1024 B apart; K step = 32 B in the
-            //    row. B: MN-major, 64-pixel blocks 8 KB apart (LBO), 8-channel groups
-            //    1 KB apart (SBO); K step = 16 rows = 2 KB.
-            const uint64_t ad = sdesc(A + k * 32, 16, 1024);
-            const uint64_t bd = MODE == kNCHW1 ? sdesc(B + k * 2048, 8192, 1024)
-                                               : sdesc(B + k * 32, 16, 1024);  // NHWC: K-major
-            if constexpr (PAIR)
-              mma_bf16_pair(d, ad, bd, kId, (kb | k) != 0);
-            else
-              mma_bf16(d, ad, bd, kId, (kb | k) != 0);
+          for (int j = 0; j < KBS; ++j) {
+            if (j >= nk) break;
+            const uint32_t A = A0 + j * kTileA, B = B0 + j * T::kTileB1;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              // A: K-major rows of 128 B, 8-row atoms 1024 B apart; K step = 32 B in the
+              //    row. B: MN-major, 64-pixel blocks 8 KB apart (LBO), 8-channel groups
+              //    1 KB apart (SBO); K step = 16 rows = 2 KB.
+              const uint64_t ad = sdesc(A + k * 32, 16, 1024);
+              const uint64_t bd = MODE == kNCHW1 ? sdesc(B + k * 2048, 8192, 1024)
+                                                 : sdesc(B + k * 32, 16, 1024);  // NHWC: K-major
+              if constexpr (PAIR)
+                mma_bf16_pair(d, ad, bd, kId, (kb | j | k) != 0);
+              else
+                mma_bf16(d, ad, bd, kId, (kb | j | k) != 0);
+            }
           }
           if constexpr (PAIR)
             mma_commit_pair(&empty[s]);
@@ -999,11 +1052,12 @@ int make_im2col_map(CUtensorMap* m, const void* base, int64_t N, int64_t C, int6
 }
 
 size_t conv_smem_bytes(int tbn, bool pair, bool staged) {
+  // the kernel's Tile: NCHW staged, single-k-block stages; NHWC pairs single; NHWC 2 (KBS)
   if (staged)
     return pair ? (tbn == 256 ? Tile<256, true, true>::kSmem : Tile<128, true, true>::kSmem)
                 : (tbn == 256 ? Tile<256, false, true>::kSmem : Tile<128, false, true>::kSmem);
   return pair ? (tbn == 256 ? Tile<256, true, false>::kSmem : Tile<128, true, false>::kSmem)
-              : (tbn == 256 ? Tile<256, false, false>::kSmem : Tile<128, false, false>::kSmem);
+              : (tbn == 256 ? Tile<256, false, false>::kSmem : Tile<128, false, false, 2>::kSmem);
 }
 
 bool conv_pdl() {  // CGBN_NO_PDL=1 disables programmatic dependent launch (read once)
@@ -1035,9 +1089,27 @@ struct Geo {
   int tbn, tilesP, mtiles, kblocks;
   bool pair;  // cta_group::2 over adjacent channel tiles (mtiles even)
   int64_t tiles;
-  int ksteps, splits, kper;  // k-steps per tile; split-K ranges (1 = none)
+  int kbs, kst;              // k-blocks per ring stage; stages per tap
+  int ksteps, splits, kper;  // ring stages per tile; split-K ranges (1 = none)
   int64_t units;             // tiles x splits
 };
+
+// k-blocks per stage: 2 for the NHWC modes with 128-pixel tiles (single CTAs, Cin a
+// multiple of 64 so the k-block views never reach into the next row), else 1.
+int plan_kbs(const Geo& g, int tbn, bool pair) {
+  // (256-pixel tiles keep 1: a 96 KB stage leaves room for two, which measured slower)
+  return g.mode != kNCHW1 && !pair && tbn == 128 && g.Cin % 64 == 0 && g.kblocks >= 2 ? 2 : 1;
+}
+
+// One ring stage's cost in SM clocks (tools/lab/tmabench.cu, B200): the single producer
+// thread's issue chain (~450 + 60 per TMA), the per-SM TMA fill bandwidth (~77 B/clk)
+// and the MMA (2 x TBN clocks per k-block), whichever binds.
+double stage_clocks(const Geo& g, int tbn, bool pair, int kbs) {
+  const int pix = pair ? tbn / 2 : tbn;
+  const int ntma = g.mode == kNCHW1 ? 1 + pix / 64 : (g.mode == kNHWC1 ? 2 : 1 + kbs);
+  const double bytes = (double)kbs * (16384.0 + 128.0 * pix);
+  return std::max({450.0 + 60.0 * ntma, bytes / 77.0, 2.0 * tbn * kbs});
+}
 
 int conv_grid_for(int64_t mtiles, int64_t tiles) {
   if (mtiles <= 0 || tiles <= 0) return 1;  // invalid extents: validate() reports them
@@ -1090,9 +1162,10 @@ void plan_tiles(Geo& g) {
       set_tiles(g, tbn);
       const int grid = conv_grid_for(g.mtiles, g.tiles);
       const int64_t rounds = (g.tiles + grid - 1) / grid;
-      const int64_t ksteps = (int64_t)g.kblocks * (g.mode == kNHWC3 ? g.ksize * g.ksize : 1);
-      const double fill = (16384.0 + 128.0 * (pair ? tbn / 2 : tbn)) / 40.0;
-      const double step = std::max(fill, 2.0 * tbn);
+      const int kbs = plan_kbs(g, tbn, pair != 0);
+      const int64_t ksteps =
+          (int64_t)((g.kblocks + kbs - 1) / kbs) * (g.mode == kNHWC3 ? g.ksize * g.ksize : 1);
+      const double step = stage_clocks(g, tbn, pair != 0, kbs);
       const double cost = (double)rounds * ((double)ksteps * step + 4.0 * tbn);
       if (first || cost < best) {
         best = cost;
@@ -1104,6 +1177,8 @@ void plan_tiles(Geo& g) {
   }
   g.pair = pick_pair;
   set_tiles(g, pick_tbn);
+  g.kbs = plan_kbs(g, pick_tbn, pick_pair);
+  g.kst = (g.kblocks + g.kbs - 1) / g.kbs;
 }
 
 // CGBN_CONV_SPLITS=n pins the split-K factor (read once; experiments only).
@@ -1120,12 +1195,12 @@ int forced_splits() {
 // and the last one adds the others' fp32 partials (64 KB each, through L2) before the
 // epilogue. Cost model as in plan_tiles, plus the measured hand-off.
 void plan_splits(Geo& g, bool allowed) {
-  g.ksteps = g.kblocks * (g.mode == kNHWC3 ? g.ksize * g.ksize : 1);
+  g.ksteps = g.kst * (g.mode == kNHWC3 ? g.ksize * g.ksize : 1);
   g.splits = 1;
   if (allowed && g.tbn == 128 && !g.pair && g.tiles <= (int64_t)(kTicketBytes / sizeof(int))) {
     int best_s = 0;
     double best = 0.0;
-    const double step = std::max((16384.0 + 128.0 * 128) / 40.0, 256.0);
+    const double step = stage_clocks(g, 128, false, g.kbs);
     for (int sp = 1; sp <= 4; ++sp) {
       if (forced_splits() && sp != forced_splits()) continue;
       const int kper = (g.ksteps + sp - 1) / sp;
@@ -1221,7 +1296,23 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
       sz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUtensorMap tmW, tmX, tmZ;
-  if constexpr (MODE == kNHWC3) {  // w[Cout][tap][Cin] (OHWI): dims {Cin, Cout, tap}
+  if (MODE != kNCHW1 && g.kbs == 2) {
+    // k-block views (Cin % 64 == 0): the outermost box dimension walks 2 k-blocks of 64
+    // channels, 128 B apart, so one box lands as [kb][rows][64] — two 16 KB tiles
+    const cuuint64_t nkb = (cuuint64_t)(g.Cin / 64);
+    if (MODE == kNHWC3) {  // w[Cout][tap][Cin]: {64, Cout, tap, kb}
+      const int64_t taps = g.ksize * g.ksize;
+      const cuuint64_t wd[4] = {64, (cuuint64_t)g.Cout, (cuuint64_t)taps, nkb};
+      const cuuint64_t ws[3] = {(cuuint64_t)(taps * g.Cin * 2), (cuuint64_t)g.Cin * 2, 128};
+      const cuuint32_t wb[4] = {BK, BM, 1, 2};
+      if (int rc = make_map(&tmW, bf, 4, w, wd, ws, wb, "w")) return rc;
+    } else {  // w[Cout][Cin]: {64, Cout, kb}
+      const cuuint64_t wd[3] = {64, (cuuint64_t)g.Cout, nkb};
+      const cuuint64_t ws[2] = {(cuuint64_t)g.Cin * 2, 128};
+      const cuuint32_t wb[3] = {BK, BM, 2};
+      if (int rc = make_map(&tmW, bf, 3, w, wd, ws, wb, "w")) return rc;
+    }
+  } else if constexpr (MODE == kNHWC3) {  // w[Cout][tap][Cin] (OHWI): dims {Cin, Cout, tap}
     const int64_t taps = g.ksize * g.ksize;
     const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout, (cuuint64_t)taps};
     const cuuint64_t ws[2] = {(cuuint64_t)(taps * g.Cin * 2), (cuuint64_t)g.Cin * 2};
@@ -1244,10 +1335,17 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
     if (int rc = make_map(&tmZ, zdt, 3, z, zd, zs, zb, "z")) return rc;
   } else {
     if constexpr (MODE == kNHWC1) {  // x as [M][Cin]
-      const cuuint64_t xd[2] = {(cuuint64_t)g.Cin, (cuuint64_t)g.M};
-      const cuuint64_t xs[1] = {(cuuint64_t)g.Cin * 2};
-      const cuuint32_t xb[2] = {BK, (cuuint32_t)(g.pair ? g.tbn / 2 : g.tbn)};
-      if (int rc = make_map(&tmX, bf, 2, x, xd, xs, xb, "x")) return rc;
+      if (g.kbs == 2) {  // {64, M, kb}
+        const cuuint64_t xd[3] = {64, (cuuint64_t)g.M, (cuuint64_t)(g.Cin / 64)};
+        const cuuint64_t xs[2] = {(cuuint64_t)g.Cin * 2, 128};
+        const cuuint32_t xb[3] = {BK, (cuuint32_t)g.tbn, 2};
+        if (int rc = make_map(&tmX, bf, 3, x, xd, xs, xb, "x")) return rc;
+      } else {
+        const cuuint64_t xd[2] = {(cuuint64_t)g.Cin, (cuuint64_t)g.M};
+        const cuuint64_t xs[1] = {(cuuint64_t)g.Cin * 2};
+        const cuuint32_t xb[2] = {BK, (cuuint32_t)(g.pair ? g.tbn / 2 : g.tbn)};
+        if (int rc = make_map(&tmX, bf, 2, x, xd, xs, xb, "x")) return rc;
+      }
     } else {
       if (int rc = make_im2col_map(&tmX, x, g.N, g.Cin, g.H, g.W, g.ksize, g.stride, g.pad,
                                    g.pair ? g.tbn / 2 : g.tbn))
@@ -1280,6 +1378,8 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
   a.splits = g.splits;
   a.kper = g.kper;
   a.ksteps = g.ksteps;
+  a.kbs = g.kbs;
+  a.kst = g.kst;
   a.units = (int)g.units;
   a.tickets = tickets;
   a.part = part;
