@@ -12,9 +12,9 @@
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(64, 1)
+__global__ void __launch_bounds__(128, 1)
     k_fill(const __grid_constant__ CUtensorMap tm, int stages, int boxes, int rows, int iters,
-           int nrows_total, unsigned long long* cyc) {
+           int nrows_total, int producers, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t stage_bytes = (uint32_t)boxes * rows * 128;
@@ -29,8 +29,9 @@ __global__ void __launch_bounds__(64, 1)
   }
   __syncthreads();
   unsigned long long t0 = clock64();
-  if (threadIdx.x == 0) {  // producer
-    for (int it = 0; it < iters; ++it) {
+  const int pw = threadIdx.x >> 5;  // producer warps 0 and 2 (lane 0) split the iterations
+  if ((threadIdx.x & 31) == 0 && (pw == 0 || (pw == 2 && producers == 2))) {  // producer
+    for (int it = pw == 0 ? 0 : 1; it < iters; it += producers) {
       const int s = it % stages;
       if (it >= stages) {
         const uint32_t par = ((it / stages) & 1) ^ 1;
@@ -80,8 +81,10 @@ int main() {
   const int cfg[][3] = {{4, 2, 128}, {6, 2, 128}, {8, 2, 128}, {6, 1, 256}, {6, 4, 64},
                         {4, 3, 128}, {3, 2, 256}, {12, 1, 128}, {6, 2, 64}, {2, 2, 128},
                         {1, 2, 128}, {12, 2, 64}};
+  for (int producers = 1; producers <= 2; ++producers)
   for (auto& c : cfg) {
     const int stages = c[0], boxes = c[1], rows = c[2];
+    if (stages % producers) continue;
     CUtensorMap tm;
     const cuuint64_t dims[2] = {64, (cuuint64_t)nrows};
     const cuuint64_t strides[1] = {128};
@@ -95,7 +98,7 @@ int main() {
     cudaFuncSetAttribute(k_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int iters = 2000;
     for (int rep = 0; rep < 2; ++rep)
-      k_fill<<<sms, 64, smem>>>(tm, stages, boxes, rows, iters, nrows, cyc);
+      k_fill<<<sms, 128, smem>>>(tm, stages, boxes, rows, iters, nrows, producers, cyc);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     unsigned long long h[148];
@@ -104,8 +107,8 @@ int main() {
     for (int i = 0; i < sms; ++i) { mx = h[i] > mx ? h[i] : mx; avg += h[i]; }
     avg /= sms;
     const double bytes = (double)iters * boxes * rows * 128;
-    printf("{\"stages\": %d, \"boxes\": %d, \"rows\": %d, \"stage_kb\": %d, \"bytes_per_clk_sm\": %.1f, \"chip_tb_s_at_1.92ghz\": %.2f}\n",
-           stages, boxes, rows, boxes * rows * 128 / 1024, bytes / avg, bytes / avg * sms * 1.92e9 / 1e12);
+    printf("{\"producers\": %d, \"stages\": %d, \"boxes\": %d, \"rows\": %d, \"stage_kb\": %d, \"bytes_per_clk_sm\": %.1f, \"chip_tb_s_at_1.92ghz\": %.2f}\n",
+           producers, stages, boxes, rows, boxes * rows * 128 / 1024, bytes / avg, bytes / avg * sms * 1.92e9 / 1e12);
   }
   return 0;
 }
