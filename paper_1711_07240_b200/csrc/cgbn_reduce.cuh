@@ -253,6 +253,7 @@ template <class T, bool PUSH = false>
 struct StatsRows {
   static constexpr int kU = 8;
   static constexpr int kIn = 1;
+  static constexpr bool kPipe = true;  // two rounds in flight when they fit (k_reduce_rows)
   StatsOp<T, 1, PUSH> base;
   Geom gg;
   struct State { double K[4]; };
@@ -311,6 +312,7 @@ template <class T, bool RELU, bool PUSH = false>
 struct BwdRows {
   static constexpr int kU = 4;
   static constexpr int kIn = 2;
+  static constexpr bool kPipe = !RELU;  // (the ReLU mask's state would spill)
   BwdOp<T, 1, RELU, PUSH> base;
   Geom gg;
   struct State { double mean[4], P[4], Q[4]; };
@@ -384,14 +386,36 @@ k_reduce_rows(NGeom g, NOp op, double2* __restrict__ slots) {
     typename NOp::State s;
     op.init(c4, s);
     constexpr int U = NOp::kU;
-    for (uint32_t r = r0 + ro; r < r1; r += U * g.rpp) {
-      typename NOp::Regs v[U];
+    // 16-bit data: two rounds in flight — round r + 1's loads are issued before round r
+    // is reduced (a round at a time left each CTA waiting out one memory latency per U
+    // rows of 8-byte loads). fp32 rounds already carry 128 B per thread and would spill.
+    constexpr bool kTwo = NOp::kPipe && sizeof(typename NOp::Regs) * U <= 64;
+    typename NOp::Regs va[U], vb[kTwo ? U : 1];
+    auto load_round = [&](uint32_t r, typename NOp::Regs (&v)[U]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t rr = r + u * g.rpp;
         if (rr < r1) op.load((size_t)rr * g.C4 + c4, v[u]);
       }
-      op.template acc_round<U>(s, v, r, r1, g.rpp, a, b);
+    };
+    const uint32_t step = U * g.rpp;
+    if constexpr (kTwo) {
+      uint32_t r = r0 + ro;
+      if (r < r1) load_round(r, va);
+      while (r < r1) {
+        if (r + step < r1) load_round(r + step, vb);
+        op.template acc_round<U>(s, va, r, r1, g.rpp, a, b);
+        r += step;
+        if (r >= r1) break;
+        if (r + step < r1) load_round(r + step, va);
+        op.template acc_round<U>(s, vb, r, r1, g.rpp, a, b);
+        r += step;
+      }
+    } else {
+      for (uint32_t r = r0 + ro; r < r1; r += step) {
+        load_round(r, va);
+        op.template acc_round<U>(s, va, r, r1, g.rpp, a, b);
+      }
     }
   }
 #pragma unroll
