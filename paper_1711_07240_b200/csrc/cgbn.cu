@@ -229,7 +229,7 @@ int CGBN_FN(cgbn_fwd_normalize_sums)(const void* x, int64_t N, int64_t C, int64_
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
   launch_pdl(k_finalize_sums, chan_blocks(C), true, st, sum, sq, count, centered ? 1 : 0, F);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st, true, w.T1);
   return check_launch("cgbn_fwd_normalize_sums");
 }
 
@@ -252,7 +252,7 @@ int CGBN_FN(cgbn_fwd_normalize)(const void* x, int64_t N, int64_t C, int64_t HW,
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
   launch_pdl(k_finalize_fwd, chan_blocks(C), true, st, parts, F);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st, true, w.T1);
   return check_launch("cgbn_fwd_normalize");
 }
 
@@ -284,12 +284,13 @@ int CGBN_FN(cgbn_fwd_train_local)(const void* x, int64_t N, int64_t C, int64_t H
   oa.out = y;
   oa.F = F;
   oa.F.P = oa.F.Q = nullptr;
+  oa.F.T1 = nullptr;
   const int oc = try_onchip<false>(act, relu != 0, N, C, HW, layout,
                                    (uintptr_t)x | (uintptr_t)y, oa, st);
   if (oc < 0) return -oc;
   if (oc == 1) return check_launch("cgbn_fwd_train_local");
   CGBN_TRY(dispatch_stats(pl, x, true, kLocalFinal, nullptr, nullptr, &F, w, st));
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st, true, w.T1);
   return check_launch("cgbn_fwd_train_local");
 }
 
@@ -310,7 +311,7 @@ int CGBN_FN(cgbn_fwd_eval)(const void* x, int64_t N, int64_t C, int64_t HW, int 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_coef_eval<<<chan_blocks(C), 256, 0, st>>>(gamma, beta, running_mean, running_var, eps, w.P,
                                               w.Q, (uint32_t)C);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);  // (fp64 tables only)
   return check_launch("cgbn_fwd_eval");
 }
 
@@ -419,6 +420,8 @@ int CGBN_FN(cgbn_bwd_local)(const void* dy, const void* x, int64_t N, int64_t C,
   oa.out = dx;
   oa.B = F;
   oa.B.A = oa.B.B = oa.B.Cc = oa.B.P = oa.B.Q = nullptr;
+  oa.B.T1 = nullptr;
+  oa.B.T2 = nullptr;
   const int oc = try_onchip<true>(act, relu != 0, N, C, HW, layout,
                                   (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, oa, st);
   if (oc < 0) return -oc;
@@ -476,6 +479,7 @@ int CGBN_FN(cgbn_fwd_fused)(const void* x, int64_t N, int64_t C, int64_t HW, int
   oa.out = y;
   oa.F = make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
   oa.F.P = oa.F.Q = nullptr;  // the coefficients stay in shared memory
+  oa.F.T1 = nullptr;
   const int oc = try_onchip<false>(act, relu != 0, N, C, HW, layout,
                                    (uintptr_t)x | (uintptr_t)y, oa,
                                    reinterpret_cast<cudaStream_t>(stream), false);
@@ -506,6 +510,8 @@ int CGBN_FN(cgbn_bwd_fused)(const void* dy, const void* x, int64_t N, int64_t C,
   oa.out = dx;
   oa.B = make_bwd_final(C, saved, gamma, beta, eps, relu != 0, dgamma, dbeta, status, w);
   oa.B.A = oa.B.B = oa.B.Cc = oa.B.P = oa.B.Q = nullptr;
+  oa.B.T1 = nullptr;
+  oa.B.T2 = nullptr;
   const int oc = try_onchip<true>(act, relu != 0, N, C, HW, layout,
                                   (uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx, oa,
                                   reinterpret_cast<cudaStream_t>(stream), false);
@@ -610,7 +616,7 @@ int CGBN_FN(cgbn_fwd_normalize_p2p)(const void* x, int64_t N, int64_t C, int64_t
   const FwdFinal F =
       make_fwd_final(C, gamma, beta, eps, momentum, running_mean, running_var, saved, status, w);
   launch_pdl(k_finalize_fwd_p2p, chan_blocks(C), true, st, pull, F);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st, true, w.T1);
   return check_launch("cgbn_fwd_normalize_p2p");
 }
 
@@ -716,7 +722,7 @@ int CGBN_FN(cgbn_fwd_normalize_slots)(const void* x, int64_t N, int64_t C, int64
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, k_finalize_slots, slot_ws, F);
-  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st);
+  launch_ew_affine(ep, relu != 0, x, y, w.P, w.Q, st, true, w.T1);
   return check_launch("cgbn_fwd_normalize_slots");
 }
 

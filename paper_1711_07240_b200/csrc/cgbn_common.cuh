@@ -362,6 +362,27 @@ __device__ __forceinline__ void stv(T* __restrict__ p, const double (&t)[V]) {
   }
 }
 
+// Round V fp32 values to the 16-bit T (pairs packed, one F2FP each) and store them as one
+// vector (the fp32 elementwise path of 16-bit activations).
+template <class T, int V>
+__device__ __forceinline__ void stvf(T* __restrict__ p, const float (&t)[V]) {
+  static_assert(sizeof(T) == 2 && V % 2 == 0, "16-bit pairs");
+  uint32_t w[V / 2];
+#pragma unroll
+  for (int k = 0; k < V / 2; ++k) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(t[2 * k], t[2 * k + 1]);
+      w[k] = *reinterpret_cast<const uint32_t*>(&b);
+    } else {
+      const __half2 b = __floats2half2_rn(t[2 * k], t[2 * k + 1]);
+      w[k] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+  }
+  if constexpr (V == 8) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  else if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  else *reinterpret_cast<uint32_t*>(p) = w[0];
+}
+
 // Loads in flight per thread per round: ~128 B for one input stream, ~128 B total for
 // two (NIN = number of input streams).
 #ifndef CGBN_RED_U1

@@ -201,10 +201,95 @@ constexpr int kEwU = CGBN_EWU;  // 16-byte units per elementwise thread (one rou
 template <class T>
 constexpr int ew_ue() { return 16 / (int)sizeof(T); }
 
+// fp32 records of the 16-bit passes (cgbn_ops.cuh FwdFinal / BwdFinal T1, T2) for the UE
+// channels of a channels_last unit at element e (CM 3), or one channel's record.
+template <int UE, class R>
+__device__ __forceinline__ void ew_rec_unit(const EwGeom& g, const R* __restrict__ T, uint32_t e,
+                                            R (&r)[UE]) {
+  const uint32_t c0 = e - g.dc.div(e) * g.C;
+#pragma unroll
+  for (int k = 0; k < UE; ++k) r[k] = __ldg(T + c0 + k);
+}
+
+// The 16-bit activations' normalise without ReLU, in fp32 (the output keeps 8 / 11
+// significant bits): y = P ((x - mean_hi) - mean_lo) + beta. x is exact in fp32, the mean
+// a float pair, so the difference keeps ~2^-23 relative error whatever |mean| / std, and
+// y ~2^-22 — against the output's 2^-8 (bf16) / 2^-11 (fp16) rounding. No fp64 conversion
+// (these bound the fp64 path: XU pipe 66% busy, tools/gpu/ncu_bf16.sh).
+template <class T, int CM, int U>
+__device__ __forceinline__ void ew_affine_f32(const EwGeom& g, const T* __restrict__ x,
+                                              T* __restrict__ y, const float4* __restrict__ T1) {
+  constexpr int UE = ew_ue<T>();
+  pdl_trigger();
+  const uint32_t stride = gridDim.x * kThreads;
+  uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  Vec<T, UE> v[U];
+  auto load = [&](uint32_t i0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < g.n4) v[u].load(x + (size_t)UE * ew_unit(g, i0 + u * stride));
+  };
+  load(i);
+  pdl_wait();
+  constexpr bool kReuse = CM == 3;
+  float4 tr[kReuse ? UE : 1];
+  if constexpr (kReuse) {
+    if (g.reuse && i < g.n4) ew_rec_unit<UE>(g, T1, UE * ew_unit(g, i), tr);
+  }
+  for (; i < g.n4; i += U * stride) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = i + u * stride;
+      if (j >= g.n4) continue;
+      const uint32_t jm = ew_unit(g, j);
+      float o[UE];
+      if constexpr (CM == 0) {  // one channel per unit
+        const float4 t = __ldg(T1 + chan_of<0>(g, UE * jm));
+#pragma unroll
+        for (int k = 0; k < UE; ++k) o[k] = fmaf(t.x, (v[u].get(k) - t.y) - t.z, t.w);
+      } else {
+#pragma unroll
+        for (int h = 0; h < UE; h += 4) {
+          float4 t[4];
+          if (kReuse && g.reuse) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) t[k] = tr[kReuse ? h + k : 0];
+          } else {
+            uint32_t c[4];
+            chan4<CM>(g, UE * jm + h, c);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) t[k] = __ldg(T1 + c[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            o[h + k] = fmaf(t[k].x, (v[u].get(h + k) - t[k].y) - t[k].z, t[k].w);
+        }
+      }
+      stvf<T, UE>(y + (size_t)UE * jm, o);
+    }
+    load(i + U * stride);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < g.tail) {
+    const uint32_t e = UE * g.n4 + threadIdx.x;
+    const uint32_t c = CM >= 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
+    const float4 t = __ldg(T1 + c);
+    st1(y + e, (double)fmaf(t.x, (ld1(x + e) - t.y) - t.z, t.w));
+  }
+}
+
 template <class T, bool RELU, int CM, int U>
 __global__ void __launch_bounds__(kThreads)
 k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
-            const double* __restrict__ P, const double* __restrict__ Q) {
+            const double* __restrict__ P, const double* __restrict__ Q,
+            const float4* __restrict__ T1) {
+  // (NCHW only: with channels_last units of 8 channels the per-channel records cost more
+  // than the conversions they save — step 2.16 -> 2.50 ms, profiles/r2_negative)
+  if constexpr (sizeof(T) == 2 && !RELU && CM <= 1) {
+    if (T1 != nullptr) {  // training forward: the finisher wrote the fp32 records
+      ew_affine_f32<T, CM, U>(g, x, y, T1);
+      return;
+    }
+  }
   constexpr int UE = ew_ue<T>();
   pdl_trigger();  // the next reduction may launch and wait
   const uint32_t stride = gridDim.x * kThreads;
@@ -267,12 +352,104 @@ k_ew_affine(EwGeom g, const T* __restrict__ x, T* __restrict__ y,
   }
 }
 
+// The 16-bit activations' dx without ReLU, in fp32: dx = A g + B ((x - mean_hi) - mean_lo)
+// + C3 with C3 = Cc + B mean (= -A dbeta / m), the same error argument as ew_affine_f32.
+template <class T, int CM, int U>
+__device__ __forceinline__ void ew_dx_f32(const EwGeom& g, const T* __restrict__ dy,
+                                          const T* __restrict__ x, T* __restrict__ dx,
+                                          const float4* __restrict__ T1,
+                                          const float2* __restrict__ T2) {
+  constexpr int UE = ew_ue<T>();
+  pdl_trigger();
+  const uint32_t stride = gridDim.x * kThreads;
+  uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  Vec<T, UE> gv[U], xv[U];
+  auto load = [&](uint32_t i0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < g.n4) {
+        const size_t off = (size_t)UE * ew_unit(g, i0 + u * stride);
+        gv[u].load(dy + off);
+        xv[u].load(x + off);
+      }
+  };
+  load(i);
+  pdl_wait();
+  constexpr bool kReuse = CM == 3;
+  float4 tr[kReuse ? UE : 1];
+  float2 mr[kReuse ? UE : 1];
+  if constexpr (kReuse) {
+    if (g.reuse && i < g.n4) {
+      ew_rec_unit<UE>(g, T1, UE * ew_unit(g, i), tr);
+      ew_rec_unit<UE>(g, T2, UE * ew_unit(g, i), mr);
+    }
+  }
+  for (; i < g.n4; i += U * stride) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = i + u * stride;
+      if (j >= g.n4) continue;
+      const uint32_t jm = ew_unit(g, j);
+      float o[UE];
+      if constexpr (CM == 0) {
+        const uint32_t c = chan_of<0>(g, UE * jm);
+        const float4 t = __ldg(T1 + c);
+        const float2 m = __ldg(T2 + c);
+#pragma unroll
+        for (int k = 0; k < UE; ++k)
+          o[k] = fmaf(t.x, gv[u].get(k), fmaf(t.y, (xv[u].get(k) - m.x) - m.y, t.z));
+      } else {
+#pragma unroll
+        for (int h = 0; h < UE; h += 4) {
+          float4 t[4];
+          float2 m[4];
+          if (kReuse && g.reuse) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              t[k] = tr[kReuse ? h + k : 0];
+              m[k] = mr[kReuse ? h + k : 0];
+            }
+          } else {
+            uint32_t c[4];
+            chan4<CM>(g, UE * jm + h, c);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              t[k] = __ldg(T1 + c[k]);
+              m[k] = __ldg(T2 + c[k]);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            o[h + k] = fmaf(t[k].x, gv[u].get(h + k),
+                            fmaf(t[k].y, (xv[u].get(h + k) - m[k].x) - m[k].y, t[k].z));
+        }
+      }
+      stvf<T, UE>(dx + (size_t)UE * jm, o);
+    }
+    load(i + U * stride);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < g.tail) {
+    const uint32_t e = UE * g.n4 + threadIdx.x;
+    const uint32_t c = CM >= 2 ? chan_of<2>(g, e) : chan_of<1>(g, e);
+    const float4 t = __ldg(T1 + c);
+    const float2 m = __ldg(T2 + c);
+    st1(dx + e, (double)fmaf(t.x, ld1(dy + e), fmaf(t.y, (ld1(x + e) - m.x) - m.y, t.z)));
+  }
+}
+
 template <class T, bool RELU, int CM, int U>
 __global__ void __launch_bounds__(kThreads)
 k_ew_dx(EwGeom g, const T* __restrict__ dy, const T* __restrict__ x, T* __restrict__ dx,
         const double* __restrict__ A, const double* __restrict__ B,
         const double* __restrict__ Cc, const double* __restrict__ P,
-        const double* __restrict__ Q) {
+        const double* __restrict__ Q, const float4* __restrict__ T1,
+        const float2* __restrict__ T2) {
+  if constexpr (sizeof(T) == 2 && !RELU && CM <= 1) {  // (NCHW only, as k_ew_affine)
+    if (T1 != nullptr) {  // the backward finisher wrote the fp32 records
+      ew_dx_f32<T, CM, U>(g, dy, x, dx, T1, T2);
+      return;
+    }
+  }
   constexpr int UE = ew_ue<T>();
   pdl_trigger();  // the next reduction may launch and wait
   const uint32_t stride = gridDim.x * kThreads;

@@ -90,7 +90,8 @@ size_t slots_bytes(int64_t N, int64_t C, int64_t HW, int layout, int sms) {
   return n * sizeof(double2);
 }
 size_t ws_bytes_for(int64_t N, int64_t C, int64_t HW, int layout, int sms) {
-  return kTicketBytes + slots_bytes(N, C, HW, layout, sms) + 5 * (size_t)C * sizeof(double);
+  // coefficients: P, Q, A, B, Cc (fp64), then the fp32 records T1 (float4) and T2 (float2)
+  return kTicketBytes + slots_bytes(N, C, HW, layout, sms) + (8 * (size_t)C + 2) * sizeof(double);
 }
 
 struct WsView {
@@ -102,6 +103,8 @@ struct WsView {
   double* A;
   double* B;
   double* Cc;
+  float4* T1;  // fp32 records of the 16-bit elementwise passes (cgbn_ops.cuh)
+  float2* T2;
 };
 
 int ws_view(void* ws, size_t ws_bytes, int64_t N, int64_t C, int64_t HW, int layout,
@@ -124,6 +127,8 @@ int ws_view(void* ws, size_t ws_bytes, int64_t N, int64_t C, int64_t HW, int lay
   v->A = coef + 2 * C;
   v->B = coef + 3 * C;
   v->Cc = coef + 4 * C;
+  v->T1 = reinterpret_cast<float4*>(coef + ((5 * C + 1) & ~(int64_t)1));  // 16-byte aligned
+  v->T2 = reinterpret_cast<float2*>(reinterpret_cast<double*>(v->T1) + 2 * C);
   return CGBN_OK;
 }
 
@@ -735,35 +740,39 @@ unsigned ew_grid_geom(K kernel, const EwPlan& ep, EwGeom* g, int units) {
 
 template <class T, bool RELU, int CM>
 void launch_ew_affine_t(const EwPlan& ep, const void* x, void* y, const double* P,
-                        const double* Q, bool pdl, cudaStream_t st) {
+                        const double* Q, const float4* T1, bool pdl, cudaStream_t st) {
   EwGeom g;
   constexpr int U = ew_units<CM>();
   const unsigned grid = ew_grid_geom(k_ew_affine<T, RELU, CM, U>, ep, &g, U);
   launch_pdl(k_ew_affine<T, RELU, CM, U>, grid, pdl, st, g, static_cast<const T*>(x),
-             static_cast<T*>(y), P, Q);
+             static_cast<T*>(y), P, Q, T1);
 }
 
 template <class T, bool RELU>
 void launch_ew_affine_r(const EwPlan& ep, int cm, const void* x, void* y, const double* P,
-                        const double* Q, bool pdl, cudaStream_t st) {
-  if (cm == 0) launch_ew_affine_t<T, RELU, 0>(ep, x, y, P, Q, pdl, st);
-  else if (cm == 1) launch_ew_affine_t<T, RELU, 1>(ep, x, y, P, Q, pdl, st);
-  else if (cm == 2) launch_ew_affine_t<T, RELU, 2>(ep, x, y, P, Q, pdl, st);
-  else launch_ew_affine_t<T, RELU, 3>(ep, x, y, P, Q, pdl, st);
+                        const double* Q, const float4* T1, bool pdl, cudaStream_t st) {
+  if (cm == 0) launch_ew_affine_t<T, RELU, 0>(ep, x, y, P, Q, T1, pdl, st);
+  else if (cm == 1) launch_ew_affine_t<T, RELU, 1>(ep, x, y, P, Q, T1, pdl, st);
+  else if (cm == 2) launch_ew_affine_t<T, RELU, 2>(ep, x, y, P, Q, T1, pdl, st);
+  else launch_ew_affine_t<T, RELU, 3>(ep, x, y, P, Q, T1, pdl, st);
 }
 
 template <class T>
 void launch_ew_affine_d(const EwPlan& ep, int cm, bool relu, const void* x, void* y,
-                        const double* P, const double* Q, bool pdl, cudaStream_t st) {
-  if (relu) launch_ew_affine_r<T, true>(ep, cm, x, y, P, Q, pdl, st);
-  else launch_ew_affine_r<T, false>(ep, cm, x, y, P, Q, pdl, st);
+                        const double* P, const double* Q, const float4* T1, bool pdl,
+                        cudaStream_t st) {
+  if (relu) launch_ew_affine_r<T, true>(ep, cm, x, y, P, Q, T1, pdl, st);
+  else launch_ew_affine_r<T, false>(ep, cm, x, y, P, Q, T1, pdl, st);
 }
 
+// T1: the forward finisher's fp32 records (16-bit activations, no ReLU: the fp32 path of
+// k_ew_affine), or null for caller-provided tables (eval, x_hat, channel_affine).
 void launch_ew_affine(const EwPlan& ep, bool relu, const void* x, void* y, const double* P,
-                      const double* Q, cudaStream_t st, bool pdl = true) {
+                      const double* Q, cudaStream_t st, bool pdl = true,
+                      const float4* T1 = nullptr) {
   int cm = ep.cm;
   if (cm == 3 && (((uintptr_t)P | (uintptr_t)Q) % 16) != 0) cm = 2;  // caller's tables
-  launch_ew_affine_d<TuAct>(ep, cm, relu, x, y, P, Q, pdl, st);
+  launch_ew_affine_d<TuAct>(ep, cm, relu, x, y, P, Q, T1, pdl, st);
 }
 
 template <class T, bool RELU, int CM>
@@ -775,7 +784,7 @@ void launch_ew_dx_t(const EwPlan& ep, const void* dy, const void* x, void* dx, c
   launch_pdl(k_ew_dx<T, RELU, CM, U>, grid, true, st, g,
              static_cast<const T*>(dy), static_cast<const T*>(x), static_cast<T*>(dx),
              (const double*)w.A, (const double*)w.B, (const double*)w.Cc, (const double*)w.P,
-             (const double*)w.Q);
+             (const double*)w.Q, (const float4*)w.T1, (const float2*)w.T2);
 }
 
 template <class T, bool RELU>
@@ -810,6 +819,7 @@ FwdFinal make_fwd_final(int64_t C, const float* gamma, const float* beta, double
   F.rmean = rm; F.rvar = rv;
   F.saved = saved;
   F.P = w.P; F.Q = w.Q;
+  F.T1 = w.T1;
   F.status = status;
   F.C = (uint32_t)C;
   return F;
@@ -823,6 +833,7 @@ BwdFinal make_bwd_final(int64_t C, const double* saved, const float* gamma, cons
   F.eps = eps;
   F.relu = relu ? 1 : 0;
   F.A = w.A; F.B = w.B; F.Cc = w.Cc; F.P = w.P; F.Q = w.Q;
+  F.T1 = w.T1; F.T2 = w.T2;
   F.dgamma = dgamma; F.dbeta = dbeta;
   F.status = status;
   F.C = (uint32_t)C;

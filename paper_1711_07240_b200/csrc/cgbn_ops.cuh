@@ -85,6 +85,7 @@ struct FwdFinal {
   double* saved;  // [mean C | var C | inv_std C | m]
   double* P;      // coefficient table (null when the caller keeps the coefficients)
   double* Q;
+  float4* T1;     // fp32 record {P, mean_hi, mean_lo, beta} for 16-bit activations (or null)
   unsigned* status;
   uint32_t C;
 };
@@ -120,6 +121,10 @@ __device__ __forceinline__ void finalize_fwd_channel_var(const FwdFinal& F, uint
   const double inv_std = 1.0 / sqrt(var + F.eps);
   affine_coeffs(mean, inv_std, (double)v.gamma, (double)v.beta, P, Q);
   if (F.P) { F.P[c] = P; F.Q[c] = Q; }
+  if (F.T1) {  // y = P (x - mean) + beta in fp32, the mean as a float pair (no cancellation)
+    const float mh = (float)mean;
+    F.T1[c] = make_float4((float)P, mh, (float)(mean - (double)mh), v.beta);
+  }
   if (!write) return;
   const uint32_t C = F.C;
   F.saved[c] = mean;
@@ -167,6 +172,8 @@ struct BwdFinal {
   double* Cc;
   double* P;
   double* Q;
+  float4* T1;     // fp32 records for 16-bit activations (or null): {A, B, C3, 0} with
+  float2* T2;     // dx = A g + B (x - mean) + C3 and the mean as a float pair {hi, lo}
   float* dgamma;  // may be null
   float* dbeta;
   unsigned* status;
@@ -227,6 +234,11 @@ __device__ __forceinline__ DxCoef finalize_bwd_channel(const BwdFinal& F, uint32
     F.Cc[c] = k.Cc;
     F.P[c] = k.P;
     F.Q[c] = k.Q;
+  }
+  if (F.T1) {
+    const float mh = (float)mean;
+    F.T1[c] = make_float4((float)k.A, (float)k.B, (float)(k.Cc + k.B * mean), 0.f);
+    F.T2[c] = make_float2(mh, (float)(mean - (double)mh));
   }
   if (write) {
     if (F.dgamma) F.dgamma[c] = (float)dgamma;
