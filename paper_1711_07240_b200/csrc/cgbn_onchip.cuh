@@ -251,7 +251,21 @@ __device__ __forceinline__ void acc_unit(uint32_t ax, uint32_t ag, uint32_t mask
                                          double P, double Q, double& a, double& b) {
   float xv[VE];
   lds_vec<T, VE>(ax, xv);
-  if constexpr (!BWD) {
+  if constexpr (!BWD && sizeof(T) == 2) {
+    // 16-bit activations, as the split statistics kernels: K (a 16-bit value) and x are
+    // exact in fp32, the unit's differences and squares are summed in fp32 and added once
+    const float Kf = (float)K;
+    float s = 0.f, q = 0.f;
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      if (MASKED && !((mask >> e) & 1u)) continue;
+      const float d = xv[e] - Kf;
+      s += d;
+      q = __fmaf_rn(d, d, q);
+    }
+    a += (double)s;
+    b += (double)q;
+  } else if constexpr (!BWD) {
 #pragma unroll
     for (int e = 0; e < VE; ++e) {
       if (MASKED && !((mask >> e) & 1u)) continue;
@@ -259,6 +273,19 @@ __device__ __forceinline__ void acc_unit(uint32_t ax, uint32_t ag, uint32_t mask
       a += d;
       b = __fma_rn(d, d, b);
     }
+  } else if constexpr (sizeof(T) == 2 && !RELU) {
+    // 16-bit backward: sum g in an fp32 partial of the unit; g*(x - mean) in fp64 per
+    // element (BwdOp::acc explains why)
+    float gv[VE];
+    lds_vec<T, VE>(ag, gv);
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      if (MASKED && !((mask >> e) & 1u)) continue;
+      s += gv[e];
+      b = __fma_rn((double)gv[e], (double)xv[e] - K, b);
+    }
+    a += (double)s;
   } else {
     float gv[VE];
     lds_vec<T, VE>(ag, gv);
@@ -296,6 +323,10 @@ k_onchip(OGeom g, Args a) {
   constexpr int UE = 16 / (int)es;  // elements per 16-byte chunk
   constexpr bool ALIGNED = VE == UE;
   constexpr uint32_t NIN = BWD ? 2 : 1;
+  // 16-bit activations without ReLU, aligned planes: the write pass in fp32 from fp32
+  // records the finisher leaves in c01 / c2 (the split kernels' k_ew_affine / k_ew_dx
+  // fp32 form, cgbn_ew.cuh: no fp64 conversion per element)
+  constexpr bool kF32W = sizeof(T) == 2 && !RELU && ALIGNED;
   extern __shared__ __align__(16) unsigned char smem[];
   Head& H = *reinterpret_cast<Head*>(smem);
   const uint32_t KC = g.KC;
@@ -508,7 +539,13 @@ k_onchip(OGeom g, Args a) {
       }
       double P, Q;
       finalize_fwd_channel(a.F, c, n, mean, M2, write, ca.pre[i], P, Q);
-      ca.c01[i] = make_double2(P, Q);
+      if constexpr (kF32W) {  // the fp32 write below: {P, mean_hi, mean_lo, beta}
+        const float mh = (float)mean;
+        reinterpret_cast<float4*>(ca.c01)[i] =
+            make_float4((float)P, mh, (float)(mean - (double)mh), ca.pre[i].beta);
+      } else {
+        ca.c01[i] = make_double2(P, Q);
+      }
     } else {
       double S1 = 0.0, S2 = 0.0;
       for (uint32_t u = 0; u < KC; ++u) {
@@ -521,8 +558,17 @@ k_onchip(OGeom g, Args a) {
         continue;
       }
       const DxCoef k = finalize_bwd_channel(a.B, c, S1, S2, write, ca.pre[i]);
-      ca.c01[i] = make_double2(k.A, k.B);
-      ca.c2[i] = make_double2(k.Cc, 0.0);
+      if constexpr (kF32W) {  // {A, B, C3 = Cc + B mean, mean_hi}, {mean_lo}
+        const double mean = ca.pre[i].mean;
+        const float mh = (float)mean;
+        reinterpret_cast<float4*>(ca.c01)[i] =
+            make_float4((float)k.A, (float)k.B, (float)(k.Cc + k.B * mean), mh);
+        reinterpret_cast<float4*>(ca.c2)[i] =
+            make_float4((float)(mean - (double)mh), 0.f, 0.f, 0.f);
+      } else {
+        ca.c01[i] = make_double2(k.A, k.B);
+        ca.c2[i] = make_double2(k.Cc, 0.0);
+      }
     }
   }
   if (KC > 1) cluster_arrive_relaxed();  // done reading the peers' partials
@@ -541,6 +587,23 @@ k_onchip(OGeom g, Args a) {
       const uint32_t sx = data + k * kstride + xoff + qq * 16;
       float xv[UE];
       lds_vec<T, UE>(sx, xv);
+      if constexpr (kF32W) {
+        float of[UE];
+        const float4 t = reinterpret_cast<const float4*>(ca.c01)[i];
+        if constexpr (!BWD) {
+#pragma unroll
+          for (int e = 0; e < UE; ++e) of[e] = fmaf(t.x, (xv[e] - t.y) - t.z, t.w);
+        } else {
+          float gv[UE];
+          lds_vec<T, UE>(sx - xoff, gv);
+          const float ml = reinterpret_cast<const float4*>(ca.c2)[i].x;
+#pragma unroll
+          for (int e = 0; e < UE; ++e)
+            of[e] = fmaf(t.x, gv[e], fmaf(t.y, (xv[e] - t.w) - ml, t.z));
+        }
+        stvf<T, UE>(og + run_start(k) + (size_t)qq * UE, of);
+        continue;
+      }
       double o[UE];
       if constexpr (!BWD) {
         const double2 pq = ca.c01[i];
