@@ -124,3 +124,18 @@ def test_dtype_units_share_the_error_message(act):
     assert rc == _lib.ERR_INVALID and b"dtype" in lib.cgbn_last_error()
     for name in ("cgbn_fwd_stats_a0", "cgbn_fwd_stats_a1", "cgbn_fwd_stats_a2"):
         assert hasattr(lib, name)
+
+
+def test_conv_workspace_plan_without_gpu():
+    """The conv workspace (ABI v7) sizes itself from the host-side plan: statistics slots,
+    then split-K partials for layers the plan splits (the 3x3 512-channel layers: 52 tiles
+    of 128 pixels, 72 k-steps), then the 16 KB ticket region every layer keeps."""
+    lib = _lib.load()
+    slots_only = lib.cgbn_conv_nhwc_ws_bytes(32, 256, 256, 14, 14, 3, 1)  # not split
+    split = lib.cgbn_conv_nhwc_ws_bytes(32, 512, 512, 7, 7, 3, 1)
+    assert slots_only > 16384 and split > slots_only
+    # 52 tiles x (2 - 1) partials x 128 x 128 fp32 beyond the slot table
+    slots_512 = lib.cgbn_conv_nhwc_ws_bytes(32, 64, 512, 7, 7, 1, 1)  # Cin 64: never split
+    assert split - slots_512 == 52 * 128 * 128 * 4
+    assert lib.cgbn_conv_nhwc_ws_bytes(32, 64, 64, 7, 7, 2, 1) == 0  # ksize 2: invalid
+    assert lib.cgbn_conv1x1_ws_bytes(0, 64, 64, 49) == 0
