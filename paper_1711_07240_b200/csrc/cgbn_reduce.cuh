@@ -248,10 +248,20 @@ struct NGeom {
   uint32_t nb;       // row blocks per slice
 };
 
+// fp32 rows per round (statistics / backward reduction without ReLU): 4 / 2 with two
+// rounds in flight measured better than 8 / 4 one at a time (channels_last fp32 step
+// 2.507 -> 2.467 ms, no spills; tools/gpu/rows_ab.sh, profiles/r2_rows_ab/)
+#ifndef CGBN_ROWS_U32
+#define CGBN_ROWS_U32 4
+#endif
+#ifndef CGBN_ROWS_BU32
+#define CGBN_ROWS_BU32 2
+#endif
+
 // Forward statistics over rows: the shift K of every channel is the NCHW op's (row 0).
 template <class T, bool PUSH = false>
 struct StatsRows {
-  static constexpr int kU = 8;
+  static constexpr int kU = sizeof(T) == 4 ? CGBN_ROWS_U32 : 8;
   static constexpr int kIn = 1;
   static constexpr bool kPipe = true;  // two rounds in flight when they fit (k_reduce_rows)
   StatsOp<T, 1, PUSH> base;
@@ -310,7 +320,7 @@ struct StatsRows {
 // Backward sums over rows: [sum g, sum g*(x - mean)] with the forward's ReLU mask.
 template <class T, bool RELU, bool PUSH = false>
 struct BwdRows {
-  static constexpr int kU = 4;
+  static constexpr int kU = sizeof(T) == 4 && !RELU ? CGBN_ROWS_BU32 : 4;
   static constexpr int kIn = 2;
   static constexpr bool kPipe = !RELU;  // (the ReLU mask's state would spill)
   BwdOp<T, 1, RELU, PUSH> base;
@@ -386,9 +396,9 @@ k_reduce_rows(NGeom g, NOp op, double2* __restrict__ slots) {
     typename NOp::State s;
     op.init(c4, s);
     constexpr int U = NOp::kU;
-    // 16-bit data: two rounds in flight — round r + 1's loads are issued before round r
-    // is reduced (a round at a time left each CTA waiting out one memory latency per U
-    // rows of 8-byte loads). fp32 rounds already carry 128 B per thread and would spill.
+    // Two rounds in flight when a round's registers fit in 64 bytes (16-bit data; fp32
+    // with 4 / 2 rows per round): round r + 1's loads are issued before round r is
+    // reduced (a round at a time left each CTA waiting out one memory latency per round).
     constexpr bool kTwo = NOp::kPipe && sizeof(typename NOp::Regs) * U <= 64;
     typename NOp::Regs va[U], vb[kTwo ? U : 1];
     auto load_round = [&](uint32_t r, typename NOp::Regs (&v)[U]) {
