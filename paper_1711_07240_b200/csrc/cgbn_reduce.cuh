@@ -257,11 +257,17 @@ struct NGeom {
 #ifndef CGBN_ROWS_BU32
 #define CGBN_ROWS_BU32 2
 #endif
+#ifndef CGBN_ROWS_U16
+#define CGBN_ROWS_U16 8  // 16-bit rows per round, statistics / backward (A/B knobs)
+#endif
+#ifndef CGBN_ROWS_BU16
+#define CGBN_ROWS_BU16 4
+#endif
 
 // Forward statistics over rows: the shift K of every channel is the NCHW op's (row 0).
 template <class T, bool PUSH = false>
 struct StatsRows {
-  static constexpr int kU = sizeof(T) == 4 ? CGBN_ROWS_U32 : 8;
+  static constexpr int kU = sizeof(T) == 4 ? CGBN_ROWS_U32 : CGBN_ROWS_U16;
   static constexpr int kIn = 1;
   static constexpr bool kPipe = true;  // two rounds in flight when they fit (k_reduce_rows)
   StatsOp<T, 1, PUSH> base;
@@ -320,7 +326,7 @@ struct StatsRows {
 // Backward sums over rows: [sum g, sum g*(x - mean)] with the forward's ReLU mask.
 template <class T, bool RELU, bool PUSH = false>
 struct BwdRows {
-  static constexpr int kU = sizeof(T) == 4 && !RELU ? CGBN_ROWS_BU32 : 4;
+  static constexpr int kU = sizeof(T) == 4 ? (RELU ? 4 : CGBN_ROWS_BU32) : CGBN_ROWS_BU16;
   static constexpr int kIn = 2;
   static constexpr bool kPipe = !RELU;  // (the ReLU mask's state would spill)
   BwdOp<T, 1, RELU, PUSH> base;
