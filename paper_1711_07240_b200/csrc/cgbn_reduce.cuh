@@ -326,7 +326,7 @@ struct StatsRows {
 // Backward sums over rows: [sum g, sum g*(x - mean)] with the forward's ReLU mask.
 template <class T, bool RELU, bool PUSH = false>
 struct BwdRows {
-  static constexpr int kU = sizeof(T) == 4 ? (RELU ? 4 : CGBN_ROWS_BU32) : CGBN_ROWS_BU16;
+  static constexpr int kU = sizeof(T) == 4 ? CGBN_ROWS_BU32 : CGBN_ROWS_BU16;
   static constexpr int kIn = 2;
   static constexpr bool kPipe = !RELU;  // (the ReLU mask's state would spill)
   BwdOp<T, 1, RELU, PUSH> base;

@@ -38,13 +38,7 @@ __device__ __forceinline__ void merge(const Slot* __restrict__ slots, int Cout, 
   const int mt = c / 128;
   double n = 0.0, A = 0.0, B = 0.0, K0 = 0.0;
   if (c < Cout) {
-    Slot p[kFoldPerWarp];  // every load of this warp in flight at once
-#pragma unroll
-    for (int u = 0; u < kFoldPerWarp; ++u) {
-      const int s = w + 32 * u;
-      const bool ok = s < nslots && (s >> 1) * mtiles + mt < grid;
-      p[u] = ok ? slots[(size_t)s * Cout + c] : Slot{0.0, 0.0, 0.0};
-    }
+    Slot p[kFoldPerWarp];
     // the shift: the first non-empty slot's mean (a CTA that only ran non-final split-K
     // ranges leaves n = 0 slots)
     for (int s = 0; s < nslots; ++s) {
@@ -55,13 +49,25 @@ __device__ __forceinline__ void merge(const Slot* __restrict__ slots, int Cout, 
         break;
       }
     }
+    // two halves of kFoldPerWarp / 2 loads in flight (all of them at once spilled at the
+    // 1024-thread block's 64-register cap); the adds keep the u order
+    constexpr int kHalf = kFoldPerWarp / 2;
 #pragma unroll
-    for (int u = 0; u < kFoldPerWarp; ++u) {
-      if (p[u].n == 0.0) continue;
-      const double d = p[u].mean - K0;
-      n += p[u].n;
-      A = fma(p[u].n, d, A);
-      B += fma(p[u].n * d, d, p[u].M2);
+    for (int h = 0; h < kFoldPerWarp; h += kHalf) {
+#pragma unroll
+      for (int u = h; u < h + kHalf; ++u) {
+        const int s = w + 32 * u;
+        const bool ok = s < nslots && (s >> 1) * mtiles + mt < grid;
+        p[u] = ok ? slots[(size_t)s * Cout + c] : Slot{0.0, 0.0, 0.0};
+      }
+#pragma unroll
+      for (int u = h; u < h + kHalf; ++u) {
+        if (p[u].n == 0.0) continue;
+        const double d = p[u].mean - K0;
+        n += p[u].n;
+        A = fma(p[u].n, d, A);
+        B += fma(p[u].n * d, d, p[u].M2);
+      }
     }
   }
   sn[w][lane] = n;
