@@ -383,17 +383,18 @@ __device__ __forceinline__ void stvf(T* __restrict__ p, const float (&t)[V]) {
   else *reinterpret_cast<uint32_t*>(p) = w[0];
 }
 
-// Loads in flight per thread per round: 64 B for one input stream, 64 B total for two
+// Loads in flight per thread per round: 64 B for one input stream, 32 B total for two
 // (NIN = number of input streams).
-// 4 / 2 (round 2): the same fp32 step as 8 / 4 (2.092 vs 2.095 ms, backward reduction
-// +1%) without the 16-124 B spills of 60 fp32 reduction instantiations at the 64-register
-// cap, and a faster 16-bit step (bf16 ResNet-50 1.525 -> 1.468 ms: statistics +8%,
-// backward reduction +5%); profiles/r2_red_ab/.
+// Round 2, measured on the ResNet-50 steps (profiles/r2_red_ab/): 8 / 4 (round 1) ->
+// 4 / 2 kept the fp32 step (2.095 -> 2.092 ms) without the 16-124 B spills of 60 fp32
+// reduction instantiations at the 64-register cap and sped up bf16 (1.525 -> 1.468 ms);
+// 4 / 1 then gained the backward reduction another 3-5% (fp32 2.091 -> 2.077 ms, bf16
+// 1.468 -> 1.449 ms); 2 / 1 lost on the statistics.
 #ifndef CGBN_RED_U1
 #define CGBN_RED_U1 4  // loads in flight per thread per round, one input stream
 #endif
 #ifndef CGBN_RED_U2
-#define CGBN_RED_U2 2  // units per round with two input streams (dy, x)
+#define CGBN_RED_U2 1  // units per round with two input streams (dy, x)
 #endif
 #ifndef CGBN_CT_MINB
 #define CGBN_CT_MINB 4  // k_reduce_ct CTAs per SM (register bound)
