@@ -969,6 +969,11 @@ bool onchip_plan_t(int64_t N, int64_t C, int64_t HW, OnchipPlan* p, bool capped)
   // explicit *_fused entry points (any layer that fits in one resident wave)
   const double max_frac = !capped ? 1.0 : es == 4 ? env.max_frac4 : env.max_frac2;
   if ((double)total > max_frac * (double)(S * smem_sm)) return false;
+  // a single image has no image split to spread over a cluster: with cold inputs the
+  // split path measured slightly faster ([1,2048,7,7] fwd+bwd 11.9 vs 12.3 us,
+  // tools/gpu/lat_sweep.sh, profiles/r2_knobs/lat_sweep/); the explicit *_fused entry
+  // points still run it on chip
+  if (capped && N == 1) return false;
   const size_t head = ((sizeof(onchip::Head) + 15) / 16) * 16;
   double best = 1e300;
   bool found = false;

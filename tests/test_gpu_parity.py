@@ -373,6 +373,8 @@ def test_fused_eligibility():
     assert lib.cgbn_onchip_selected(32, 64, 3136, 0, 0) == 0
     assert lib.cgbn_onchip_selected(32, 256, 196, 0, 1) == 1
     assert lib.cgbn_onchip_selected(32, 256, 196, _lib.ACT_BF16, 0) == 0  # 16-bit: off
+    assert lib.cgbn_onchip_selected(1, 2048, 49, 0, 0) == 0       # one image: split path
+    assert lib.cgbn_fused_supported(1, 2048, 49, 0, 0) == 1       # (forced: still on chip)
 
 
 def test_fused_run_to_run_bitwise_and_matches_split_closely():
