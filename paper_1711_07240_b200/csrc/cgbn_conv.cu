@@ -393,6 +393,10 @@ struct ConvArgs {
   // the others' fp32 partials (part) once its ticket shows them all written
   int splits, kper, ksteps, units;
   int kbs, kst;       // k-blocks per ring stage (1 or 2); stages per tap = ceil(kblocks / kbs)
+  // bytes of W per k-block: 128 rows x 128 B, or 64 rows for Cout <= 64 (the MMA still
+  // runs M = 128; TMEM lanes 64..127 then hold products of stale shared memory that no
+  // epilogue warp reads — warps 2 and 3 of each half are inactive for such layers)
+  uint32_t wbytes;
   int* tickets;       // [tiles], zero between launches (the last split resets its own)
   float* part;        // [tiles][splits - 1][128 x 128]
   unsigned long long* trace;  // debug (cgbn_debug_conv_trace): [CTA][16 units][8 stamps]
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps pe
                                       (uint16_t)ty);
             }
           } else if constexpr (MODE == kNCHW1) {
-            mbar_expect_tx(&full[s], T::kStage);
+            mbar_expect_tx(&full[s], T::kStage - kTileA + a.wbytes);
             tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
 #pragma unroll
             for (int j = 0; j < TBN / 64; ++j)  // 64-pixel boxes of 8 KB
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps pe
             // stride s: the traversal walks input positions s apart)
             const int nk = min(a.kbs, a.kblocks - kb);  // k-blocks of this stage
             if constexpr (MODE == kNHWC1) {
-              mbar_expect_tx(&full[s], (uint32_t)a.kbs * (kTileA + T::kTileB1));
+              mbar_expect_tx(&full[s], (uint32_t)a.kbs * (a.wbytes + T::kTileB1));
               if (a.kbs == 1) {
                 tma_load_2d(A, &tmW, &full[s], kb * BK, mt * BM);
                 tma_load_2d(B, &tmX, &full[s], kb * BK, p0);
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps pe
                 tma_load_3d(B, &tmX, &full[s], 0, p0, kb);
               }
             } else {
-              mbar_expect_tx(&full[s], (uint32_t)a.kbs * kTileA + (uint32_t)nk * T::kTileB1);
+              mbar_expect_tx(&full[s], (uint32_t)a.kbs * a.wbytes + (uint32_t)nk * T::kTileB1);
               if (a.kbs == 1)
                 tma_load_3d(A, &tmW, &full[s], kb * BK, mt * BM, tap);
               else  // view {64, Cout, tap, k-block}
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)  // 168 registers: 3 warps pe
 #pragma unroll
           for (int j = 0; j < KBS; ++j) {
             if (j >= nk) break;
-            const uint32_t A = A0 + j * kTileA, B = B0 + j * T::kTileB1;
+            const uint32_t A = A0 + j * a.wbytes, B = B0 + j * T::kTileB1;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               // A: K-major rows of 128 B, 8-row atoms 1024 B apart; K step = 32 B in the
@@ -1087,6 +1091,7 @@ struct Geo {
   int ksize, stride, pad;
   int64_t Ho, Wo;
   int tbn, tilesP, mtiles, kblocks;
+  int wrows;  // rows of a W box: 64 when Cout <= 64 (half the W bytes per stage), else BM
   bool pair;  // cta_group::2 over adjacent channel tiles (mtiles even)
   int64_t tiles;
   int kbs, kst;              // k-blocks per ring stage; stages per tap
@@ -1107,7 +1112,7 @@ int plan_kbs(const Geo& g, int tbn, bool pair) {
 double stage_clocks(const Geo& g, int tbn, bool pair, int kbs) {
   const int pix = pair ? tbn / 2 : tbn;
   const int ntma = g.mode == kNCHW1 ? 1 + pix / 64 : (g.mode == kNHWC1 ? 2 : 1 + kbs);
-  const double bytes = (double)kbs * (16384.0 + 128.0 * pix);
+  const double bytes = (double)kbs * (128.0 * g.wrows + 128.0 * pix);
   return std::max({450.0 + 60.0 * ntma, bytes / 77.0, 2.0 * tbn * kbs});
 }
 
@@ -1181,6 +1186,15 @@ void plan_tiles(Geo& g) {
   g.kst = (g.kblocks + g.kbs - 1) / g.kbs;
 }
 
+// CGBN_CONV_WROWS=128 keeps 128-row W boxes for Cout <= 64 (read once; experiments only).
+int forced_wrows() {
+  static const int v = [] {
+    const char* e = getenv("CGBN_CONV_WROWS");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 // CGBN_CONV_SPLITS=n pins the split-K factor (read once; experiments only).
 int forced_splits() {
   static const int v = [] {
@@ -1243,6 +1257,7 @@ Geo make_geo(int mode, int64_t N, int64_t Cin, int64_t Cout, int64_t H, int64_t 
   g.M = N * g.Ho * g.Wo;
   g.mtiles = (int)((Cout + BM - 1) / BM);
   g.kblocks = (int)((Cin + BK - 1) / BK);
+  g.wrows = Cout <= 64 && forced_wrows() != 128 ? 64 : BM;
   plan_tiles(g);
   plan_splits(g, allow_split);
   return g;
@@ -1304,24 +1319,24 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
       const int64_t taps = g.ksize * g.ksize;
       const cuuint64_t wd[4] = {64, (cuuint64_t)g.Cout, (cuuint64_t)taps, nkb};
       const cuuint64_t ws[3] = {(cuuint64_t)(taps * g.Cin * 2), (cuuint64_t)g.Cin * 2, 128};
-      const cuuint32_t wb[4] = {BK, BM, 1, 2};
+      const cuuint32_t wb[4] = {BK, (cuuint32_t)g.wrows, 1, 2};
       if (int rc = make_map(&tmW, bf, 4, w, wd, ws, wb, "w")) return rc;
     } else {  // w[Cout][Cin]: {64, Cout, kb}
       const cuuint64_t wd[3] = {64, (cuuint64_t)g.Cout, nkb};
       const cuuint64_t ws[2] = {(cuuint64_t)g.Cin * 2, 128};
-      const cuuint32_t wb[3] = {BK, BM, 2};
+      const cuuint32_t wb[3] = {BK, (cuuint32_t)g.wrows, 2};
       if (int rc = make_map(&tmW, bf, 3, w, wd, ws, wb, "w")) return rc;
     }
   } else if constexpr (MODE == kNHWC3) {  // w[Cout][tap][Cin] (OHWI): dims {Cin, Cout, tap}
     const int64_t taps = g.ksize * g.ksize;
     const cuuint64_t wd[3] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout, (cuuint64_t)taps};
     const cuuint64_t ws[2] = {(cuuint64_t)(taps * g.Cin * 2), (cuuint64_t)g.Cin * 2};
-    const cuuint32_t wb[3] = {BK, BM, 1};
+    const cuuint32_t wb[3] = {BK, (cuuint32_t)g.wrows, 1};
     if (int rc = make_map(&tmW, bf, 3, w, wd, ws, wb, "w")) return rc;
   } else {  // w[Cout][Cin]
     const cuuint64_t wd[2] = {(cuuint64_t)g.Cin, (cuuint64_t)g.Cout};
     const cuuint64_t ws[1] = {(cuuint64_t)g.Cin * 2};
-    const cuuint32_t wb[2] = {BK, BM};
+    const cuuint32_t wb[2] = {BK, (cuuint32_t)g.wrows};
     if (int rc = make_map(&tmW, bf, 2, w, wd, ws, wb, "w")) return rc;
   }
   if constexpr (MODE == kNCHW1) {
@@ -1380,6 +1395,7 @@ int launch_conv(const void* x, const void* w, const float* bias, const Geo& g, v
   a.ksteps = g.ksteps;
   a.kbs = g.kbs;
   a.kst = g.kst;
+  a.wbytes = (uint32_t)g.wrows * BK * 2;
   a.units = (int)g.units;
   a.tickets = tickets;
   a.part = part;

@@ -3,7 +3,7 @@
 the BN statistics epilogue) next to cuDNN's conv (torch conv2d, bf16 out), CUDA-graph
 timed over rotating input sets (no L2 reuse between launches). One JSON line per layer.
 
-    python tools/conv_lab.py [--layers all|3x3|small] [--sets 3] [--iters 20]
+    python tools/conv_lab.py [--layers all|3x3|small|c64] [--sets 3] [--iters 20]
 """
 import argparse
 import json
@@ -53,6 +53,8 @@ def main():
         layers = [L for L in layers if L[0] == 3]
     elif a.layers == "small":
         layers = [L for L in layers if L[4] <= 14]
+    elif a.layers == "c64":
+        layers = [L for L in layers if L[3] <= 64]
     tot = {"ours": 0.0, "ours_stats": 0.0, "cudnn": 0.0}
     for k, sd, cin, cout, h, w, cnt in layers:
         xs = [torch.randn(a.batch, cin, h, w, device=dev).to(torch.bfloat16).contiguous(
