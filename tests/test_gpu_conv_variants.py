@@ -1,5 +1,5 @@
 """The producer conv's pinned variants (cgbn_conv.cu): 128- / 256-pixel tiles, split-K
-ranges, cta_group::2 CTA pairs. The per-layer plan picks among them, so one process sees
+ranges, cta_group::2 CTA pairs, 64- / 128-row weight boxes for Cout <= 64. The per-layer plan picks among them, so one process sees
 only the planned ones; each variant here runs the producer parity tests
 (tests/test_gpu_producer.py: z against an fp64 reference, the fused partial against the
 oracle's statistics of z as stored, the fused BN forward / backward against the oracle)
@@ -23,6 +23,7 @@ VARIANTS = [
     {"CGBN_CONV_TBN": "128", "CGBN_CONV_SPLITS": "3"},
     {"CGBN_CONV_PAIR": "1"},
     {"CGBN_CONV_PAIR": "1", "CGBN_CONV_TBN": "256"},
+    {"CGBN_CONV_WROWS": "128"},  # 128-row weight boxes also for Cout <= 64
 ]
 
 
